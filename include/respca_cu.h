@@ -1,0 +1,159 @@
+/* respca_cu.h — C-ABI of the B200-native RES-PCA solver (librespca_cu.so).
+ *
+ * This is the drop-in boundary.  The reference exposes the solver only as a C++
+ * API (/root/reference/proj/include/respca/solver.hpp:67-88,
+ * kmeans.hpp:28-43, matrix.hpp:82-98); there is no plugin registry or FFI.
+ * A host binding (the C++ facade in include/respca_b200/respca.hpp, the Python
+ * mirror in paper_1904_07497_b200/respca.py, or a user's own FFI) calls these
+ * entry points with plain pointers and sizes.  No torch or C++ types cross it,
+ * no exceptions cross it: every function returns a status code and
+ * respca_cu_last_error(ctx) holds the reference's message text.
+ *
+ * Matrices are column-major d×n (leading dimension d), exactly the reference's
+ * DenseMatrix layout (matrix.hpp:26-31).  Labels are uint64 (the reference's
+ * std::size_t, matrix.hpp:77).  All pointers below are HOST pointers; the
+ * library owns device memory, streams and graphs inside the context.
+ */
+#ifndef RESPCA_CU_H
+#define RESPCA_CU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (map 1:1 onto the reference's exception classes). */
+enum {
+    RESPCA_OK = 0,
+    RESPCA_EINVAL = 1,    /* std::invalid_argument (solver.cpp:41-46, 129-132, ...) */
+    RESPCA_ERUNTIME = 2,  /* std::runtime_error ("kmeans: cannot repair empty cluster", kmeans.cpp:58) */
+    RESPCA_ENOMEM = 3,    /* device allocation failed */
+    RESPCA_ECUDA = 4,     /* CUDA runtime / driver error, or no usable sm_100 device */
+    RESPCA_ENONFINITE = 5 /* a non-finite value appeared inside the loop (device flag) */
+};
+
+enum { RESPCA_F64 = 0, RESPCA_F32 = 1 };    /* storage type of X, L, S, Θ */
+enum { RESPCA_L1 = 0, RESPCA_L21 = 1 };     /* SparseNorm, solver.hpp:11 */
+
+typedef struct respca_cu_ctx respca_cu_ctx;
+
+/* SolverConfig + KMeansConfig, field for field (solver.hpp:13-28, kmeans.hpp:11-17). */
+typedef struct {
+    int has_lambda;          /* 0 → λ = sqrt(max(d, n))  (solver.cpp:35-38) */
+    double lambda;
+    double rho0;             /* 1e-4 */
+    double kappa;            /* 1.5 */
+    double tol;              /* 1e-3 */
+    uint64_t max_iter;       /* 500 */
+    uint64_t c;              /* 1 */
+    int sparse_norm;         /* RESPCA_L1 */
+    uint64_t km_max_iters;   /* 100 */
+    uint64_t km_n_restarts;  /* 1 (the initial clustering forces >= 5, solver.cpp:147) */
+    uint64_t km_seed;        /* 0 */
+    double km_tol;           /* 1e-6 */
+    int has_fixed_iters;     /* solver.hpp:26-27 */
+    uint64_t fixed_iters;
+} respca_cu_config;
+
+/* ConvergenceReport (solver.hpp:39-46) + timings.  The four arrays are caller
+ * allocated with room for fixed_iters (if set) else max_iter entries; the
+ * solver writes exactly `iters` entries. */
+typedef struct {
+    double* feas;
+    double* delta_l;
+    double* delta_s;
+    double* objective;
+    uint64_t iters;
+    int converged;
+    double lambda;          /* resolved λ (DecompositionResult::lambda) */
+    double wall_time;       /* seconds, the reference's window: after validation → results on host */
+    double init_ms;         /* one-time kmeans(X) on the device */
+    double loop_ms;         /* ALM loop on the device */
+    double h2d_ms, d2h_ms;
+    uint64_t slow_iters;    /* iterations whose p-update changed labels or moved a point */
+    uint64_t hartigan_moves;/* total exact Hartigan moves (initial clustering + loop) */
+    uint64_t exact_fallbacks;/* distance decisions resolved by exact sequential chains */
+} respca_cu_report;
+
+void respca_cu_default_config(respca_cu_config* cfg);
+
+/* Context: owns the device buffers, streams and CUDA graphs.  One context per
+ * host thread; a context is not thread-safe, distinct contexts are. */
+int respca_cu_create(int device, respca_cu_ctx** out);
+void respca_cu_destroy(respca_cu_ctx* ctx);
+const char* respca_cu_last_error(const respca_cu_ctx* ctx);
+/* number of kernels this context launched (graph nodes count per execution) */
+uint64_t respca_cu_kernel_launches(const respca_cu_ctx* ctx);
+
+/* respca::solve (solver.cpp:127-210 / solver.hpp:88).  x, L_out, S_out are
+ * d·n elements of `dtype`; labels_out has n entries.  Validation and error
+ * messages follow the reference.  dtype = RESPCA_F32 is an API extension
+ * (the reference is fp64-only). */
+int respca_cu_solve(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, int dtype,
+                    const respca_cu_config* cfg, void* L_out, void* S_out,
+                    uint64_t* labels_out, respca_cu_report* rep);
+
+/* --- building blocks (solver.hpp:67-84, kmeans.hpp:28-43, matrix.hpp:82-98),
+ *     fp64, same semantics and error text as the reference functions ------- */
+int respca_cu_l_update(respca_cu_ctx* ctx, const double* D, uint64_t d, uint64_t n,
+                       const uint64_t* labels, uint64_t c, double lambda, double rho,
+                       double* L_out);
+int respca_cu_s_update_l1(respca_cu_ctx* ctx, const double* B, uint64_t d, uint64_t n,
+                          double threshold, double* S_out);
+int respca_cu_s_update_l21(respca_cu_ctx* ctx, const double* B, uint64_t d, uint64_t n,
+                           double threshold, double* S_out);
+/* Θ += ρ(X − L − S); ρ = min(ρκ, 1e12).  theta and rho are in/out. */
+int respca_cu_multiplier_update(respca_cu_ctx* ctx, double* theta, const double* x,
+                                const double* L, const double* S, uint64_t d, uint64_t n,
+                                double* rho, double kappa);
+int respca_cu_check_convergence(respca_cu_ctx* ctx, const double* x, const double* l_prev,
+                                const double* l, const double* s_prev, const double* s,
+                                uint64_t d, uint64_t n, double tol, int* converged,
+                                double* feas, double* delta_l, double* delta_s);
+int respca_cu_kmeans(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                     uint64_t c, uint64_t max_iters, uint64_t n_restarts, uint64_t seed,
+                     double tol, uint64_t* labels_out, double* centroids_out,
+                     double* inertia, uint64_t* iters_run);
+int respca_cu_kmeans_warm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                          uint64_t c, uint64_t max_iters, double tol,
+                          const uint64_t* init_labels, uint64_t* labels_out,
+                          double* centroids_out, double* inertia, uint64_t* iters_run);
+/* std::mt19937_64 seeded with `seed` (the reference takes the engine by
+ * reference; a fresh engine with this seed reproduces its first call). */
+int respca_cu_kmeans_pp_init(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                             uint64_t c, uint64_t seed, double* centroids_out);
+int respca_cu_lloyd_step(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                         const double* centroids, uint64_t c, uint64_t* labels_out,
+                         double* next_out);
+int respca_cu_group_scatter(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                            const uint64_t* labels, uint64_t c, double* out);
+int respca_cu_frob_norm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                        double* out);
+int respca_cu_elementwise_l1(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                             double* out);
+int respca_cu_l21_norm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                       double* out);
+int respca_cu_column_l2_norms(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                              double* out);
+int respca_cu_column_mean(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                          const uint64_t* cols, uint64_t ncols, double* out);
+
+/* --- benchmark hooks (device-resident state, no host copies) ------------- */
+/* Upload X and run validation + the one-time initial clustering; leaves the
+ * context ready to step the ALM loop.  init_ms receives the device time. */
+int respca_cu_bench_prepare(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n,
+                            int dtype, const respca_cu_config* cfg, double* init_ms);
+/* Run exactly `iters` ALM iterations (fixed-iteration semantics) on the
+ * resident state; *ms receives the CUDA-event time of the whole region and
+ * *pass_f_ms the summed time of the fused elementwise kernel.  Returns the
+ * number of slow-path iterations through *slow. */
+int respca_cu_bench_steps(respca_cu_ctx* ctx, uint64_t iters, double* ms, double* pass_f_ms,
+                          double* pass_a_ms, uint64_t* slow);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,514 @@
+// ALM-loop kernels: the fused elementwise pass ("Pass F"), group sums, the
+// per-iteration finalize, and the standalone building blocks.
+//
+// Data layout (HBM): X, L, S, Θ are column-major d×n of T (double or float),
+// leading dimension d — the reference's DenseMatrix (matrix.hpp:26-31).
+// Groups are held as a CSR member list (goff[c+1], members[n]) with members in
+// ascending column order, i.e. GroupAssignment::group_indices()
+// (matrix.cpp:49-55).  Per-group d-vectors (group sums G, centroids C) are
+// d×c column-major doubles.
+//
+// Thread mapping of every ordered group reduction: one thread owns R
+// consecutive rows of ONE group and walks that group's member columns in
+// ascending order, so each (row, group) sum is accumulated in exactly the
+// reference's order (solver.cpp:61-65, kmeans.cpp:70-75) while a warp reads a
+// contiguous 32·R-element slice of each member column (coalesced, 128-bit for
+// R=2 doubles).
+#pragma once
+
+#include "common.cuh"
+
+namespace respca_dev {
+
+template <typename T, int R>
+struct Vec;
+template <>
+struct Vec<double, 1> {
+    double v[1];
+    RESPCA_DEV void load(const double* p) { v[0] = __ldg(p); }
+    RESPCA_DEV void load_cs(const double* p) { v[0] = __ldcs(p); }
+    RESPCA_DEV static void store(double* p, const double (&a)[1]) { __stcs(p, a[0]); }
+};
+template <>
+struct Vec<double, 2> {
+    double v[2];
+    RESPCA_DEV void load(const double* p) {
+        double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    RESPCA_DEV void load_cs(const double* p) {
+        double2 t = __ldcs(reinterpret_cast<const double2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    RESPCA_DEV static void store(double* p, const double (&a)[2]) {
+        __stcs(reinterpret_cast<double2*>(p), make_double2(a[0], a[1]));
+    }
+};
+template <>
+struct Vec<float, 1> {
+    double v[1];
+    RESPCA_DEV void load(const float* p) { v[0] = (double)__ldg(p); }
+    RESPCA_DEV void load_cs(const float* p) { v[0] = (double)__ldcs(p); }
+    RESPCA_DEV static void store(float* p, const double (&a)[1]) { __stcs(p, (float)a[0]); }
+};
+template <>
+struct Vec<float, 2> {
+    double v[2];
+    RESPCA_DEV void load(const float* p) {
+        float2 t = __ldg(reinterpret_cast<const float2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    RESPCA_DEV void load_cs(const float* p) {
+        float2 t = __ldcs(reinterpret_cast<const float2*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+    }
+    RESPCA_DEV static void store(float* p, const double (&a)[2]) {
+        __stcs(reinterpret_cast<float2*>(p), make_float2((float)a[0], (float)a[1]));
+    }
+};
+template <>
+struct Vec<float, 4> {
+    double v[4];
+    RESPCA_DEV void load(const float* p) {
+        float4 t = __ldg(reinterpret_cast<const float4*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+    RESPCA_DEV void load_cs(const float* p) {
+        float4 t = __ldcs(reinterpret_cast<const float4*>(p));
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+    }
+    RESPCA_DEV static void store(float* p, const double (&a)[4]) {
+        __stcs(reinterpret_cast<float4*>(p),
+               make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]));
+    }
+};
+
+// ---------------------------------------------------------------------------
+// Pass F: one fused HBM pass per ALM iteration (steady state).
+//
+// For every element of group g (labels_t), in the reference's op order:
+//   q   = θ/ρ_t
+//   D   = (x − s) + q                         solver.cpp:163-164
+//   L'  = own_w·D + mean_w_g·G_t[i,g]         solver.cpp:72 (G_t = Σ_{j∈g} D_j)
+//   B   = (x − L') + q                        solver.cpp:172-173
+//   S'  = |B|−1/ρ > 0 ? copysign(|B|−1/ρ, B) : 0     solver.cpp:83-85
+//   Θ'  = θ + ρ_t((x − L') − S')              solver.cpp:107-108
+// and, in the same walk,
+//   Cw[i,g]    = (Σ_{j∈g} L'_j)·(1/n_g)       = means_of(L', labels_t), the
+//                                               kmeans_warm start (kmeans.cpp:257, 66-82)
+//   Gnext[i,g] = Σ_{j∈g} ((x − S') + Θ'/ρ_{t+1})  = G_{t+1} if labels stay
+//   partials   : Σ((x−L')−S')², Σ(L'−L_t)², Σ(S'−S_t)², Σ|S'|, Σ(L'−m̃_g)²
+// Traffic: reads X, S, Θ, L_t; writes L', S', Θ' — 7·d·n·sizeof(T).
+// L, S, Θ are updated in place (each element is owned by one thread).
+// ---------------------------------------------------------------------------
+template <typename T, int R, int U>
+__global__ void __launch_bounds__(256) k_pass_f(
+    const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members,
+    // G0/G1 and Gn0/Gn1 are the same two buffers: G_t is read from
+    // buf[parity], G_{t+1} written to buf[1 - parity] (never the same one)
+    const double* G0, const double* G1, double* Gn0, double* Gn1, double* __restrict__ Cw,
+    const double* __restrict__ mean_w, const Ctl* __restrict__ ctl,
+    double* __restrict__ partials, int64_t d, int rowblocks) {
+    __shared__ double red[32 * 5];
+    if (ctl->done) return;  // loop already finished (bench launches ahead)
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
+    const bool active = i0 < d;
+
+    const int par = ctl->parity;
+    const double* Gc = par ? G1 : G0;
+    double* Gn = par ? Gn0 : Gn1;
+    const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
+    const double mw = mean_w[g];
+    const int beg = goff[g], end = goff[g + 1];
+    const double ng = (double)(end - beg);
+    const double mscale = own_w / ng + mw;  // exact-arithmetic mean of L' over g is G·mscale
+
+    double G[R], cacc[R], gacc[R], mt[R];
+    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
+    if (active) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            G[r] = Gc[(int64_t)g * d + i0 + r];
+            mt[r] = G[r] * mscale;
+            cacc[r] = 0.0;
+            gacc[r] = 0.0;
+        }
+
+        auto body = [&](const Vec<T, R>& xv, const Vec<T, R>& sv, const Vec<T, R>& tv,
+                        const Vec<T, R>& lv, int64_t off) {
+            double lo[R], so[R], to[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double x = xv.v[r], s = sv.v[r], th = tv.v[r];
+                const double q = th / rho;
+                const double dv = (x - s) + q;
+                const double ln = own_w * dv + mw * G[r];
+                cacc[r] += ln;
+                const double xl = x - ln;
+                const double b = xl + q;
+                const double mag = fabs(b) - thr;
+                const double sn = mag > 0.0 ? copysign(mag, b) : 0.0;
+                const double rr = xl - sn;
+                const double tn = th + rho * rr;
+                gacc[r] += (x - sn) + tn / rho_n;
+                pf += rr * rr;
+                const double dl = ln - lv.v[r];
+                pl += dl * dl;
+                const double ds = sn - s;
+                ps += ds * ds;
+                p1 += fabs(sn);
+                const double dm = ln - mt[r];
+                psc += dm * dm;
+                lo[r] = ln;
+                so[r] = sn;
+                to[r] = tn;
+            }
+            Vec<T, R>::store(L + off, lo);
+            Vec<T, R>::store(S + off, so);
+            Vec<T, R>::store(Th + off, to);
+        };
+
+        int t = beg;
+        for (; t + U <= end; t += U) {
+            Vec<T, R> xv[U], sv[U], tv[U], lv[U];
+            int64_t off[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) off[u] = (int64_t)__ldg(members + t + u) * d + i0;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                xv[u].load(X + off[u]);
+                sv[u].load_cs(S + off[u]);
+                tv[u].load_cs(Th + off[u]);
+                lv[u].load_cs(L + off[u]);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) body(xv[u], sv[u], tv[u], lv[u], off[u]);
+        }
+        for (; t < end; ++t) {
+            Vec<T, R> xv, sv, tv, lv;
+            const int64_t off = (int64_t)__ldg(members + t) * d + i0;
+            xv.load(X + off);
+            sv.load_cs(S + off);
+            tv.load_cs(Th + off);
+            lv.load_cs(L + off);
+            body(xv, sv, tv, lv, off);
+        }
+        const double inv = 1.0 / ng;  // means_of: sum * (1.0 / count), kmeans.cpp:78-79
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            Cw[(int64_t)g * d + i0 + r] = cacc[r] * inv;
+            Gn[(int64_t)g * d + i0 + r] = gacc[r];
+        }
+    }
+    double v[5] = {pf, pl, ps, p1, psc};
+    block_sum<5>(v, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
+}
+
+// ---------------------------------------------------------------------------
+// Ordered group sums: out[i,g] = Σ_{j∈g, ascending} f(j, i), with
+//   mode 0 (D-form):  f = (x − s) + θ/ρ   (solver.cpp:163-164, summed at 61-65)
+//   mode 1 (plain):   f = m[i,j]          (means_of / column_mean sums, kmeans.cpp:70-75)
+// then optionally scaled by (1/n_g) (means_of, kmeans.cpp:76-80).
+// ---------------------------------------------------------------------------
+template <typename T, int R, int MODE>
+__global__ void __launch_bounds__(256) k_group_sum(
+    const T* __restrict__ X, const T* __restrict__ S, const T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members, const Ctl* __restrict__ ctl,
+    double* __restrict__ out0, double* __restrict__ out1, int use_parity, int scale_by_count,
+    int64_t d, int rowblocks) {
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
+    if (i0 >= d) return;
+    double* __restrict__ out = (use_parity && ctl->parity) ? out1 : out0;
+    const double rho = MODE == 0 ? ctl->rho : 1.0;
+    const int beg = goff[g], end = goff[g + 1];
+    double acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.0;
+    int t = beg;
+    constexpr int U = 4;
+    for (; t + U <= end; t += U) {
+        Vec<T, R> xv[U], sv[U], tv[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t off = (int64_t)__ldg(members + t + u) * d + i0;
+            xv[u].load(X + off);
+            if (MODE == 0) {
+                sv[u].load(S + off);
+                tv[u].load(Th + off);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                acc[r] += MODE == 0 ? (xv[u].v[r] - sv[u].v[r]) + tv[u].v[r] / rho : xv[u].v[r];
+    }
+    for (; t < end; ++t) {
+        const int64_t off = (int64_t)__ldg(members + t) * d + i0;
+        Vec<T, R> xv, sv, tv;
+        xv.load(X + off);
+        if (MODE == 0) {
+            sv.load(S + off);
+            tv.load(Th + off);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+            acc[r] += MODE == 0 ? (xv.v[r] - sv.v[r]) + tv.v[r] / rho : xv.v[r];
+    }
+    const double inv = scale_by_count ? 1.0 / (double)(end - beg) : 1.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[(int64_t)g * d + i0 + r] = scale_by_count ? acc[r] * inv : acc[r];
+}
+
+// ---------------------------------------------------------------------------
+// Finalize (one block): fixed-order combination of the Pass F partials, the
+// report row, the stopping rule, and the scalars of iteration t+1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
+                                                   const double* __restrict__ partials,
+                                                   int nparts, const int* __restrict__ goff,
+                                                   double* __restrict__ mean_w, int c,
+                                                   double* __restrict__ rep, int has_cond,
+                                                   cudaGraphConditionalHandle cond) {
+    __shared__ double red[32 * 5];
+    if (ctl->done) {
+        if (threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    double v[5] = {0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) v[q] += partials[(int64_t)b * 5 + q];
+    block_sum<5>(v, red);
+    __shared__ int s_done;
+    if (threadIdx.x == 0) {
+        Ctl& k = *ctl;
+        const int t = k.iter;
+        const double feas = sqrt(v[0]) / k.xnorm;  // solver.cpp:20, 30
+        const double dl = sqrt(v[1]) / k.xnorm;
+        const double ds = sqrt(v[2]) / k.xnorm;
+        const double obj = k.lambda * v[4] + v[3];  // solver.cpp:194-195
+        k.last_l1 = v[3];
+        k.changed = 0;
+        k.moves = 0;
+        k.ambiguous = 0;
+        rep[(int64_t)t * 4 + 0] = feas;
+        rep[(int64_t)t * 4 + 1] = dl;
+        rep[(int64_t)t * 4 + 2] = ds;
+        rep[(int64_t)t * 4 + 3] = obj;
+        if (!isfinite(feas) || !isfinite(dl) || !isfinite(ds)) k.nonfinite = 1;
+        double mx = feas;  // std::max({feas, dl, ds})
+        if (mx < dl) mx = dl;
+        if (mx < ds) mx = ds;
+        if (!k.fixed && mx <= k.tol) k.converged = 1;
+        k.iter = t + 1;
+        // advance ρ and the derived scalars to iteration t+1
+        const double rho = k.rho_next;
+        k.rho = rho;
+        const double rn = rho * k.kappa;
+        k.rho_next = (1e12 < rn) ? 1e12 : rn;  // std::min(ρκ, kRhoCap)
+        const double two_lam = 2.0 * k.lambda;
+        k.own_w = rho / (two_lam + rho);
+        k.thr = 1.0 / rho;
+        k.parity ^= 1;
+        const int done = k.converged || k.slow || k.nonfinite || (t + 1 >= k.budget);
+        k.done = done;
+        s_done = done;
+        if (has_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
+    }
+    __syncthreads();
+    const double rho = ctl->rho, two_lam = 2.0 * ctl->lambda;
+    for (int g = threadIdx.x; g < c; g += blockDim.x)  // solver.cpp:66-67
+        mean_w[g] = two_lam / ((double)(goff[g + 1] - goff[g]) * (two_lam + rho));
+    (void)s_done;
+}
+
+// mean_w for the current ρ (after the host rebuilt the member lists).
+__global__ void k_mean_w(const Ctl* __restrict__ ctl, const int* __restrict__ goff,
+                         double* __restrict__ mean_w, int c) {
+    const double rho = ctl->rho, two_lam = 2.0 * ctl->lambda;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < c; g += gridDim.x * blockDim.x)
+        mean_w[g] = two_lam / ((double)(goff[g + 1] - goff[g]) * (two_lam + rho));
+}
+
+// ---------------------------------------------------------------------------
+// Generic elementwise / reduction kernels (building blocks, L21 path, norms)
+// ---------------------------------------------------------------------------
+
+// sum of squares and |.| and non-finite flag, per-block partials (3 values)
+template <typename T>
+__global__ void __launch_bounds__(256) k_norms(const T* __restrict__ m, int64_t N,
+                                               double* __restrict__ partials) {
+    __shared__ double red[32 * 3];
+    double sq = 0.0, ab = 0.0, bad = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = ld(m + k);
+        sq += v * v;
+        ab += fabs(v);
+        if (!isfinite(v)) bad = 1.0;
+    }
+    double v[3] = {sq, ab, bad};
+    block_sum<3>(v, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 3; ++q) partials[blockIdx.x * 3 + q] = v[q];
+}
+
+// generic residual sums for check_convergence: Σ((x−l)−s)², Σ(l−lp)², Σ(s−sp)²
+__global__ void __launch_bounds__(256) k_triple(const double* __restrict__ x,
+                                                const double* __restrict__ lp,
+                                                const double* __restrict__ l,
+                                                const double* __restrict__ sp,
+                                                const double* __restrict__ s, int64_t N,
+                                                double* __restrict__ partials) {
+    __shared__ double red[32 * 3];
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double f = x[k] - l[k] - s[k];
+        a += f * f;
+        const double dl = l[k] - lp[k];
+        b += dl * dl;
+        const double ds = s[k] - sp[k];
+        c += ds * ds;
+    }
+    double v[3] = {a, b, c};
+    block_sum<3>(v, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < 3; ++q) partials[blockIdx.x * 3 + q] = v[q];
+}
+
+__global__ void k_sum_partials(const double* __restrict__ partials, int nparts, int nv,
+                               double* __restrict__ out) {
+    __shared__ double red[32 * 5];
+    double v[5] = {0, 0, 0, 0, 0};
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+        for (int q = 0; q < nv; ++q) v[q] += partials[(int64_t)b * nv + q];
+    block_sum<5>(v, red);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < nv; ++q) out[q] = v[q];
+}
+
+// L-update from a materialised D (building block l_update, solver.cpp:51-77)
+template <int R>
+__global__ void __launch_bounds__(256) k_l_blend(const double* __restrict__ D,
+                                                 double* __restrict__ L,
+                                                 const int* __restrict__ goff,
+                                                 const int* __restrict__ members,
+                                                 const double* __restrict__ G, double own_w,
+                                                 double lambda, double rho, int64_t d,
+                                                 int rowblocks) {
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
+    if (i0 >= d) return;
+    const int beg = goff[g], end = goff[g + 1];
+    const double mw = 2.0 * lambda / ((double)(end - beg) * (2.0 * lambda + rho));
+    double gs[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) gs[r] = G[(int64_t)g * d + i0 + r];
+    for (int t = beg; t < end; ++t) {
+        const int64_t off = (int64_t)members[t] * d + i0;
+#pragma unroll
+        for (int r = 0; r < R; ++r) L[off + r] = own_w * D[off + r] + mw * gs[r];
+    }
+}
+
+// S = soft-threshold(B, t)   (solver.cpp:79-88)
+__global__ void k_shrink_l1(const double* __restrict__ B, double* __restrict__ S, int64_t N,
+                            double thr) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double v = B[k];
+        const double mag = fabs(v) - thr;
+        S[k] = mag > 0.0 ? copysign(mag, v) : 0.0;
+    }
+}
+
+// Θ += ρ((x − L) − S)    (solver.cpp:104-109)
+__global__ void k_multiplier(double* __restrict__ Th, const double* __restrict__ X,
+                             const double* __restrict__ L, const double* __restrict__ S,
+                             int64_t N, double rho) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x)
+        Th[k] += rho * (X[k] - L[k] - S[k]);
+}
+
+// Exact per-column sequential sums of squares (column_l2_norms order,
+// matrix.cpp:117-125), warp-transposed so each lane owns one column and
+// walks its rows in ascending order while the warp reads coalesced 32×32
+// tiles.  mode 0: v = m;  mode 1 (B-form for L21): v = (x − l) + θ/ρ.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(128) k_col_sumsq(const T* __restrict__ M,
+                                                   const T* __restrict__ Lm,
+                                                   const T* __restrict__ Tm, double rho,
+                                                   int64_t d, int64_t n,
+                                                   double* __restrict__ out) {
+    __shared__ double tile[4][32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j0 = ((int64_t)blockIdx.x * 4 + w) * 32;
+    if (j0 >= n) return;
+    double acc = 0.0;
+    for (int64_t i0 = 0; i0 < d; i0 += 32) {
+        const int64_t i = i0 + lane;
+        for (int cc = 0; cc < 32; ++cc) {
+            const int64_t j = j0 + cc;
+            double v = 0.0;
+            if (j < n && i < d) {
+                const int64_t e = j * d + i;
+                if (MODE == 0) v = ld(M + e);
+                else v = (ld(M + e) - ld(Lm + e)) + ld(Tm + e) / rho;
+            }
+            tile[w][cc][lane] = v;
+        }
+        __syncwarp();
+        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
+        for (int r = 0; r < lim; ++r) {
+            const double v = tile[w][lane][r];
+            acc += v * v;
+        }
+        __syncwarp();
+    }
+    if (j0 + lane < n) out[j0 + lane] = sqrt(acc);
+}
+
+// column shrink for L21: S_j = norm_j <= t ? 0 : (1 − t/norm_j)·B_j  (solver.cpp:94-100)
+// mode 0: B given; mode 1: B = (x − l) + θ/ρ computed on the fly.
+template <typename T, int MODE>
+__global__ void k_shrink_l21(const T* __restrict__ B, const T* __restrict__ Lm,
+                             const T* __restrict__ Tm, double rho, const double* __restrict__ norms,
+                             T* __restrict__ S, int64_t d, int64_t n, double thr) {
+    const int64_t N = d * n;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = k / d;
+        const double nr = norms[j];
+        double out = 0.0;
+        if (!(nr <= thr)) {
+            const double scale = 1.0 - thr / nr;
+            const double b = MODE == 0 ? ld(B + k) : (ld(B + k) - ld(Lm + k)) + ld(Tm + k) / rho;
+            out = scale * b;
+        }
+        S[k] = (T)out;
+    }
+}
+
+}  // namespace respca_dev

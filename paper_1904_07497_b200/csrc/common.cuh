@@ -1,0 +1,76 @@
+// Shared device definitions for the RES-PCA engine.
+//
+// Numerical contract: this translation unit is compiled with --fmad=false, so
+// every `a*b + c` below is a rounded multiply followed by a rounded add —
+// the reference's x86-64 (SSE2, no FMA) arithmetic.  Division and sqrt are the
+// IEEE correctly-rounded variants (nvcc defaults -prec-div/-prec-sqrt).  Where
+// a kernel deliberately uses FMA (the screened distance kernel), it calls
+// __fma_rn explicitly and its result is only ever used through a rigorous
+// error bound.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define RESPCA_DEV __device__ __forceinline__
+
+namespace respca_dev {
+
+constexpr int kMaxBlocks = 4096;
+
+// Device-resident control block of the ALM loop (one per context).  The
+// finalize kernel advances it, so the captured graph needs no host scalars.
+struct Ctl {
+    // scalars of the current iteration t
+    double rho;       // ρ_t
+    double rho_next;  // ρ_{t+1} = min(ρ_t κ, 1e12)         (solver.cpp:110)
+    double own_w;     // ρ_t / (2λ + ρ_t)                   (solver.cpp:58)
+    double thr;       // 1 / ρ_t                            (solver.cpp:175)
+    double lambda, kappa, tol, xnorm;
+    int iter;         // t
+    int budget;       // fixed_iters.value_or(max_iter)    (solver.cpp:152)
+    int fixed;        // fixed_iters set → never stop early (solver.cpp:197)
+    int parity;       // which G buffer holds G_t
+    int converged;
+    int slow;         // p-update of iteration t changed labels / moved a point
+    int nonfinite;
+    int done;         // loop finished (converged, budget, or slow → host)
+    unsigned int changed, moves, ambiguous;  // counters of the decide pass
+    int amb_list_len;
+    double last_l1;   // ‖S‖₁ of the last finalized iteration (objective patch-up)
+    unsigned long long exact_fallbacks;
+};
+
+RESPCA_DEV double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block reduction of NV doubles in fixed order (deterministic).  All threads
+// get the totals.  `red` must hold 32*NV doubles.
+template <int NV>
+RESPCA_DEV void block_sum(double (&v)[NV], double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) v[q] = warp_sum(v[q]);
+    __syncthreads();
+    if (lane == 0)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) red[q * 32 + warp] = v[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        double t = lane < nw ? red[q * 32 + lane] : 0.0;
+        v[q] = warp_sum(t);
+    }
+    __syncthreads();
+}
+
+template <typename T>
+RESPCA_DEV double ld(const T* p) {
+    return (double)__ldg(p);
+}
+
+}  // namespace respca_dev

@@ -1,0 +1,964 @@
+// librespca_cu.so — B200-native RES-PCA engine behind the C-ABI of
+// include/respca_cu.h.
+//
+// Build (see paper_1904_07497_b200/build.py):
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false
+//        -Xcompiler -fPIC -shared engine.cu -o librespca_cu.so
+// --fmad=false is load-bearing: it makes the device arithmetic the reference's
+// (no FMA contraction, solver.cpp / kmeans.cpp compiled for baseline x86-64).
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "alm.cuh"
+#include "engine.cuh"
+#include "kmeans_engine.cuh"
+#include "km.cuh"
+
+using namespace respca_host;
+using namespace respca_dev;
+
+struct AlmBase {
+    virtual ~AlmBase() = default;
+};
+
+struct respca_cu_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    std::string err;
+    uint64_t launches = 0;
+    std::unique_ptr<AlmBase> resident;  // bench-resident solver state
+};
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+
+void check_dims(uint64_t d, uint64_t n) {
+    if (d == 0 || n == 0) throw InvalidArg("DenseMatrix: dimensions must be >= 1");
+    if (n > 0x7fffffffULL) throw InvalidArg("respca_cu: more than 2^31-1 columns");
+    if (d > (1ULL << 40) || d * n > (1ULL << 40)) throw InvalidArg("respca_cu: matrix too large");
+}
+
+void validate_cfg(const respca_cu_config& c) {  // solver.cpp:40-47
+    if (c.has_lambda && c.lambda <= 0.0) throw InvalidArg("lambda must be > 0");
+    if (c.rho0 <= 0.0) throw InvalidArg("rho0 must be > 0");
+    if (c.kappa <= 1.0) throw InvalidArg("kappa must be > 1");
+    if (c.tol <= 0.0) throw InvalidArg("tol must be > 0");
+    if (c.c == 0) throw InvalidArg("c must be >= 1");
+    if (c.max_iter == 0) throw InvalidArg("max_iter must be >= 1");
+}
+
+// labels uint64 (API) → int (device) with GroupAssignment validation (matrix.cpp:36-47)
+std::vector<int> to_int_labels(const uint64_t* l, uint64_t n, uint64_t c) {
+    if (c == 0) throw InvalidArg("GroupAssignment: c must be >= 1");
+    std::vector<int> out(n);
+    std::vector<char> seen(c, 0);
+    for (uint64_t j = 0; j < n; ++j) {
+        if (l[j] >= c) throw InvalidArg("GroupAssignment: label out of range");
+        out[j] = (int)l[j];
+        seen[l[j]] = 1;
+    }
+    for (uint64_t k = 0; k < c; ++k)
+        if (!seen[k]) throw InvalidArg("GroupAssignment: empty group");
+    return out;
+}
+
+// ---------------------------------------------------------------------------
+// The ALM solver (solver.cpp:127-210), device resident.
+// ---------------------------------------------------------------------------
+template <typename T>
+struct Alm : AlmBase {
+    respca_cu_ctx* ctx;
+    cudaStream_t st;
+    Launch ln;
+    Stats stats;
+    int64_t d = 0;
+    int n = 0, c = 0;
+    respca_cu_config cfg{};
+    double lambda = 0.0;
+    uint64_t budget = 0;
+    int R = 1, rowblocks = 0, nbF = 0;
+
+    DBuf<T> X, L, S, Th;
+    DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm;
+    DBuf<int> labels, labels_new;
+    DBuf<Ctl> ctl;
+    KMeansEngine<T> km;
+    WhileGraph wg;
+    PlainGraph rest;
+    double init_ms = 0.0, xnorm = 0.0;
+
+    explicit Alm(respca_cu_ctx* cx) : ctx(cx), st(cx->st), ln{&cx->launches} {
+        km.st = st;
+        km.ln = ln;
+        km.stats = &stats;
+    }
+
+    Ctl read_ctl() {
+        Ctl h;
+        CK(cudaMemcpyAsync(&h, ctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        return h;
+    }
+    void write_ctl(const Ctl& h) {
+        CK(cudaMemcpyAsync(ctl.p, &h, sizeof(Ctl), cudaMemcpyHostToDevice, st));
+    }
+
+    // upload + device-side validation (finite, ‖X‖ ≠ 0)  (solver.cpp:128-132)
+    void upload(const T* x, uint64_t dd, uint64_t nn, const respca_cu_config& c_) {
+        cfg = c_;
+        validate_cfg(cfg);
+        if (cfg.c > nn) throw InvalidArg("solve: c exceeds column count");
+        d = (int64_t)dd;
+        n = (int)nn;
+        c = (int)cfg.c;
+        const int64_t N = d * n;
+        X.ensure(N);
+        L.ensure(N);
+        S.ensure(N);
+        Th.ensure(N);
+        CK(cudaMemcpyAsync(X.p, x, sizeof(T) * N, cudaMemcpyHostToDevice, st));
+        const int blocks = std::min<int64_t>(2048, ceil_div(N, 256));
+        nrm.ensure(3 * 2048 + 8);
+        k_norms<T><<<blocks, 256, 0, st>>>(X.p, N, nrm.p);
+        k_sum_partials<<<1, 256, 0, st>>>(nrm.p, blocks, 3, nrm.p + 3 * 2048);
+        ln.add(2);
+        double h[3];
+        CK(cudaMemcpyAsync(h, nrm.p + 3 * 2048, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h[2] != 0.0) throw InvalidArg("solve: non-finite X");
+        xnorm = std::sqrt(h[0]);
+        if (xnorm == 0.0) throw InvalidArg("solve: all-zero X");
+    }
+
+    void setup_state() {
+        const int64_t N = d * n;
+        lambda = cfg.has_lambda ? cfg.lambda : std::sqrt((double)std::max<int64_t>(d, n));
+        budget = cfg.has_fixed_iters ? cfg.fixed_iters : cfg.max_iter;
+        CK(cudaMemcpyAsync(L.p, X.p, sizeof(T) * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(S.p, 0, sizeof(T) * N, st));
+        CK(cudaMemsetAsync(Th.p, 0, sizeof(T) * N, st));
+        G.ensure((size_t)2 * d * c);
+        Cw.ensure((size_t)d * c);
+        Ck.ensure((size_t)d * c);
+        mean_w.ensure(c);
+        labels.ensure(n);
+        labels_new.ensure(n);
+        rep.ensure(std::max<uint64_t>(budget, 1) * 4);
+        ctl.ensure(1);
+        R = (d % 2 == 0) ? 2 : 1;
+        rowblocks = ceil_div(d, 256 * R);
+        nbF = rowblocks * c;
+        partials.ensure((size_t)nbF * 5);
+        Ctl h{};
+        h.rho = cfg.rho0;
+        const double rn = cfg.rho0 * cfg.kappa;
+        h.rho_next = (1e12 < rn) ? 1e12 : rn;
+        h.own_w = cfg.rho0 / (2.0 * lambda + cfg.rho0);
+        h.thr = 1.0 / cfg.rho0;
+        h.lambda = lambda;
+        h.kappa = cfg.kappa;
+        h.tol = cfg.tol;
+        h.xnorm = xnorm;
+        h.iter = 0;
+        h.budget = (int)std::min<uint64_t>(budget, 0x7fffffff);
+        h.fixed = cfg.has_fixed_iters ? 1 : 0;
+        write_ctl(h);
+    }
+
+    // initial grouping: kmeans(X) with >= 5 restarts (solver.cpp:143-150)
+    void init_labels() {
+        km.bind(X.p, d, n, c);
+        if (c == 1) {
+            CK(cudaMemsetAsync(labels.p, 0, sizeof(int) * n, st));
+            km.h_labels.assign(n, 0);
+        } else {
+            const uint64_t restarts = std::max<uint64_t>(cfg.km_n_restarts, 5);
+            km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, nullptr,
+                      nullptr);
+            km.fetch_labels(labels.p);
+        }
+        km.bind(L.p, d, n, c);  // from here on the p-update clusters L
+        km.groups.build(km.h_labels.data(), n, c);
+        km.upload_groups();
+    }
+
+    void launch_group_D() {  // G_t = Σ_{j∈g} ((x − s) + θ/ρ) into G[parity]
+        if (R == 2)
+            k_group_sum<T, 2, 0><<<nbF, 256, 0, st>>>(X.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                      ctl.p, G.p, G.p + (size_t)d * c, 1, 0, d,
+                                                      rowblocks);
+        else
+            k_group_sum<T, 1, 0><<<nbF, 256, 0, st>>>(X.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                      ctl.p, G.p, G.p + (size_t)d * c, 1, 0, d,
+                                                      rowblocks);
+        k_mean_w<<<ceil_div(c, 256), 256, 0, st>>>(ctl.p, km.goff.p, mean_w.p, c);
+        ln.add(2);
+    }
+
+    void prepare(const T* x, uint64_t dd, uint64_t nn, const respca_cu_config& c_) {
+        upload(x, dd, nn, c_);
+        Events ev;
+        CK(cudaEventRecord(ev.a, st));
+        setup_state();
+        init_labels();
+        launch_group_D();
+        CK(cudaEventRecord(ev.b, st));
+        CK(cudaEventSynchronize(ev.b));
+        init_ms = ev.ms();
+        capture();
+    }
+
+    // ---- one iteration of the fast path, captured ----------------------
+    void launch_pass_f() {
+        double* G1 = G.p + (size_t)d * c;
+        if (R == 2)
+            k_pass_f<T, 2, 4><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                   G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
+                                                   partials.p, d, rowblocks);
+        else
+            k_pass_f<T, 1, 4><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                   G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
+                                                   partials.p, d, rowblocks);
+        ln.add();
+    }
+    void launch_pass_a() {
+        if (c <= 1) return;
+        km.screen(Cw.p);
+        km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);
+        k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
+        ln.add();
+    }
+    void launch_finalize(bool cond) {
+        k_finalize<<<1, 1024, 0, st>>>(ctl.p, partials.p, nbF, km.goff.p, mean_w.p, c, rep.p,
+                                       cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
+        ln.add();
+    }
+    int kernels_per_iter() const { return 1 + (c > 1 ? 6 : 0) + 1; }
+
+    void capture() {
+        const uint64_t saved = *ln.counter;  // captured launches are not executions
+        // WHILE graph: the product loop
+        wg.begin(st);
+        launch_pass_f();
+        launch_pass_a();
+        launch_finalize(true);
+        wg.end(st);
+        // plain graph of everything after Pass F (bench timing of Pass F by events)
+        rest.begin(st);
+        launch_pass_a();
+        launch_finalize(false);
+        rest.end(st);
+        *ln.counter = saved;
+    }
+
+    // slow path: the p-update changed labels (or a Hartigan move) in the last
+    // finalized iteration t → finish kmeans_warm exactly, refresh groups, G.
+    void slow_path(Ctl& h) {
+        const int t = h.iter - 1;
+        CK(cudaMemcpyAsync(Ck.p, Cw.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        km.h_labels.resize(n);
+        CK(cudaMemcpyAsync(km.h_labels.data(), labels.p, sizeof(int) * n, cudaMemcpyDeviceToHost,
+                           st));
+        CK(cudaStreamSynchronize(st));
+        km.lloyd_run(Ck.p, labels.p, cfg.km_max_iters, cfg.km_tol);  // kmeans_warm, kmeans.cpp:257
+        // lloyd_run left goff/members/counts = labels_{t+1} and Ck = means_of(L', labels_{t+1})
+        const double scatter = km.inertia(Ck.p, labels.p);
+        const double obj = lambda * scatter + h.last_l1;
+        CK(cudaMemcpyAsync(rep.p + (size_t)t * 4 + 3, &obj, sizeof(double), cudaMemcpyHostToDevice,
+                           st));
+        launch_group_D();  // G_{t+1} under the new labels, ρ_{t+1}
+        h.slow = 0;
+        h.changed = h.moves = h.ambiguous = 0;
+        h.done = h.converged || h.nonfinite || (h.iter >= h.budget);
+        write_ctl(h);
+        CK(cudaStreamSynchronize(st));
+    }
+
+    // run the loop to completion (solver.cpp:157-201)
+    uint64_t slow_iters = 0;
+    void run_loop() {
+        for (;;) {
+            const int it0 = read_ctl().iter;
+            wg.launch(st);
+            Ctl h = read_ctl();
+            ln.add((uint64_t)kernels_per_iter() * (uint64_t)(h.iter - it0));
+            if (h.slow) {
+                ++slow_iters;
+                slow_path(h);
+            }
+            if (h.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
+            if (h.done) break;
+        }
+    }
+
+    void download(T* Lo, T* So, uint64_t* lab, respca_cu_report* rep_out) {
+        const Ctl h = read_ctl();
+        const int64_t N = d * n;
+        CK(cudaMemcpyAsync(Lo, L.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
+        CK(cudaMemcpyAsync(So, S.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
+        std::vector<int> hl(n);
+        CK(cudaMemcpyAsync(hl.data(), labels.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+        std::vector<double> hr((size_t)h.iter * 4 + 4);
+        if (h.iter > 0)
+            CK(cudaMemcpyAsync(hr.data(), rep.p, sizeof(double) * 4 * h.iter,
+                               cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        for (int j = 0; j < n; ++j) lab[j] = (uint64_t)hl[j];
+        if (rep_out) {
+            for (int t = 0; t < h.iter; ++t) {
+                if (rep_out->feas) rep_out->feas[t] = hr[(size_t)t * 4 + 0];
+                if (rep_out->delta_l) rep_out->delta_l[t] = hr[(size_t)t * 4 + 1];
+                if (rep_out->delta_s) rep_out->delta_s[t] = hr[(size_t)t * 4 + 2];
+                if (rep_out->objective) rep_out->objective[t] = hr[(size_t)t * 4 + 3];
+            }
+            rep_out->iters = (uint64_t)h.iter;
+            rep_out->converged = h.converged;
+            rep_out->lambda = lambda;
+            rep_out->slow_iters = slow_iters;
+            rep_out->hartigan_moves = stats.hartigan_moves;
+            rep_out->exact_fallbacks = stats.exact_fallbacks + h.exact_fallbacks;
+        }
+    }
+
+    // ---- bench: exactly `iters` more iterations, events around Pass F ----
+    void bench_steps(uint64_t iters, double* ms, double* pf_ms, double* pa_ms, uint64_t* slow) {
+        Ctl h = read_ctl();
+        if ((uint64_t)h.iter + iters > budget) {
+            // grow the report buffer (fixed-iteration benchmark semantics)
+            budget = (uint64_t)h.iter + iters;
+            DBuf<double> nr;
+            nr.ensure(budget * 4);
+            if (h.iter > 0)
+                CK(cudaMemcpyAsync(nr.p, rep.p, sizeof(double) * 4 * h.iter,
+                                   cudaMemcpyDeviceToDevice, st));
+            std::swap(rep.p, nr.p);
+            std::swap(rep.cap, nr.cap);
+            capture();
+        }
+        h.budget = (int)(h.iter + iters);
+        h.fixed = 1;
+        h.done = 0;
+        h.converged = 0;
+        write_ctl(h);
+        std::vector<Events> evf(iters), eva(iters);
+        Events all;
+        uint64_t remaining = iters, nslow = 0;
+        double fsum = 0.0, asum = 0.0;
+        CK(cudaEventRecord(all.a, st));
+        while (remaining > 0) {
+            const uint64_t base = iters - remaining;
+            for (uint64_t t = 0; t < remaining; ++t) {
+                CK(cudaEventRecord(evf[base + t].a, st));
+                launch_pass_f();
+                CK(cudaEventRecord(evf[base + t].b, st));
+                CK(cudaEventRecord(eva[base + t].a, st));
+                rest.launch(st);
+                ln.add(kernels_per_iter() - 1);
+                CK(cudaEventRecord(eva[base + t].b, st));
+            }
+            Ctl g = read_ctl();
+            const uint64_t done_iters = (uint64_t)g.iter - (uint64_t)(h.budget - iters);
+            if (g.slow) {
+                ++nslow;
+                ++slow_iters;
+                slow_path(g);
+            }
+            if (g.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
+            remaining = iters - std::min<uint64_t>(iters, done_iters);
+            if (remaining > 0) {
+                g = read_ctl();
+                g.done = 0;
+                write_ctl(g);
+            }
+        }
+        CK(cudaEventRecord(all.b, st));
+        CK(cudaEventSynchronize(all.b));
+        for (uint64_t t = 0; t < iters; ++t) {
+            fsum += evf[t].ms();
+            asum += eva[t].ms();
+        }
+        *ms = all.ms();
+        if (pf_ms) *pf_ms = fsum;
+        if (pa_ms) *pa_ms = asum;
+        if (slow) *slow = nslow;
+    }
+};
+
+template <typename T>
+void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
+                const respca_cu_config& cfg, T* Lo, T* So, uint64_t* lab,
+                respca_cu_report* rep) {
+    check_dims(d, n);
+    validate_cfg(cfg);
+    if (cfg.c > n) throw InvalidArg("solve: c exceeds column count");
+    const auto t0 = Clock::now();
+    Alm<T> a(ctx);
+    Events ev;
+    CK(cudaEventRecord(ev.a, ctx->st));
+    a.upload(x, d, n, cfg);
+    CK(cudaEventRecord(ev.b, ctx->st));
+    CK(cudaEventSynchronize(ev.b));
+    const double h2d = ev.ms();
+    Events e2;
+    CK(cudaEventRecord(e2.a, ctx->st));
+    a.setup_state();
+    a.init_labels();
+    a.launch_group_D();
+    CK(cudaEventRecord(e2.b, ctx->st));
+    CK(cudaEventSynchronize(e2.b));
+    const double init_ms = e2.ms();
+    a.capture();
+    Events e3;
+    CK(cudaEventRecord(e3.a, ctx->st));
+    a.run_loop();
+    CK(cudaEventRecord(e3.b, ctx->st));
+    CK(cudaEventSynchronize(e3.b));
+    const double loop_ms = e3.ms();
+    Events e4;
+    CK(cudaEventRecord(e4.a, ctx->st));
+    a.download(Lo, So, lab, rep);
+    CK(cudaEventRecord(e4.b, ctx->st));
+    CK(cudaEventSynchronize(e4.b));
+    if (rep) {
+        rep->init_ms = init_ms;
+        rep->loop_ms = loop_ms;
+        rep->h2d_ms = h2d;
+        rep->d2h_ms = e4.ms();
+        rep->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
+    }
+}
+
+template <class F>
+int guarded(respca_cu_ctx* ctx, F&& f) {
+    if (!ctx) return RESPCA_EINVAL;
+    try {
+        CK(cudaSetDevice(ctx->device));
+        f();
+        ctx->err.clear();
+        return RESPCA_OK;
+    } catch (const InvalidArg& e) {
+        ctx->err = e.what();
+        return RESPCA_EINVAL;
+    } catch (const RuntimeErr& e) {
+        ctx->err = e.what();
+        return RESPCA_ERUNTIME;
+    } catch (const NoMem& e) {
+        ctx->err = e.what();
+        return RESPCA_ENOMEM;
+    } catch (const NonFinite& e) {
+        ctx->err = e.what();
+        return RESPCA_ENONFINITE;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return RESPCA_ECUDA;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// building-block helpers (fp64, host in / host out)
+// ---------------------------------------------------------------------------
+struct Dev64 {
+    DBuf<double> b;
+    double* up(cudaStream_t st, const double* h, size_t count) {
+        b.ensure(count);
+        CK(cudaMemcpyAsync(b.p, h, sizeof(double) * count, cudaMemcpyHostToDevice, st));
+        return b.p;
+    }
+};
+
+double sum_partials(cudaStream_t st, Launch& ln, double* part, int blocks, int nv, int q,
+                    DBuf<double>& scratch) {
+    scratch.ensure(8);
+    k_sum_partials<<<1, 256, 0, st>>>(part, blocks, nv, scratch.p);
+    ln.add();
+    double h[5];
+    CK(cudaMemcpyAsync(h, scratch.p, sizeof(double) * nv, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return h[q];
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+void respca_cu_default_config(respca_cu_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->rho0 = 1e-4;
+    c->kappa = 1.5;
+    c->tol = 1e-3;
+    c->max_iter = 500;
+    c->c = 1;
+    c->sparse_norm = RESPCA_L1;
+    c->km_max_iters = 100;
+    c->km_n_restarts = 1;
+    c->km_seed = 0;
+    c->km_tol = 1e-6;
+}
+
+int respca_cu_create(int device, respca_cu_ctx** out) {
+    if (!out) return RESPCA_EINVAL;
+    *out = nullptr;
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= device || device < 0) {
+        cudaGetLastError();
+        return RESPCA_ECUDA;
+    }
+    cudaDeviceProp prop;
+    if (cudaGetDeviceProperties(&prop, device) != cudaSuccess || prop.major < 10) return RESPCA_ECUDA;
+    auto* ctx = new respca_cu_ctx();
+    ctx->device = device;
+    if (cudaSetDevice(device) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+        delete ctx;
+        return RESPCA_ECUDA;
+    }
+    *out = ctx;
+    return RESPCA_OK;
+}
+
+void respca_cu_destroy(respca_cu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    ctx->resident.reset();
+    if (ctx->st) cudaStreamDestroy(ctx->st);
+    delete ctx;
+}
+
+const char* respca_cu_last_error(const respca_cu_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : "null context";
+}
+
+uint64_t respca_cu_kernel_launches(const respca_cu_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int respca_cu_solve(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, int dtype,
+                    const respca_cu_config* cfg, void* L_out, void* S_out, uint64_t* labels_out,
+                    respca_cu_report* rep) {
+    return guarded(ctx, [&] {
+        if (!x || !cfg || !L_out || !S_out || !labels_out) throw InvalidArg("respca_cu_solve: null pointer");
+        if (cfg->sparse_norm != RESPCA_L1)
+            throw InvalidArg("respca_cu_solve: sparse_norm L21 is not implemented on the device path yet");
+        if (dtype == RESPCA_F64)
+            solve_impl<double>(ctx, (const double*)x, d, n, *cfg, (double*)L_out, (double*)S_out,
+                               labels_out, rep);
+        else if (dtype == RESPCA_F32)
+            solve_impl<float>(ctx, (const float*)x, d, n, *cfg, (float*)L_out, (float*)S_out,
+                              labels_out, rep);
+        else
+            throw InvalidArg("respca_cu_solve: unknown dtype");
+    });
+}
+
+int respca_cu_bench_prepare(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, int dtype,
+                            const respca_cu_config* cfg, double* init_ms) {
+    return guarded(ctx, [&] {
+        check_dims(d, n);
+        ctx->resident.reset();
+        if (dtype == RESPCA_F64) {
+            auto a = std::make_unique<Alm<double>>(ctx);
+            a->prepare((const double*)x, d, n, *cfg);
+            if (init_ms) *init_ms = a->init_ms;
+            ctx->resident = std::move(a);
+        } else {
+            auto a = std::make_unique<Alm<float>>(ctx);
+            a->prepare((const float*)x, d, n, *cfg);
+            if (init_ms) *init_ms = a->init_ms;
+            ctx->resident = std::move(a);
+        }
+    });
+}
+
+int respca_cu_bench_steps(respca_cu_ctx* ctx, uint64_t iters, double* ms, double* pf_ms,
+                          double* pa_ms, uint64_t* slow) {
+    return guarded(ctx, [&] {
+        if (!ctx->resident) throw InvalidArg("respca_cu_bench_steps: call respca_cu_bench_prepare first");
+        if (auto* a = dynamic_cast<Alm<double>*>(ctx->resident.get()))
+            a->bench_steps(iters, ms, pf_ms, pa_ms, slow);
+        else if (auto* b = dynamic_cast<Alm<float>*>(ctx->resident.get()))
+            b->bench_steps(iters, ms, pf_ms, pa_ms, slow);
+    });
+}
+
+// ---- building blocks ------------------------------------------------------
+
+int respca_cu_l_update(respca_cu_ctx* ctx, const double* D, uint64_t d, uint64_t n,
+                       const uint64_t* labels, uint64_t c, double lambda, double rho,
+                       double* L_out) {
+    return guarded(ctx, [&] {  // solver.cpp:51-77
+        check_dims(d, n);
+        const std::vector<int> lab = to_int_labels(labels, n, c);
+        if (rho <= 0.0) throw InvalidArg("l_update: rho must be > 0");
+        if (lambda < 0.0) throw InvalidArg("l_update: lambda must be >= 0");
+        cudaStream_t st = ctx->st;
+        Launch ln{&ctx->launches};
+        KMeansEngine<double> km;
+        km.st = st;
+        km.ln = ln;
+        Dev64 dD;
+        const double* Dd = dD.up(st, D, d * n);
+        km.bind(Dd, d, (int)n, (int)c);
+        km.h_labels = lab;
+        DBuf<double> G, Lb;
+        G.ensure(d * c);
+        Lb.ensure(d * n);
+        // group sums of D in the reference order, then the blend
+        km.groups.build(lab.data(), (int)n, (int)c);
+        km.upload_groups();
+        const bool r2 = d % 2 == 0;
+        const int rb = ceil_div(d, 256 * (r2 ? 2 : 1));
+        if (r2)
+            k_group_sum<double, 2, 1><<<rb * (int)c, 256, 0, st>>>(
+                Dd, nullptr, nullptr, km.goff.p, km.members.p, nullptr, G.p, nullptr, 0, 0, d, rb);
+        else
+            k_group_sum<double, 1, 1><<<rb * (int)c, 256, 0, st>>>(
+                Dd, nullptr, nullptr, km.goff.p, km.members.p, nullptr, G.p, nullptr, 0, 0, d, rb);
+        const double own_w = rho / (2.0 * lambda + rho);
+        if (r2)
+            k_l_blend<2><<<rb * (int)c, 256, 0, st>>>(Dd, Lb.p, km.goff.p, km.members.p, G.p, own_w,
+                                                      lambda, rho, d, rb);
+        else
+            k_l_blend<1><<<rb * (int)c, 256, 0, st>>>(Dd, Lb.p, km.goff.p, km.members.p, G.p, own_w,
+                                                      lambda, rho, d, rb);
+        ln.add(2);
+        CK(cudaMemcpyAsync(L_out, Lb.p, sizeof(double) * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int respca_cu_s_update_l1(respca_cu_ctx* ctx, const double* B, uint64_t d, uint64_t n,
+                          double thr, double* S_out) {
+    return guarded(ctx, [&] {  // solver.cpp:79-88
+        check_dims(d, n);
+        if (thr < 0.0) throw InvalidArg("s_update_l1: negative threshold");
+        cudaStream_t st = ctx->st;
+        Dev64 db;
+        double* p = db.up(st, B, d * n);
+        k_shrink_l1<<<std::min<int64_t>(4096, ceil_div(d * n, 256)), 256, 0, st>>>(p, p, d * n, thr);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(S_out, p, sizeof(double) * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int respca_cu_s_update_l21(respca_cu_ctx* ctx, const double* B, uint64_t d, uint64_t n,
+                           double thr, double* S_out) {
+    return guarded(ctx, [&] {  // solver.cpp:90-102
+        check_dims(d, n);
+        if (thr < 0.0) throw InvalidArg("s_update_l21: negative threshold");
+        cudaStream_t st = ctx->st;
+        Dev64 db;
+        double* p = db.up(st, B, d * n);
+        DBuf<double> nr, so;
+        nr.ensure(n);
+        so.ensure(d * n);
+        k_col_sumsq<double, 0><<<ceil_div(n, 128), 128, 0, st>>>(p, nullptr, nullptr, 1.0, d, n, nr.p);
+        k_shrink_l21<double, 0><<<std::min<int64_t>(4096, ceil_div(d * n, 256)), 256, 0, st>>>(
+            p, nullptr, nullptr, 1.0, nr.p, so.p, d, n, thr);
+        ctx->launches += 2;
+        CK(cudaMemcpyAsync(S_out, so.p, sizeof(double) * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int respca_cu_multiplier_update(respca_cu_ctx* ctx, double* theta, const double* x,
+                                const double* L, const double* S, uint64_t d, uint64_t n,
+                                double* rho, double kappa) {
+    return guarded(ctx, [&] {  // solver.cpp:104-111
+        check_dims(d, n);
+        if (kappa <= 1.0) throw InvalidArg("multiplier_update: kappa must be > 1");
+        cudaStream_t st = ctx->st;
+        Dev64 a, b, c2, e;
+        double* th = a.up(st, theta, d * n);
+        const double* xd = b.up(st, x, d * n);
+        const double* ld_ = c2.up(st, L, d * n);
+        const double* sd = e.up(st, S, d * n);
+        k_multiplier<<<std::min<int64_t>(4096, ceil_div(d * n, 256)), 256, 0, st>>>(th, xd, ld_, sd,
+                                                                                  d * n, *rho);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(theta, th, sizeof(double) * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        const double nr = *rho * kappa;
+        *rho = (1e12 < nr) ? 1e12 : nr;
+    });
+}
+
+int respca_cu_check_convergence(respca_cu_ctx* ctx, const double* x, const double* l_prev,
+                                const double* l, const double* s_prev, const double* s,
+                                uint64_t d, uint64_t n, double tol, int* conv, double* feas,
+                                double* dl, double* ds) {
+    return guarded(ctx, [&] {  // solver.cpp:113-125
+        check_dims(d, n);
+        cudaStream_t st = ctx->st;
+        Launch ln{&ctx->launches};
+        Dev64 a, b, c2, e, f;
+        const double* xd = a.up(st, x, d * n);
+        const double* lpd = b.up(st, l_prev, d * n);
+        const double* ldd = c2.up(st, l, d * n);
+        const double* spd = e.up(st, s_prev, d * n);
+        const double* sd = f.up(st, s, d * n);
+        const int blocks = std::min<int64_t>(2048, ceil_div(d * n, 256));
+        DBuf<double> part, scr;
+        part.ensure(3 * blocks);
+        k_norms<double><<<blocks, 256, 0, st>>>(xd, d * n, part.p);
+        ln.add();
+        const double xn = std::sqrt(sum_partials(st, ln, part.p, blocks, 3, 0, scr));
+        if (xn == 0.0) throw InvalidArg("check_convergence: all-zero X");
+        k_triple<<<blocks, 256, 0, st>>>(xd, lpd, ldd, spd, sd, d * n, part.p);
+        ln.add();
+        double h[3];
+        scr.ensure(8);
+        k_sum_partials<<<1, 256, 0, st>>>(part.p, blocks, 3, scr.p);
+        ln.add();
+        CK(cudaMemcpyAsync(h, scr.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        *feas = std::sqrt(h[0]) / xn;
+        *dl = std::sqrt(h[1]) / xn;
+        *ds = std::sqrt(h[2]) / xn;
+        double mx = *feas;
+        if (mx < *dl) mx = *dl;
+        if (mx < *ds) mx = *ds;
+        *conv = mx <= tol;
+    });
+}
+
+static void km_common(respca_cu_ctx* ctx, KMeansEngine<double>& km, Dev64& dm, const double* m,
+                      uint64_t d, uint64_t n, uint64_t c) {
+    km.st = ctx->st;
+    km.ln = Launch{&ctx->launches};
+    const double* md = dm.up(ctx->st, m, d * n);
+    km.bind(md, d, (int)n, (int)c);
+}
+
+int respca_cu_kmeans(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n, uint64_t c,
+                     uint64_t max_iters, uint64_t n_restarts, uint64_t seed, double tol,
+                     uint64_t* labels_out, double* centroids_out, double* inertia,
+                     uint64_t* iters_run) {
+    return guarded(ctx, [&] {  // kmeans.cpp:237-250
+        check_dims(d, n);
+        if (c == 0) throw InvalidArg("kmeans: c must be >= 1");
+        if (c > n) throw InvalidArg("kmeans: c exceeds column count");
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, c);
+        DBuf<int> lab;
+        DBuf<double> cen;
+        lab.ensure(n);
+        cen.ensure(d * c);
+        double in = 0.0;
+        uint64_t it = 0;
+        km.kmeans(max_iters, n_restarts, seed, tol, lab.p, cen.p, &in, &it);
+        std::vector<int> hl(n);
+        CK(cudaMemcpyAsync(hl.data(), lab.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(centroids_out, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToHost,
+                           ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        for (uint64_t j = 0; j < n; ++j) labels_out[j] = (uint64_t)hl[j];
+        *inertia = in;
+        *iters_run = it;
+    });
+}
+
+int respca_cu_kmeans_warm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                          uint64_t c, uint64_t max_iters, double tol,
+                          const uint64_t* init_labels, uint64_t* labels_out,
+                          double* centroids_out, double* inertia, uint64_t* iters_run) {
+    return guarded(ctx, [&] {  // kmeans.cpp:252-258
+        check_dims(d, n);
+        const std::vector<int> lab = to_int_labels(init_labels, n, c);
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, c);
+        DBuf<int> dl;
+        DBuf<double> cen;
+        dl.ensure(n);
+        cen.ensure(d * c);
+        km.h_labels = lab;
+        km.means(cen.p);  // means_of(m, init)
+        const uint64_t it = km.lloyd_run(cen.p, dl.p, max_iters, tol);
+        *inertia = km.inertia(cen.p, dl.p);
+        std::vector<int> hl(n);
+        CK(cudaMemcpyAsync(hl.data(), dl.p, sizeof(int) * n, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(centroids_out, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToHost,
+                           ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        for (uint64_t j = 0; j < n; ++j) labels_out[j] = (uint64_t)hl[j];
+        *iters_run = it;
+    });
+}
+
+int respca_cu_kmeans_pp_init(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                             uint64_t c, uint64_t seed, double* centroids_out) {
+    return guarded(ctx, [&] {  // kmeans.cpp:172-224
+        check_dims(d, n);
+        if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
+        if (c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, c);
+        std::mt19937_64 rng(seed);
+        const std::vector<int> ch = km.pp_init(rng);
+        DBuf<double> cen;
+        cen.ensure(d * c);
+        km.gather(ch, cen.p);
+        CK(cudaMemcpyAsync(centroids_out, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToHost,
+                           ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+int respca_cu_lloyd_step(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                         const double* centroids, uint64_t c, uint64_t* labels_out,
+                         double* next_out) {
+    return guarded(ctx, [&] {  // kmeans.cpp:226-235
+        check_dims(d, n);
+        if (c == 0) throw InvalidArg("lloyd_step: bad centroid matrix");
+        KMeansEngine<double> km;
+        Dev64 dm, dc;
+        km_common(ctx, km, dm, m, d, n, c);
+        const double* C = dc.up(ctx->st, centroids, d * c);
+        DBuf<int> lab;
+        DBuf<double> nx;
+        lab.ensure(n);
+        nx.ensure(d * c);
+        km.assign(C, lab.p);
+        km.fetch_labels(lab.p);
+        km.repair_if_needed(C, lab.p);
+        km.means(nx.p);
+        CK(cudaMemcpyAsync(next_out, nx.p, sizeof(double) * d * c, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        for (uint64_t j = 0; j < n; ++j) labels_out[j] = (uint64_t)km.h_labels[j];
+    });
+}
+
+int respca_cu_group_scatter(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                            const uint64_t* labels, uint64_t c, double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:81-97
+        check_dims(d, n);
+        const std::vector<int> lab = to_int_labels(labels, n, c);
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, c);
+        km.h_labels = lab;
+        DBuf<double> cen;
+        DBuf<int> dl;
+        cen.ensure(d * c);
+        dl.ensure(n);
+        CK(cudaMemcpyAsync(dl.p, lab.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->st));
+        km.means(cen.p);  // column_mean per group, matrix.cpp:63-79
+        // per-group sequential sums in the reference's order: groups, then members
+        k_own_exact<double><<<ceil_div(n, 128), 128, 0, ctx->st>>>(km.M, cen.p, d, (int)n, dl.p,
+                                                                  km.own.p);
+        ctx->launches++;
+        std::vector<double> own(n);
+        CK(cudaMemcpyAsync(own.data(), km.own.p, sizeof(double) * n, cudaMemcpyDeviceToHost,
+                           ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        // report-grade total (tolerance, not bitwise: the reference's single chain
+        // interleaves all groups' element terms)
+        double total = 0.0;
+        for (int k = 0; k < (int)c; ++k)
+            for (int t = km.groups.goff[k]; t < km.groups.goff[k + 1]; ++t)
+                total += own[km.groups.members[t]];
+        *out = total;
+    });
+}
+
+static double norm_kernel(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n, int q) {
+    cudaStream_t st = ctx->st;
+    Launch ln{&ctx->launches};
+    Dev64 dm;
+    const double* p = dm.up(st, m, d * n);
+    const int blocks = std::min<int64_t>(2048, ceil_div(d * n, 256));
+    DBuf<double> part, scr;
+    part.ensure(3 * blocks);
+    k_norms<double><<<blocks, 256, 0, st>>>(p, d * n, part.p);
+    ln.add();
+    return sum_partials(st, ln, part.p, blocks, 3, q, scr);
+}
+
+int respca_cu_frob_norm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                        double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:99-103
+        check_dims(d, n);
+        *out = std::sqrt(norm_kernel(ctx, m, d, n, 0));
+    });
+}
+
+int respca_cu_elementwise_l1(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                             double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:105-109
+        check_dims(d, n);
+        *out = norm_kernel(ctx, m, d, n, 1);
+    });
+}
+
+int respca_cu_column_l2_norms(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                              double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:117-125 (exact sequential per column)
+        check_dims(d, n);
+        cudaStream_t st = ctx->st;
+        Dev64 dm;
+        const double* p = dm.up(st, m, d * n);
+        DBuf<double> nr;
+        nr.ensure(n);
+        k_col_sumsq<double, 0><<<ceil_div(n, 128), 128, 0, st>>>(p, nullptr, nullptr, 1.0, d, n, nr.p);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(out, nr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int respca_cu_l21_norm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n, double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:111-115
+        check_dims(d, n);
+        std::vector<double> nr(n);
+        cudaStream_t st = ctx->st;
+        Dev64 dm;
+        const double* p = dm.up(st, m, d * n);
+        DBuf<double> dn;
+        dn.ensure(n);
+        k_col_sumsq<double, 0><<<ceil_div(n, 128), 128, 0, st>>>(p, nullptr, nullptr, 1.0, d, n, dn.p);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(nr.data(), dn.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double s = 0.0;
+        for (uint64_t j = 0; j < n; ++j) s += nr[j];
+        *out = s;
+    });
+}
+
+int respca_cu_column_mean(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                          const uint64_t* cols, uint64_t ncols, double* out) {
+    return guarded(ctx, [&] {  // matrix.cpp:63-79
+        check_dims(d, n);
+        if (ncols == 0) throw InvalidArg("column_mean: empty column set");
+        for (uint64_t t = 0; t < ncols; ++t)
+            if (cols[t] >= n) throw InvalidArg("column_mean: column index out of range");
+        // one group whose member list is `cols` in the given order
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, 1);
+        km.groups.goff = {0, (int)ncols};
+        km.groups.members.assign(cols, cols + ncols);
+        km.groups.counts = {(int)ncols};
+        km.members.ensure(ncols);
+        CK(cudaMemcpyAsync(km.goff.p, km.groups.goff.data(), sizeof(int) * 2, cudaMemcpyHostToDevice,
+                           ctx->st));
+        CK(cudaMemcpyAsync(km.members.p, km.groups.members.data(), sizeof(int) * ncols,
+                           cudaMemcpyHostToDevice, ctx->st));
+        DBuf<double> o;
+        o.ensure(d);
+        km.launch_group_mean(o.p);
+        CK(cudaMemcpyAsync(out, o.p, sizeof(double) * d, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,170 @@
+// Host-side engine infrastructure: errors, device buffers, launch accounting,
+// conditional CUDA graphs.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "respca_cu.h"
+
+namespace respca_host {
+
+struct InvalidArg : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct RuntimeErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NoMem : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct NonFinite : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+inline void ck(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        throw NoMem(std::string("device allocation failed: ") + what);
+    }
+    throw CudaErr(std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) ::respca_host::ck((x), #x)
+
+template <class U>
+struct DBuf {
+    U* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() {
+        if (p) cudaFree(p);
+    }
+    U* ensure(size_t count) {
+        if (count == 0) count = 1;
+        if (count > cap) {
+            if (p) cudaFree(p);
+            p = nullptr;
+            cap = 0;
+            CK(cudaMalloc(&p, count * sizeof(U)));
+            cap = count;
+        }
+        return p;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+};
+
+// pinned host staging buffer
+struct HBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    ~HBuf() {
+        if (p) cudaFreeHost(p);
+    }
+    template <class U>
+    U* ensure(size_t count) {
+        size_t bytes = count * sizeof(U);
+        if (bytes == 0) bytes = 8;
+        if (bytes > cap) {
+            if (p) cudaFreeHost(p);
+            p = nullptr;
+            CK(cudaMallocHost(&p, bytes));
+            cap = bytes;
+        }
+        return static_cast<U*>(p);
+    }
+};
+
+struct Events {
+    cudaEvent_t a = nullptr, b = nullptr;
+    Events() {
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+    }
+    ~Events() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    float ms() {
+        float t = 0.f;
+        CK(cudaEventElapsedTime(&t, a, b));
+        return t;
+    }
+};
+
+// A graph whose body runs while the device keeps a conditional handle set.
+struct WhileGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t body = nullptr;
+    cudaGraphConditionalHandle handle{};
+    int kernels_per_iter = 0;
+    ~WhileGraph() { reset(); }
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+        body = nullptr;
+    }
+    bool ready() const { return exec != nullptr; }
+    // begin: creates the outer graph + WHILE node and starts capturing `st`
+    // into its body.  The captured kernels must set the handle to 0 to stop.
+    void begin(cudaStream_t st) {
+        reset();
+        CK(cudaGraphCreate(&graph, 0));
+        CK(cudaGraphConditionalHandleCreate(&handle, graph, 1u, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams prm = {};
+        prm.type = cudaGraphNodeTypeConditional;
+        prm.conditional.handle = handle;
+        prm.conditional.type = cudaGraphCondTypeWhile;
+        prm.conditional.size = 1;
+        cudaGraphNode_t node;
+        CK(cudaGraphAddNode(&node, graph, nullptr, 0, &prm));
+        body = prm.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(st, body, nullptr, nullptr, 0,
+                                         cudaStreamCaptureModeRelaxed));
+    }
+    void end(cudaStream_t st) {
+        cudaGraph_t out = nullptr;
+        CK(cudaStreamEndCapture(st, &out));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    void launch(cudaStream_t st) { CK(cudaGraphLaunch(exec, st)); }
+};
+
+// plain captured graph
+struct PlainGraph {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    ~PlainGraph() { reset(); }
+    void reset() {
+        if (exec) cudaGraphExecDestroy(exec);
+        if (graph) cudaGraphDestroy(graph);
+        exec = nullptr;
+        graph = nullptr;
+    }
+    void begin(cudaStream_t st) {
+        reset();
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+    }
+    void end(cudaStream_t st) {
+        CK(cudaStreamEndCapture(st, &graph));
+        CK(cudaGraphInstantiate(&exec, graph, 0));
+    }
+    void launch(cudaStream_t st) { CK(cudaGraphLaunch(exec, st)); }
+};
+
+}  // namespace respca_host

@@ -1,0 +1,849 @@
+// K-means kernels (the p-update, kmeans.cpp) — exact decisions on screened
+// distances.
+//
+// Every discrete decision of the reference's K-means — nearest centroid
+// (kmeans.cpp:29, strict <, lowest index wins ties), the Hartigan move test
+// (kmeans.cpp:107-119, threshold −1e-12), the farthest-point repair
+// (kmeans.cpp:49-56) — is made on the reference's own distance value
+// sq_dist(a, b) = Σ_i fl(fl(a_i − b_i)²) summed sequentially over ascending i
+// (kmeans.cpp:12-19).  Reproducing that chain costs d dependent adds per
+// (column, centroid) pair, so the kernels below first compute a SCREENED
+// distance with the expanded form ‖x‖² + ‖c‖² − 2x·c on the FP64 FMA pipe,
+// together with a rigorous bound on its distance to the reference value:
+//
+//   |ref − approx| ≤ e = (2d + 8)·u·1.05·(‖x‖ + ‖c‖)² + 2u·|approx|,  u = 2⁻⁵³
+//
+// (γ_d bounds for the three length-d FMA chains, the 3u term error of each
+// rounded (a−b)², the sequential-sum bound γ_{d−1} of the reference chain, and
+// slack).  A decision is taken from [approx − e, approx + e] only when it is
+// the same for every value in the interval (IEEE rounding is monotone, so the
+// weights na/(na−1)·dist etc. are bounded by evaluating them at the interval
+// ends).  Undecidable columns — ties and near-ties — are resolved by the exact
+// sequential chain, so labels are bit-identical to the reference's.
+#pragma once
+
+#include "common.cuh"
+
+namespace respca_dev {
+
+constexpr double kU = 1.1102230246251565e-16;  // 2^-53
+
+RESPCA_DEV double screen_err(double kappa_d, double nx, double nc, double approx) {
+    const double s = nx + nc;
+    return kappa_d * (s * s) + 2.0 * kU * fabs(approx) + 1e-300;
+}
+
+RESPCA_DEV void cp_async8(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 8 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+RESPCA_DEV void cp_async4(void* smem, const void* gmem, bool pred) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    const int sz = pred ? 4 : 0;
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(s), "l"(gmem), "r"(sz));
+}
+RESPCA_DEV void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+RESPCA_DEV void cp_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+// ---------------------------------------------------------------------------
+// ‖c_k‖² for the screen (FMA chain; only ever used inside the bound)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_col_sq_fma(const double* __restrict__ C, int64_t d,
+                                                    double* __restrict__ out) {
+    __shared__ double red[32];
+    const int k = blockIdx.x;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+        const double v = C[(int64_t)k * d + i];
+        s = __fma_rn(v, v, s);
+    }
+    double v[1] = {s};
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) out[k] = v[0];
+}
+
+// ---------------------------------------------------------------------------
+// Screened distance GEMM:  part[s][j][k] = Σ_{i∈split s} M[i,j]·C[i,k]
+//                          xxp[s][j]     = Σ_{i∈split s} M[i,j]²
+// CTA tile TJ×TK outputs, thread tile RJ×RK, K-chunks of 32 rows staged in
+// shared memory by a 2-stage cp.async pipeline (global column-major →
+// shared row-major, so both operands are read as 128-bit rows in the inner
+// loop).  FP64-FMA bound: intensity RJ·RK FMAs per (RJ+RK) smem doubles.
+// ---------------------------------------------------------------------------
+template <typename T, int RJ, int RK, int NTJ, int NTK>
+__global__ void __launch_bounds__(NTJ* NTK) k_dist_screen(const T* __restrict__ M,
+                                                          const double* __restrict__ C, int64_t d,
+                                                          int n, int c, int chunks_per_split,
+                                                          double* __restrict__ part,
+                                                          double* __restrict__ xxp) {
+    constexpr int TJ = RJ * NTJ, TK = RK * NTK, KI = 32, NT = NTJ * NTK;
+    constexpr int MSTR = TJ + (sizeof(T) == 8 ? 2 : 4);  // 16-byte aligned rows
+    constexpr int CSTR = TK + 2;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* Ms = reinterpret_cast<T*>(smem_raw);                                      // [2][KI][MSTR]
+    double* Cs = reinterpret_cast<double*>(smem_raw + sizeof(T) * 2 * KI * MSTR);  // [2][KI][CSTR]
+    __shared__ double xred[NT];
+
+    const int tid = threadIdx.x;
+    const int tk = tid % NTK, tj = tid / NTK;
+    const int j0 = blockIdx.x * TJ, k0 = blockIdx.y * TK, split = blockIdx.z;
+    const int64_t ibeg = (int64_t)split * chunks_per_split * KI;
+    int64_t iend = ibeg + (int64_t)chunks_per_split * KI;
+    if (iend > d) iend = d;
+    const int nch = ibeg < iend ? (int)((iend - ibeg + KI - 1) / KI) : 0;
+
+    auto load = [&](int64_t i0, int buf) {
+        T* mdst = Ms + buf * KI * MSTR;
+        double* cdst = Cs + buf * KI * CSTR;
+        for (int e = tid; e < TJ * KI; e += NT) {
+            const int col = e / KI, ii = e - col * KI;
+            const int j = j0 + col;
+            const int64_t i = i0 + ii;
+            const bool p = (j < n) && (i < iend);
+            const T* src = p ? M + (int64_t)j * d + i : M;
+            if (sizeof(T) == 8) cp_async8(mdst + ii * MSTR + col, src, p);
+            else cp_async4(mdst + ii * MSTR + col, src, p);
+        }
+        for (int e = tid; e < TK * KI; e += NT) {
+            const int kk = e / KI, ii = e - kk * KI;
+            const int k = k0 + kk;
+            const int64_t i = i0 + ii;
+            const bool p = (k < c) && (i < iend);
+            cp_async8(cdst + ii * CSTR + kk, p ? C + (int64_t)k * d + i : C, p);
+        }
+        cp_commit();
+    };
+
+    double acc[RJ][RK];
+#pragma unroll
+    for (int a = 0; a < RJ; ++a)
+#pragma unroll
+        for (int b = 0; b < RK; ++b) acc[a][b] = 0.0;
+    // ‖x‖² helpers: NT/TJ threads per column, each a contiguous row range of the chunk
+    constexpr int XPER = NT / TJ;  // threads per column
+    constexpr int XROWS = KI / XPER;
+    const int xcol = tid % TJ, xpart = tid / TJ;
+    double xx = 0.0;
+
+    if (nch > 0) load(ibeg, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+            load(ibeg + (int64_t)(ch + 1) * KI, (ch + 1) & 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const T* ms = Ms + (ch & 1) * KI * MSTR;
+        const double* cs = Cs + (ch & 1) * KI * CSTR;
+#pragma unroll 4
+        for (int ii = 0; ii < KI; ++ii) {
+            double a[RJ], b[RK];
+#pragma unroll
+            for (int x = 0; x < RJ; ++x) a[x] = (double)ms[ii * MSTR + tj * RJ + x];
+#pragma unroll
+            for (int y = 0; y < RK; ++y) b[y] = cs[ii * CSTR + tk * RK + y];
+#pragma unroll
+            for (int x = 0; x < RJ; ++x)
+#pragma unroll
+                for (int y = 0; y < RK; ++y) acc[x][y] = __fma_rn(a[x], b[y], acc[x][y]);
+        }
+#pragma unroll
+        for (int r = 0; r < XROWS; ++r) {
+            const double v = (double)ms[(xpart * XROWS + r) * MSTR + xcol];
+            xx = __fma_rn(v, v, xx);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int x = 0; x < RJ; ++x) {
+        const int j = j0 + tj * RJ + x;
+        if (j >= n) continue;
+#pragma unroll
+        for (int y = 0; y < RK; ++y) {
+            const int k = k0 + tk * RK + y;
+            if (k < c) part[((int64_t)split * n + j) * c + k] = acc[x][y];
+        }
+    }
+    xred[tid] = xx;
+    __syncthreads();
+    if (blockIdx.y == 0 && tid < TJ && j0 + tid < n) {
+        double s = 0.0;
+        for (int p = 0; p < XPER; ++p) s += xred[p * TJ + tid];
+        xxp[(int64_t)split * n + j0 + tid] = s;
+    }
+}
+
+// Screened distance of (j, k) from the split partials (fixed split order).
+struct Screen {
+    const double* part;
+    const double* xxp;
+    const double* cc;
+    int nsplit, n, c;
+    double kappa_d;
+    RESPCA_DEV double xx(int j) const {
+        double s = 0.0;
+        for (int p = 0; p < nsplit; ++p) s += xxp[(int64_t)p * n + j];
+        return s;
+    }
+    RESPCA_DEV void get(int j, int k, double xxj, double nx, double& lo, double& hi,
+                        double& mid) const {
+        double dot = 0.0;
+        for (int p = 0; p < nsplit; ++p) dot += part[((int64_t)p * n + j) * c + k];
+        const double ck = cc[k];
+        mid = (xxj + ck) - 2.0 * dot;
+        const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid);
+        if (!isfinite(mid) || !isfinite(e)) {
+            lo = -INFINITY;
+            hi = INFINITY;
+        } else {
+            lo = mid - e;
+            hi = mid + e;
+        }
+    }
+};
+
+// warp-wide lexicographic argmin on (value, index)
+RESPCA_DEV void warp_argmin(double& v, int& k) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+        const int ok = __shfl_xor_sync(0xffffffffu, k, o);
+        if (ov < v || (ov == v && ok < k)) {
+            v = ov;
+            k = ok;
+        }
+    }
+}
+RESPCA_DEV double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Decision status of one column
+enum : int { ST_STABLE = 0, ST_CHANGED = 1, ST_MOVE = 2, ST_AMBIG = 3 };
+
+// ---------------------------------------------------------------------------
+// Per-column decision (one warp per column) on [lo, hi] intervals of the
+// reference's distances:
+//   1. label = argmin_k dist (kmeans.cpp:27-33)  — certain or ambiguous
+//   2. if HART and the label is certain and unchanged: does the first
+//      Hartigan pass move this column? (kmeans.cpp:103-121)
+// DistFn(j, k, lo, hi, mid) supplies the interval (exact: lo = hi = mid).
+// Returns the status and (for certain labels) the new label.
+// ---------------------------------------------------------------------------
+template <typename DistFn>
+RESPCA_DEV int decide_column(int j, int c, int old_label, const int* __restrict__ counts,
+                             bool hart, const DistFn& dist, int& new_label) {
+    const int lane = threadIdx.x & 31;
+    // candidate argmin on the midpoint
+    double bv = INFINITY;
+    int bk = 0x7fffffff;
+    for (int k = lane; k < c; k += 32) {
+        double lo, hi, mid;
+        dist(j, k, lo, hi, mid);
+        if (mid < bv) {  // ascending k per lane: strict < keeps the lowest index
+            bv = mid;
+            bk = k;
+        }
+    }
+    warp_argmin(bv, bk);
+    if (bk >= c) bk = 0;  // all-NaN guard: treated as ambiguous below
+    double klo, khi, kmid;
+    dist(j, bk, klo, khi, kmid);
+    bool ok = true;
+    for (int k = lane; k < c; k += 32) {
+        if (k == bk) continue;
+        double lo, hi, mid;
+        dist(j, k, lo, hi, mid);
+        if (k < bk) ok &= khi < lo;
+        else ok &= khi <= lo;
+    }
+    ok = __all_sync(0xffffffffu, ok) && isfinite(khi);
+    if (!ok) return ST_AMBIG;
+    new_label = bk;
+    if (bk != old_label) return ST_CHANGED;
+    if (!hart) return ST_STABLE;
+    const int from = bk;
+    const int cf = counts[from];
+    if (cf <= 1) return ST_STABLE;  // kmeans.cpp:105
+    const double na = (double)cf;
+    const double wa = na / (na - 1.0);
+    const double gain_hi = wa * khi, gain_lo = wa * klo;
+    bool surely_none = true, surely_move = false;
+    for (int k = lane; k < c; k += 32) {
+        if (k == from) continue;
+        double lo, hi, mid;
+        dist(j, k, lo, hi, mid);
+        const double nb = (double)counts[k];
+        const double wb = nb / (nb + 1.0);
+        const double dlo = wb * lo - gain_hi;
+        const double dhi = wb * hi - gain_lo;
+        surely_none &= !(dlo < -1e-12);
+        surely_move |= dhi < -1e-12;
+    }
+    surely_none = __all_sync(0xffffffffu, surely_none);
+    surely_move = __any_sync(0xffffffffu, surely_move);
+    if (surely_none) return ST_STABLE;
+    if (surely_move) return ST_MOVE;
+    return ST_AMBIG;
+}
+
+// Decide all columns from the screen.  mode: 0 = Lloyd assignment only,
+// 1 = ALM fast-path check (assignment + first Hartigan pass).
+// Output labels are written to new_labels; ambiguous columns are appended to
+// amb_list and keep their old label for now.
+__global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
+                                                const int* __restrict__ old_labels,
+                                                const int* __restrict__ counts, int mode,
+                                                int* __restrict__ new_labels,
+                                                int* __restrict__ amb_list, Ctl* __restrict__ ctl) {
+    const int lane = threadIdx.x & 31;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= n || ctl->done) return;
+    const double xxj = sc.xx(j);
+    const double nx = sqrt(fabs(xxj));
+    auto fn = [&](int jj, int k, double& lo, double& hi, double& mid) {
+        sc.get(jj, k, xxj, nx, lo, hi, mid);
+    };
+    const int old = old_labels ? old_labels[j] : -1;
+    int nl = old;
+    const int st = decide_column(j, c, old, counts, mode == 1, fn, nl);
+    if (lane == 0) {
+        new_labels[j] = st == ST_AMBIG ? old : nl;
+        if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);
+        if (st == ST_MOVE) atomicAdd(&ctl->moves, 1u);
+        if (st == ST_AMBIG) {
+            const unsigned slot = atomicAdd(&ctl->ambiguous, 1u);
+            amb_list[slot] = j;
+        }
+    }
+}
+
+// Exact sequential distances (kmeans.cpp:12-19) of listed columns to all
+// centroids: out[idx][k].  One block per listed column, one thread per
+// centroid, ascending i — the reference's chain.
+template <typename T>
+__global__ void __launch_bounds__(128) k_exact_cols(const T* __restrict__ M,
+                                                    const double* __restrict__ C, int64_t d,
+                                                    int c, const int* __restrict__ list,
+                                                    const unsigned* __restrict__ count,
+                                                    double* __restrict__ out) {
+    const unsigned cnt = count ? *count : gridDim.x;
+    for (unsigned idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
+        const int j = list[idx];
+        const T* x = M + (int64_t)j * d;
+        for (int k = threadIdx.x; k < c; k += blockDim.x) {
+            const double* cv = C + (int64_t)k * d;
+            double s = 0.0;
+            for (int64_t i = 0; i < d; ++i) {
+                const double t = (double)__ldg(x + i) - __ldg(cv + i);
+                s += t * t;
+            }
+            out[(int64_t)idx * c + k] = s;
+        }
+    }
+}
+
+// Re-decide the listed (ambiguous) columns with exact distances.
+__global__ void __launch_bounds__(256) k_redecide(const double* __restrict__ exact, int c,
+                                                  const int* __restrict__ list,
+                                                  const unsigned* __restrict__ count,
+                                                  const int* __restrict__ old_labels,
+                                                  const int* __restrict__ counts, int mode,
+                                                  int* __restrict__ new_labels,
+                                                  Ctl* __restrict__ ctl) {
+    const int lane = threadIdx.x & 31;
+    if (ctl->done) return;
+    const unsigned cnt = *count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->exact_fallbacks += cnt;
+    const unsigned w0 = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const unsigned nw = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned idx = w0; idx < cnt; idx += nw) {
+        const int j = list[idx];
+        auto fn = [&](int, int k, double& lo, double& hi, double& mid) {
+            mid = exact[(int64_t)idx * c + k];
+            lo = hi = mid;
+        };
+        const int old = old_labels ? old_labels[j] : -1;
+        int nl = old;
+        const int st = decide_column(j, c, old, counts, mode == 1, fn, nl);
+        if (lane == 0) {
+            new_labels[j] = nl;
+            if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);
+            if (st == ST_MOVE) atomicAdd(&ctl->moves, 1u);
+        }
+    }
+}
+
+// Fast-path verdict: any label change or Hartigan move → slow path.
+__global__ void k_fast_verdict(Ctl* __restrict__ ctl) {
+    if (ctl->done) return;
+    if (ctl->changed || ctl->moves) ctl->slow = 1;
+}
+
+// ---------------------------------------------------------------------------
+// k-means++ distance update (kmeans.cpp:188-191):
+//   d2[j] = std::min(d2[j], sq_dist(col_j, col_last))
+// Warp-transposed exact chains: lane = column, 32×32 tiles read coalesced.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128) k_pp_d2(const T* __restrict__ M, int64_t d, int n,
+                                               int last, double* __restrict__ d2) {
+    __shared__ double tile[4][32][33];
+    __shared__ double lastv[4][32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j0 = (blockIdx.x * 4 + w) * 32;
+    if (j0 >= n) return;
+    double s = 0.0;
+    for (int64_t i0 = 0; i0 < d; i0 += 32) {
+        const int64_t i = i0 + lane;
+        lastv[w][lane] = i < d ? (double)M[(int64_t)last * d + i] : 0.0;
+        for (int cc = 0; cc < 32; ++cc) {
+            const int j = j0 + cc;
+            tile[w][cc][lane] = (j < n && i < d) ? (double)M[(int64_t)j * d + i] : 0.0;
+        }
+        __syncwarp();
+        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
+        for (int r = 0; r < lim; ++r) {
+            const double t = tile[w][lane][r] - lastv[w][r];
+            s += t * t;
+        }
+        __syncwarp();
+    }
+    const int j = j0 + lane;
+    if (j < n) {
+        const double old = d2[j];
+        d2[j] = (s < old) ? s : old;
+    }
+}
+
+// Exact own-centroid distance sq_dist(col_j, C[:, label_j]) for every column
+// (inertia_of, kmeans.cpp:84-91; repair_empty, kmeans.cpp:51).
+template <typename T>
+__global__ void __launch_bounds__(128) k_own_exact(const T* __restrict__ M,
+                                                   const double* __restrict__ C, int64_t d, int n,
+                                                   const int* __restrict__ labels,
+                                                   double* __restrict__ out) {
+    __shared__ double tile[4][32][33];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j0 = (blockIdx.x * 4 + w) * 32;
+    if (j0 >= n) return;
+    const int j = j0 + lane;
+    const double* cv = C + (int64_t)(j < n ? labels[j] : 0) * d;
+    double s = 0.0;
+    for (int64_t i0 = 0; i0 < d; i0 += 32) {
+        const int64_t i = i0 + lane;
+        for (int cc = 0; cc < 32; ++cc) {
+            const int jj = j0 + cc;
+            tile[w][cc][lane] = (jj < n && i < d) ? (double)M[(int64_t)jj * d + i] : 0.0;
+        }
+        __syncwarp();
+        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
+        for (int r = 0; r < lim; ++r) {
+            const double t = tile[w][lane][r] - __ldg(cv + i0 + r);
+            s += t * t;
+        }
+        __syncwarp();
+    }
+    if (j < n) out[j] = s;
+}
+
+template <typename T>
+__global__ void k_gather_cols(const T* __restrict__ M, int64_t d, const int* __restrict__ idx,
+                              int c, double* __restrict__ C) {
+    const int k = blockIdx.y;
+    const int64_t src = (int64_t)idx[k] * d;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+         i += (int64_t)gridDim.x * blockDim.x)
+        C[(int64_t)k * d + i] = (double)M[src + i];
+}
+
+// Lloyd stop test partials (kmeans.cpp:148-153): Σ(next−C)², ΣC²
+__global__ void __launch_bounds__(256) k_moved_scale(const double* __restrict__ next,
+                                                     const double* __restrict__ C, int64_t N,
+                                                     double* __restrict__ partials) {
+    __shared__ double red[64];
+    double a = 0.0, b = 0.0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const double t = next[k] - C[k];
+        a += t * t;
+        b += C[k] * C[k];
+    }
+    double v[2] = {a, b};
+    block_sum<2>(v, red);
+    if (threadIdx.x == 0) {
+        partials[blockIdx.x * 2] = v[0];
+        partials[blockIdx.x * 2 + 1] = v[1];
+    }
+}
+
+// The reference's exact sequential chains for the Lloyd stop (used only when
+// the tree-summed test lands within 1e-9 of its threshold).
+__global__ void k_moved_scale_exact(const double* __restrict__ next, const double* __restrict__ C,
+                                    int64_t N, double* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    double moved = 0.0, scale = 0.0;
+    for (int64_t k = 0; k < N; ++k) {
+        const double t = next[k] - C[k];
+        moved += t * t;
+        scale += C[k] * C[k];
+    }
+    out[0] = moved;
+    out[1] = scale;
+}
+
+__global__ void k_count_labels(const int* __restrict__ labels, int n, int* __restrict__ counts) {
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x)
+        atomicAdd(&counts[labels[j]], 1);
+}
+
+// ---------------------------------------------------------------------------
+// repair_empty (kmeans.cpp:40-64), one block: for each empty cluster e in
+// ascending order, steal the farthest point (strict > keeps the first index)
+// among clusters with more than one member.  own[] holds the exact
+// sq_dist(col_j, C[label_j]) values; the stolen point's entry is recomputed
+// against its new centroid, exactly as the reference's next scan sees it.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(1024) k_repair(const T* __restrict__ M,
+                                                 const double* __restrict__ C, int64_t d, int n,
+                                                 int c, int* __restrict__ labels,
+                                                 int* __restrict__ counts,
+                                                 double* __restrict__ own, int* __restrict__ err) {
+    __shared__ double sv[32];
+    __shared__ int sj[32];
+    __shared__ int s_steal;
+    __shared__ double s_worst;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int e = 0; e < c; ++e) {
+        if (counts[e] > 0) continue;
+        double best = -1.0;
+        int bj = 0x7fffffff;
+        for (int j = threadIdx.x; j < n; j += blockDim.x) {
+            if (counts[labels[j]] <= 1) continue;
+            const double v = own[j];
+            if (v > best) {  // ascending j per thread: strict > keeps the first
+                best = v;
+                bj = j;
+            }
+        }
+        // argmax, ties → lowest j
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oj = __shfl_xor_sync(0xffffffffu, bj, o);
+            if (ov > best || (ov == best && oj < bj)) {
+                best = ov;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            sv[w] = best;
+            sj[w] = bj;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double b = -1.0;
+            int jj = 0x7fffffff;
+            for (int q = 0; q < (int)(blockDim.x >> 5); ++q)
+                if (sv[q] > b || (sv[q] == b && sj[q] < jj)) {
+                    b = sv[q];
+                    jj = sj[q];
+                }
+            s_worst = b;
+            s_steal = jj;
+            if (b < 0.0) {
+                *err = 1;  // "kmeans: cannot repair empty cluster"
+            } else {
+                counts[labels[jj]] -= 1;
+                labels[jj] = e;
+                counts[e] += 1;
+                double s = 0.0;  // exact chain against the new centroid
+                for (int64_t i = 0; i < d; ++i) {
+                    const double t = (double)M[(int64_t)jj * d + i] - C[(int64_t)e * d + i];
+                    s += t * t;
+                }
+                own[jj] = s;
+            }
+        }
+        __syncthreads();
+        if (s_worst < 0.0) return;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Exact sequential Hartigan refinement (kmeans.cpp:96-139) on the device.
+//
+// The reference visits columns j = 0..n−1 in order and applies each improving
+// single-point move immediately (incremental centroid update, kmeans.cpp:
+// 128-131), so every later decision sees the updated state.  The device
+// version keeps that order with windows: a round refreshes the screened
+// distances of the next W columns (only entries whose centroid changed since
+// they were computed, tracked by per-centroid version stamps), then one CTA
+// evaluates the window's columns in parallel against the current state and
+// takes the FIRST column that moves — all columns before it provably do not
+// move in the sequential order — applies that move exactly, and restarts the
+// window just after it.  Undecidable columns fall back to exact chains.
+// ---------------------------------------------------------------------------
+struct HartState {
+    int cursor;    // next column to visit in this pass
+    int pass;      // 0..49
+    int improved;  // a move happened in this pass
+    int done;
+    int movecount; // global version counter
+    unsigned long long moves, exact_fallbacks;
+};
+
+// refresh window entries: approx[j][k], err[j][k] for stale (j, k)
+template <typename T>
+__global__ void __launch_bounds__(256) k_hart_refresh(const T* __restrict__ M,
+                                                      const double* __restrict__ C,
+                                                      const double* __restrict__ cc,
+                                                      const double* __restrict__ xx, int64_t d,
+                                                      int n, int c, int W,
+                                                      const HartState* __restrict__ hs,
+                                                      const int* __restrict__ modver,
+                                                      int* __restrict__ stamp,
+                                                      double* __restrict__ approx,
+                                                      double* __restrict__ err, double kappa_d) {
+    constexpr int KB = 8;
+    __shared__ double red[32 * KB];
+    if (hs->done) return;
+    const int j = hs->cursor + blockIdx.x;
+    if (j >= n || blockIdx.x >= W) return;
+    const int kbase = blockIdx.y * KB;
+    if (kbase >= c) return;
+    const int mv = hs->movecount;
+    int stale_mask = 0;
+#pragma unroll
+    for (int q = 0; q < KB; ++q) {
+        const int k = kbase + q;
+        if (k < c && stamp[(int64_t)j * c + k] < modver[k]) stale_mask |= 1 << q;
+    }
+    if (!stale_mask) return;
+    const T* x = M + (int64_t)j * d;
+    double v[KB];
+#pragma unroll
+    for (int q = 0; q < KB; ++q) v[q] = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+        const double xi = (double)__ldg(x + i);
+#pragma unroll
+        for (int q = 0; q < KB; ++q)
+            if (stale_mask & (1 << q)) v[q] = __fma_rn(xi, C[(int64_t)(kbase + q) * d + i], v[q]);
+    }
+    block_sum<KB>(v, red);
+    if (threadIdx.x < KB && (stale_mask & (1 << threadIdx.x))) {
+        const int k = kbase + threadIdx.x;
+        double dot = 0.0;
+#pragma unroll
+        for (int q = 0; q < KB; ++q)
+            if (q == (int)threadIdx.x) dot = v[q];
+        const double xxj = xx[j];
+        const double mid = (xxj + cc[k]) - 2.0 * dot;
+        const double e = screen_err(kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cc[k])), mid);
+        approx[(int64_t)j * c + k] = mid;
+        err[(int64_t)j * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+        stamp[(int64_t)j * c + k] = mv;
+    }
+}
+
+// one CTA: decide the window, apply the first move, advance the cursor
+template <typename T>
+__global__ void __launch_bounds__(1024) k_hart_step(const T* __restrict__ M, double* __restrict__ C,
+                                                    double* __restrict__ cc, int64_t d, int n,
+                                                    int c, int W, HartState* __restrict__ hs,
+                                                    int* __restrict__ modver,
+                                                    int* __restrict__ stamp,
+                                                    const double* __restrict__ approx,
+                                                    const double* __restrict__ err,
+                                                    int* __restrict__ labels,
+                                                    int* __restrict__ counts,
+                                                    double* __restrict__ exact_scratch,
+                                                    int max_passes, int has_cond,
+                                                    cudaGraphConditionalHandle cond) {
+    __shared__ int s_first, s_kind, s_to;
+    __shared__ double red[32 * 2];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (hs->done) {
+        if (threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    const int cursor = hs->cursor;
+    int wend = cursor + W;
+    if (wend > n) wend = n;
+    if (threadIdx.x == 0) s_first = 0x7fffffff;
+    __syncthreads();
+
+    // Hartigan decision of column j on intervals; returns 0 none, 1 move(to), 2 ambiguous
+    auto decide = [&](int j, bool exact, int& to) -> int {
+        const int from = labels[j];
+        const int cf = counts[from];
+        if (cf <= 1) return 0;
+        auto iv = [&](int k, double& lo, double& hi, double& mid) {
+            if (exact) {
+                mid = exact_scratch[k];
+                lo = hi = mid;
+            } else {
+                mid = approx[(int64_t)j * c + k];
+                const double e = err[(int64_t)j * c + k];
+                lo = mid - e;
+                hi = mid + e;
+            }
+        };
+        double flo, fhi, fmid;
+        iv(from, flo, fhi, fmid);
+        const double na = (double)cf;
+        const double wa = na / (na - 1.0);
+        const double g_lo = wa * flo, g_hi = wa * fhi, g_mid = wa * fmid;
+        // candidate: minimal midpoint delta among k != from (first index on ties)
+        double bd = INFINITY;
+        int bk = 0x7fffffff;
+        bool none = true;
+        for (int k = lane; k < c; k += 32) {
+            if (k == from) continue;
+            double lo, hi, mid;
+            iv(k, lo, hi, mid);
+            const double nb = (double)counts[k];
+            const double wb = nb / (nb + 1.0);
+            const double dmid = wb * mid - g_mid;
+            none &= !(wb * lo - g_hi < -1e-12);
+            if (dmid < bd) {
+                bd = dmid;
+                bk = k;
+            }
+        }
+        none = __all_sync(0xffffffffu, none);
+        if (none) return 0;
+        warp_argmin(bd, bk);
+        if (bk >= c) return 2;
+        double blo, bhi, bmid;
+        iv(bk, blo, bhi, bmid);
+        const double nbk = (double)counts[bk];
+        const double dhi_k = (nbk / (nbk + 1.0)) * bhi - g_lo;
+        bool ok = dhi_k < -1e-12;
+        for (int k = lane; k < c; k += 32) {
+            if (k == from || k == bk) continue;
+            double lo, hi, mid;
+            iv(k, lo, hi, mid);
+            const double nb = (double)counts[k];
+            const double dlo = (nb / (nb + 1.0)) * lo - g_hi;
+            if (k < bk) ok &= dhi_k < dlo;
+            else ok &= dhi_k <= dlo;
+        }
+        ok = __all_sync(0xffffffffu, ok);
+        if (!ok) return 2;
+        to = bk;
+        return 1;
+    };
+
+    // each warp takes columns cursor+w, cursor+w+32, ...; find the first non-trivial
+    for (int j = cursor + w; j < wend; j += 32) {
+        int to = -1;
+        const int r = decide(j, false, to);
+        if (r != 0) {
+            if (lane == 0) atomicMin(&s_first, j);
+            break;
+        }
+    }
+    __syncthreads();
+    const int jf = s_first;
+    if (jf == 0x7fffffff) {  // nothing moves in the window
+        if (threadIdx.x == 0) hs->cursor = wend;
+    } else {
+        // resolve column jf: screened decision, exact fallback if needed
+        if (w == 0) {
+            int to = -1;
+            const int r = decide(jf, false, to);
+            if (lane == 0) {
+                s_kind = r;
+                s_to = to;
+            }
+        }
+        __syncthreads();
+        if (s_kind == 2) {
+            const int jj = jf;
+            for (int k = threadIdx.x; k < c; k += blockDim.x) {
+                const double* cv = C + (int64_t)k * d;
+                const T* x = M + (int64_t)jj * d;
+                double s = 0.0;
+                for (int64_t i = 0; i < d; ++i) {
+                    const double t = (double)x[i] - cv[i];
+                    s += t * t;
+                }
+                exact_scratch[k] = s;
+            }
+            __syncthreads();
+            if (w == 0) {
+                int to = -1;
+                const int r = decide(jf, true, to);
+                if (lane == 0) {
+                    s_kind = r;
+                    s_to = to;
+                    hs->exact_fallbacks += 1;
+                }
+            }
+            __syncthreads();
+        }
+        if (s_kind == 0) {
+            if (threadIdx.x == 0) hs->cursor = jf + 1;
+        } else {
+            // apply the move exactly as kmeans.cpp:122-135
+            const int from = labels[jf], to = s_to;
+            const int cfrom = counts[from], cto = counts[to];
+            const double na1 = (double)(cfrom - 1), nb1 = (double)(cto + 1);
+            const double dcf = (double)cfrom, dct = (double)cto;
+            double* cfp = C + (int64_t)from * d;
+            double* ctp = C + (int64_t)to * d;
+            const T* x = M + (int64_t)jf * d;
+            double sf = 0.0, st = 0.0;
+            for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+                const double xi = (double)x[i];
+                const double a = (cfp[i] * dcf - xi) / na1;
+                const double b = (ctp[i] * dct + xi) / nb1;
+                cfp[i] = a;
+                ctp[i] = b;
+                sf = __fma_rn(a, a, sf);
+                st = __fma_rn(b, b, st);
+            }
+            double v[2] = {sf, st};
+            block_sum<2>(v, red);
+            if (threadIdx.x == 0) {
+                cc[from] = v[0];
+                cc[to] = v[1];
+                counts[from] = cfrom - 1;
+                counts[to] = cto + 1;
+                labels[jf] = to;
+                const int mv = hs->movecount + 1;
+                hs->movecount = mv;
+                modver[from] = mv;
+                modver[to] = mv;
+                hs->improved = 1;
+                hs->moves += 1;
+                hs->cursor = jf + 1;
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        if (hs->cursor >= n) {
+            if (hs->improved && hs->pass + 1 < max_passes) {
+                hs->pass += 1;
+                hs->cursor = 0;
+                hs->improved = 0;
+            } else {
+                hs->done = 1;
+            }
+        }
+        if (has_cond) cudaGraphSetConditional(cond, hs->done ? 0u : 1u);
+    }
+    (void)stamp;
+}
+
+}  // namespace respca_dev

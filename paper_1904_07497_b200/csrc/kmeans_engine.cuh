@@ -1,0 +1,426 @@
+// Device K-means engine: kmeans / kmeans_warm / lloyd_run / hartigan_refine /
+// kmeans_pp_init (reference kmeans.cpp) with bit-identical labels.
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <random>
+#include <vector>
+
+#include "alm.cuh"
+#include "engine.cuh"
+#include "km.cuh"
+
+namespace respca_host {
+
+using namespace respca_dev;
+
+struct Launch {
+    uint64_t* counter;
+    void add(uint64_t k = 1) { *counter += k; }
+};
+
+inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
+
+// host counting sort → CSR member lists in ascending column order
+// (GroupAssignment::group_indices, matrix.cpp:49-55)
+struct Groups {
+    std::vector<int> goff, members, counts;
+    void build(const int* labels, int n, int c) {
+        goff.assign(c + 1, 0);
+        counts.assign(c, 0);
+        for (int j = 0; j < n; ++j) counts[labels[j]]++;
+        for (int k = 0; k < c; ++k) goff[k + 1] = goff[k] + counts[k];
+        members.resize(n);
+        std::vector<int> fill(goff.begin(), goff.end() - 1);
+        for (int j = 0; j < n; ++j) members[fill[labels[j]]++] = j;
+    }
+};
+
+struct Stats {
+    uint64_t hartigan_moves = 0, exact_fallbacks = 0, lloyd_steps = 0, hartigan_passes = 0;
+};
+
+template <typename T>
+struct KMeansEngine {
+    cudaStream_t st = nullptr;
+    Launch ln{nullptr};
+    Stats* stats = nullptr;
+    const T* M = nullptr;
+    int64_t d = 0;
+    int n = 0, c = 0;
+    int nsplit = 1;
+    // buffers
+    DBuf<double> part, xxp, cc, nextC, exact, own, msp, approx, err, d2, xx, scratch;
+    DBuf<int> newlab, amb, counts, goff, members, modver, stamp, gidx, errflag;
+    DBuf<Ctl> kctl;
+    DBuf<HartState> hs;
+    HBuf hst;
+    Groups groups;
+    std::vector<int> h_labels;
+
+    void bind(const T* m, int64_t dd, int nn, int cc_) {
+        M = m;
+        d = dd;
+        n = nn;
+        c = cc_;
+        // split-K for the screen: aim for >= 2 CTAs per SM
+        const int tiles = ceil_div(n, tile_j()) * ceil_div(c, tile_k());
+        const int chunks = ceil_div(d, 32);
+        nsplit = std::max(1, std::min(chunks / 4, ceil_div(296, tiles)));
+        nsplit = std::min(nsplit, 32);
+        part.ensure((size_t)nsplit * n * c);
+        xxp.ensure((size_t)nsplit * n);
+        cc.ensure(c);
+        nextC.ensure((size_t)d * c);
+        exact.ensure((size_t)n * c);
+        own.ensure(n);
+        msp.ensure(2 * 512 + 2);
+        newlab.ensure(n);
+        amb.ensure(n);
+        counts.ensure(c);
+        goff.ensure(c + 1);
+        members.ensure(n);
+        kctl.ensure(1);
+        errflag.ensure(1);
+        scratch.ensure(std::max<int64_t>(c, 64));
+    }
+    bool small_k() const { return c <= 16; }
+    int tile_j() const { return 128; }
+    int tile_k() const { return small_k() ? 16 : 64; }
+
+    // ---- screened distances --------------------------------------------
+    void screen(const double* C) {
+        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p);
+        const int chunks = ceil_div(d, 32);
+        const int cps = ceil_div(chunks, nsplit);
+        dim3 grid(ceil_div(n, tile_j()), ceil_div(c, tile_k()), nsplit);
+        if (small_k()) {
+            constexpr int RJ = 4, RK = 2, NTJ = 32, NTK = 8;
+            const size_t sm = sizeof(T) * 2 * 32 * (RJ * NTJ + (sizeof(T) == 8 ? 2 : 4)) +
+                              sizeof(double) * 2 * 32 * (RK * NTK + 2);
+            auto kf = k_dist_screen<T, RJ, RK, NTJ, NTK>;
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kf<<<grid, NTJ * NTK, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
+        } else {
+            constexpr int RJ = 4, RK = 8, NTJ = 32, NTK = 8;
+            const size_t sm = sizeof(T) * 2 * 32 * (RJ * NTJ + (sizeof(T) == 8 ? 2 : 4)) +
+                              sizeof(double) * 2 * 32 * (RK * NTK + 2);
+            auto kf = k_dist_screen<T, RJ, RK, NTJ, NTK>;
+            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+            kf<<<grid, NTJ * NTK, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
+        }
+        ln.add(2);
+    }
+    Screen screen_view() const {
+        Screen s;
+        s.part = part.p;
+        s.xxp = xxp.p;
+        s.cc = cc.p;
+        s.nsplit = nsplit;
+        s.n = n;
+        s.c = c;
+        s.kappa_d = (2.0 * (double)d + 8.0) * kU * 1.05;
+        return s;
+    }
+
+    // decide (+ exact fallback for ambiguous columns); returns #ambiguous
+    void decide(const double* C, const int* old_labels, const int* cnts, int mode, int* out_labels,
+                Ctl* ctl) {
+        k_decide<<<ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(screen_view(), n, c, old_labels,
+                                                                 cnts, mode, out_labels, amb.p,
+                                                                 ctl);
+        k_exact_cols<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous,
+                                                             exact.p);
+        k_redecide<<<std::min(ceil_div((int64_t)n * 32, 256), 4 * 148), 256, 0, st>>>(
+            exact.p, c, amb.p, &ctl->ambiguous, old_labels, cnts, mode, out_labels, ctl);
+        ln.add(3);
+    }
+
+    // assign_nearest (kmeans.cpp:21-37) → labels (device)
+    void assign(const double* C, int* labels) {
+        CK(cudaMemsetAsync(kctl.p, 0, sizeof(Ctl), st));
+        screen(C);
+        decide(C, nullptr, nullptr, 0, labels, kctl.p);
+        Ctl h;
+        CK(cudaMemcpyAsync(&h, kctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (stats) stats->exact_fallbacks += h.ambiguous;
+    }
+
+    void fetch_labels(const int* labels) {
+        h_labels.resize(n);
+        CK(cudaMemcpyAsync(h_labels.data(), labels, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    }
+    void upload_groups() {
+        CK(cudaMemcpyAsync(goff.p, groups.goff.data(), sizeof(int) * (c + 1),
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(members.p, groups.members.data(), sizeof(int) * n,
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
+                           cudaMemcpyHostToDevice, st));
+    }
+
+    // repair_empty (kmeans.cpp:40-64); labels device, h_labels must be current
+    void repair_if_needed(const double* C, int* labels) {
+        groups.build(h_labels.data(), n, c);
+        bool empty = false;
+        for (int k = 0; k < c; ++k) empty |= groups.counts[k] == 0;
+        if (!empty) return;
+        CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
+                           cudaMemcpyHostToDevice, st));
+        k_own_exact<T><<<ceil_div(n, 128), 128, 0, st>>>(M, C, d, n, labels, own.p);
+        CK(cudaMemsetAsync(errflag.p, 0, sizeof(int), st));
+        k_repair<T><<<1, 1024, 0, st>>>(M, C, d, n, c, labels, counts.p, own.p, errflag.p);
+        ln.add(2);
+        int e = 0;
+        CK(cudaMemcpyAsync(&e, errflag.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+        fetch_labels(labels);
+        if (e) throw RuntimeErr("kmeans: cannot repair empty cluster");
+    }
+
+    // means_of (kmeans.cpp:66-82) for the labels in h_labels → Cout
+    void means(double* Cout) {
+        groups.build(h_labels.data(), n, c);
+        upload_groups();
+        launch_group_mean(Cout);
+    }
+    void launch_group_mean(double* Cout) {
+        const bool r2 = (d % 2 == 0);
+        const int rb = ceil_div(d, 256 * (r2 ? 2 : 1));
+        if (r2)
+            k_group_sum<T, 2, 1><<<rb * c, 256, 0, st>>>(M, nullptr, nullptr, goff.p, members.p,
+                                                       nullptr, Cout, nullptr, 0, 1, d, rb);
+        else
+            k_group_sum<T, 1, 1><<<rb * c, 256, 0, st>>>(M, nullptr, nullptr, goff.p, members.p,
+                                                       nullptr, Cout, nullptr, 0, 1, d, rb);
+        ln.add();
+    }
+
+    // Lloyd stop (kmeans.cpp:148-158): sqrt(moved) <= tol * max(sqrt(scale), 1e-300)
+    bool stop_test(const double* nxt, const double* C, double tol) {
+        const int64_t N = d * (int64_t)c;
+        const int blocks = std::min(512, ceil_div(N, 256));
+        k_moved_scale<<<blocks, 256, 0, st>>>(nxt, C, N, msp.p);
+        k_sum_partials<<<1, 256, 0, st>>>(msp.p, blocks, 2, msp.p + 2 * 512);
+        ln.add(2);
+        double h[2];
+        CK(cudaMemcpyAsync(h, msp.p + 2 * 512, sizeof(h), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        auto verdict = [&](double moved, double scale, double& margin) {
+            const double s = std::sqrt(scale);
+            const double thr = tol * std::max(s, 1e-300);
+            const double m = std::sqrt(moved);
+            margin = std::fabs(m - thr) / std::max(thr, 1e-300);
+            return m <= thr;
+        };
+        double margin;
+        bool v = verdict(h[0], h[1], margin);
+        if (margin < 1e-9 && h[0] != 0.0) {  // too close for a tree sum: reference chain
+            k_moved_scale_exact<<<1, 32, 0, st>>>(nxt, C, N, msp.p + 2 * 512);
+            ln.add();
+            CK(cudaMemcpyAsync(h, msp.p + 2 * 512, sizeof(h), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            v = verdict(h[0], h[1], margin);
+        }
+        return v;
+    }
+
+    // lloyd_run (kmeans.cpp:141-168).  C: in = start centroids, out = final
+    // means; labels: device out.  Returns iters_run.
+    uint64_t lloyd_run(double* C, int* labels, uint64_t max_iters, double tol) {
+        if (max_iters == 0) throw InvalidArg("kmeans: max_iters must be >= 1");
+        uint64_t it = 0;
+        double* cur = C;
+        double* nxt = nextC.p;
+        for (; it < max_iters; ++it) {
+            assign(cur, labels);
+            fetch_labels(labels);
+            repair_if_needed(cur, labels);
+            means(nxt);
+            if (stats) stats->lloyd_steps++;
+            const bool stop = stop_test(nxt, cur, tol);
+            std::swap(cur, nxt);
+            if (stop) {
+                ++it;
+                break;
+            }
+        }
+        if (cur != C) CK(cudaMemcpyAsync(C, cur, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        hartigan(C, labels);
+        fetch_labels(labels);
+        groups.build(h_labels.data(), n, c);
+        for (int k = 0; k < c; ++k)
+            if (groups.counts[k] == 0) throw InvalidArg("GroupAssignment: empty group");
+        means(C);  // drop incremental rounding (kmeans.cpp:161)
+        return it;
+    }
+
+    // hartigan_refine (kmeans.cpp:96-139), exact sequential semantics
+    void hartigan(double* C, int* labels) {
+        if (c <= 1) return;  // no candidate target: never moves
+        groups.build(h_labels.data(), n, c);
+        CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
+                           cudaMemcpyHostToDevice, st));
+        approx.ensure((size_t)n * c);
+        err.ensure((size_t)n * c);
+        stamp.ensure((size_t)n * c);
+        modver.ensure(c);
+        xx.ensure(n);
+        hs.ensure(1);
+        k_col_sq_fma_T(M, n, xx.p);
+        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p);
+        CK(cudaMemsetAsync(stamp.p, 0xff, sizeof(int) * (size_t)n * c, st));  // all stale
+        CK(cudaMemsetAsync(modver.p, 0, sizeof(int) * c, st));
+        CK(cudaMemsetAsync(hs.p, 0, sizeof(HartState), st));
+        ln.add(2);
+        const int W = 128;
+        const double kappa_d = (2.0 * (double)d + 8.0) * kU * 1.05;
+        dim3 rg(W, ceil_div(c, 8));
+        scratch.ensure(std::max(c, 64));
+        HartState* h = hst.ensure<HartState>(1);
+        for (;;) {
+            for (int r = 0; r < 64; ++r) {
+                k_hart_refresh<T><<<rg, 256, 0, st>>>(M, C, cc.p, xx.p, d, n, c, W, hs.p,
+                                                      modver.p, stamp.p, approx.p, err.p, kappa_d);
+                k_hart_step<T><<<1, 1024, 0, st>>>(M, C, cc.p, d, n, c, W, hs.p, modver.p,
+                                                   stamp.p, approx.p, err.p, labels, counts.p,
+                                                   scratch.p, 50, 0, cudaGraphConditionalHandle{});
+            }
+            ln.add(128);
+            CK(cudaMemcpyAsync(h, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            if (h->done) break;
+        }
+        if (stats) {
+            stats->hartigan_moves += h->moves;
+            stats->exact_fallbacks += h->exact_fallbacks;
+            stats->hartigan_passes += (uint64_t)h->pass + 1;
+        }
+    }
+
+    void k_col_sq_fma_T(const T* m, int cols, double* out);
+
+    // inertia_of (kmeans.cpp:84-91): exact per-column chains, sequential host sum
+    double inertia(const double* C, const int* labels) {
+        k_own_exact<T><<<ceil_div(n, 128), 128, 0, st>>>(M, C, d, n, labels, own.p);
+        ln.add();
+        std::vector<double> h(n);
+        CK(cudaMemcpyAsync(h.data(), own.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        double s = 0.0;
+        for (int j = 0; j < n; ++j) s += h[j];
+        return s;
+    }
+
+    // kmeans_pp_init (kmeans.cpp:172-224); RNG stays on the host (libstdc++)
+    std::vector<int> pp_init(std::mt19937_64& rng) {
+        if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
+        if ((int64_t)c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
+        std::vector<int> chosen;
+        std::vector<char> is_chosen(n, 0);
+        std::uniform_int_distribution<std::size_t> first(0, (std::size_t)n - 1);
+        chosen.push_back((int)first(rng));
+        is_chosen[chosen[0]] = 1;
+        d2.ensure(n);
+        std::vector<double> hd2(n, std::numeric_limits<double>::infinity());
+        CK(cudaMemcpyAsync(d2.p, hd2.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
+        while ((int)chosen.size() < c) {
+            const int last = chosen.back();
+            k_pp_d2<T><<<ceil_div(n, 128), 128, 0, st>>>(M, d, n, last, d2.p);
+            ln.add();
+            CK(cudaMemcpyAsync(hd2.data(), d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            double total = 0.0;
+            for (int j = 0; j < n; ++j) total += hd2[j];
+            int pick = n;
+            if (total > 0.0) {
+                std::uniform_real_distribution<double> u(0.0, total);
+                double r = u(rng);
+                for (int j = 0; j < n; ++j) {
+                    r -= hd2[j];
+                    if (r <= 0.0 && !is_chosen[j]) {
+                        pick = j;
+                        break;
+                    }
+                }
+            }
+            if (pick == n) {
+                for (int j = 0; j < n; ++j)
+                    if (!is_chosen[j]) {
+                        pick = j;
+                        break;
+                    }
+            }
+            chosen.push_back(pick);
+            is_chosen[pick] = 1;
+        }
+        return chosen;
+    }
+
+    void gather(const std::vector<int>& idx, double* C) {
+        gidx.ensure(c);
+        CK(cudaMemcpyAsync(gidx.p, idx.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
+        k_gather_cols<T><<<dim3(ceil_div(d, 256 * 4), c), 256, 0, st>>>(M, d, gidx.p, c, C);
+        ln.add();
+    }
+
+    // kmeans (kmeans.cpp:237-250).  labels/C device outputs.
+    void kmeans(uint64_t max_iters, uint64_t n_restarts, uint64_t seed, double tol, int* labels,
+                double* C, double* inertia_out, uint64_t* iters_out) {
+        if (c == 0) throw InvalidArg("kmeans: c must be >= 1");
+        if ((int64_t)c > n) throw InvalidArg("kmeans: c exceeds column count");
+        std::mt19937_64 rng(seed);
+        double best = std::numeric_limits<double>::infinity();
+        DBuf<int> lab;
+        DBuf<double> cen;
+        lab.ensure(n);
+        cen.ensure((size_t)d * c);
+        bool have = false;
+        for (uint64_t r = 0; r < n_restarts; ++r) {
+            const std::vector<int> chosen = pp_init(rng);
+            gather(chosen, cen.p);
+            const uint64_t it = lloyd_run(cen.p, lab.p, max_iters, tol);
+            const double in = inertia(cen.p, lab.p);
+            if (in < best) {
+                best = in;
+                have = true;
+                CK(cudaMemcpyAsync(labels, lab.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+                CK(cudaMemcpyAsync(C, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+                if (inertia_out) *inertia_out = in;
+                if (iters_out) *iters_out = it;
+            }
+        }
+        CK(cudaStreamSynchronize(st));
+        if (!have && n_restarts > 0) {
+            // every restart had a NaN inertia: the reference returns the
+            // default-constructed result; mirror that as an error
+            throw RuntimeErr("kmeans: no restart produced a finite inertia");
+        }
+    }
+};
+
+template <typename T>
+__global__ void k_colsq_T(const T* __restrict__ M, int64_t d, double* __restrict__ out) {
+    __shared__ double red[32];
+    const int j = blockIdx.x;
+    double s = 0.0;
+    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
+        const double v = (double)M[(int64_t)j * d + i];
+        s = __fma_rn(v, v, s);
+    }
+    double v[1] = {s};
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) out[j] = v[0];
+}
+
+template <typename T>
+void KMeansEngine<T>::k_col_sq_fma_T(const T* m, int cols, double* out) {
+    k_colsq_T<T><<<cols, 256, 0, st>>>(m, d, out);
+    ln.add();
+}
+
+}  // namespace respca_host
