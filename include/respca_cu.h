@@ -140,6 +140,13 @@ int respca_cu_column_l2_norms(respca_cu_ctx* ctx, const double* m, uint64_t d, u
 int respca_cu_column_mean(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
                           const uint64_t* cols, uint64_t ncols, double* out);
 
+/* Test hook: the screened K-means distance of every (column j, centroid k)
+ * pair and the rigorous half-width of its interval around the reference's
+ * sq_dist (kmeans.cpp:12-19); row-major n×c outputs. */
+int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                           const double* centroids, uint64_t c, double* approx_out,
+                           double* err_out);
+
 /* --- benchmark hooks (device-resident state, no host copies) ------------- */
 /* Upload X and run validation + the one-time initial clustering; leaves the
  * context ready to step the ALM loop.  init_ms receives the device time. */

@@ -57,7 +57,7 @@ EXPORTS = [
     "respca_cu_kmeans_pp_init", "respca_cu_lloyd_step", "respca_cu_group_scatter",
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
-    "respca_cu_bench_steps",
+    "respca_cu_bench_steps", "respca_cu_debug_screen",
 ]
 
 
@@ -106,6 +106,7 @@ def lib() -> C.CDLL:
             L.respca_cu_bench_prepare.argtypes = [vp, vp, u64, u64, C.c_int, C.POINTER(CConfig),
                                                   dptr]
             L.respca_cu_bench_steps.argtypes = [vp, u64, dptr, dptr, dptr, u64ptr]
+            L.respca_cu_debug_screen.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             _lib = L
         return _lib
 

@@ -6,7 +6,10 @@
 //        -Xcompiler -fPIC -shared engine.cu -o librespca_cu.so
 // --fmad=false is load-bearing: it makes the device arithmetic the reference's
 // (no FMA contraction, solver.cpp / kmeans.cpp compiled for baseline x86-64).
+#include <cuda_profiler_api.h>
+
 #include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -348,6 +351,11 @@ struct Alm : AlmBase {
         std::vector<Events> evf(iters), eva(iters);
         Events all;
         uint64_t remaining = iters, nslow = 0;
+        // RESPCA_PROFILE_TIMED=1: scope an `ncu --profile-from-start off` capture
+        // to exactly the timed iterations
+        const char* prof = std::getenv("RESPCA_PROFILE_TIMED");
+        const bool profiling = prof && prof[0] == '1' && iters > 1;
+        if (profiling) CK(cudaProfilerStart());
         double fsum = 0.0, asum = 0.0;
         CK(cudaEventRecord(all.a, st));
         while (remaining > 0) {
@@ -378,6 +386,7 @@ struct Alm : AlmBase {
         }
         CK(cudaEventRecord(all.b, st));
         CK(cudaEventSynchronize(all.b));
+        if (profiling) CK(cudaProfilerStop());
         for (uint64_t t = 0; t < iters; ++t) {
             fsum += evf[t].ms();
             asum += eva[t].ms();
@@ -931,6 +940,28 @@ int respca_cu_l21_norm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t
         double s = 0.0;
         for (uint64_t j = 0; j < n; ++j) s += nr[j];
         *out = s;
+    });
+}
+
+int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                           const double* centroids, uint64_t c, double* approx_out,
+                           double* err_out) {
+    return guarded(ctx, [&] {  // test hook: the screened distance and its bound
+        check_dims(d, n);
+        KMeansEngine<double> km;
+        Dev64 dm, dc;
+        km_common(ctx, km, dm, m, d, n, c);
+        const double* C = dc.up(ctx->st, centroids, d * c);
+        km.screen(C);
+        DBuf<double> a, e;
+        a.ensure(n * c);
+        e.ensure(n * c);
+        k_screen_dump<<<ceil_div((int64_t)n * c, 256), 256, 0, ctx->st>>>(km.screen_view(), (int)n,
+                                                                          (int)c, a.p, e.p);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(approx_out, a.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(err_out, e.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
     });
 }
 

@@ -178,6 +178,154 @@ __global__ void __launch_bounds__(NTJ* NTK) k_dist_screen(const T* __restrict__ 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Screened distance GEMM on the FP64 tensor cores (DMMA, mma.sync m8n8k4 f64):
+//   part[s][j][k] = Σ_{i∈split s} M[i,j]·C[i,k],   xxp[s][j] = Σ_{i∈split s} M[i,j]²
+// A = Mᵀ (rows j, K = i) and B = C (K = i, cols k) are both staged in shared
+// memory in their global (i-contiguous) layout by 16-byte cp.async — no
+// transposes — with a row stride of 36 elements, which makes every fragment
+// load (lane → row lane/4, k lane%4) conflict-free.  CTA = 8 warps, tile
+// 128 (j) × TK (k); warp tile (MJ·8) × (NK·8); K-chunks of 32 rows, 2 stages.
+// ---------------------------------------------------------------------------
+RESPCA_DEV void dmma884(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+RESPCA_DEV void cp_async16(void* smem, const void* gmem, int bytes) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+
+template <typename T, int WK, int MJ, int NK>
+__global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
+                                                     const double* __restrict__ C, int64_t d,
+                                                     int n, int c, int chunks_per_split,
+                                                     double* __restrict__ part,
+                                                     double* __restrict__ xxp) {
+    constexpr int NW = 8, WJ = NW / WK;
+    constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8, KI = 32;
+    constexpr int AS = 36;  // row stride (elements) of both smem tiles
+    constexpr int EPV = 16 / sizeof(T);  // elements per 16-byte copy
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    T* As = reinterpret_cast<T*>(smem_raw);  // [2][TJ][AS]
+    double* Bs = reinterpret_cast<double*>(smem_raw + sizeof(T) * 2 * TJ * AS);  // [2][TK][AS]
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wj = warp / WK, wk = warp % WK;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int j0 = blockIdx.x * TJ, k0 = blockIdx.y * TK, split = blockIdx.z;
+    const int64_t ibeg = (int64_t)split * chunks_per_split * KI;
+    int64_t iend = ibeg + (int64_t)chunks_per_split * KI;
+    if (iend > d) iend = d;
+    const int nch = ibeg < iend ? (int)((iend - ibeg + KI - 1) / KI) : 0;
+    // 16-byte copies need 16-byte aligned global rows: true when d is a
+    // multiple of 16/sizeof(T); otherwise fall back to element copies.
+    const bool vec_ok = (d % EPV) == 0;
+
+    auto load = [&](int64_t i0, int buf) {
+        T* adst = As + buf * TJ * AS;
+        double* bdst = Bs + buf * TK * AS;
+        if (vec_ok) {
+            constexpr int AV = KI / EPV;  // 16-byte vectors per row chunk
+            for (int e = tid; e < TJ * AV; e += 256) {
+                const int row = e / AV, v = e - row * AV;
+                const int j = j0 + row;
+                const int64_t i = i0 + v * EPV;
+                int bytes = 0;
+                if (j < n && i < iend) bytes = (int)(sizeof(T) * ((iend - i) < EPV ? (iend - i) : EPV));
+                cp_async16(adst + row * AS + v * EPV, bytes ? M + (int64_t)j * d + i : M, bytes);
+            }
+            for (int e = tid; e < TK * (KI / 2); e += 256) {
+                const int row = e / (KI / 2), v = e - row * (KI / 2);
+                const int k = k0 + row;
+                const int64_t i = i0 + v * 2;
+                int bytes = 0;
+                if (k < c && i < iend) bytes = (int)(8 * ((iend - i) < 2 ? (iend - i) : 2));
+                cp_async16(bdst + row * AS + v * 2, bytes ? C + (int64_t)k * d + i : C, bytes);
+            }
+        } else {
+            for (int e = tid; e < TJ * KI; e += 256) {
+                const int row = e / KI, ii = e - row * KI;
+                const int j = j0 + row;
+                const int64_t i = i0 + ii;
+                const bool p = j < n && i < iend;
+                if (sizeof(T) == 8) cp_async8(adst + row * AS + ii, p ? M + (int64_t)j * d + i : M, p);
+                else cp_async4(adst + row * AS + ii, p ? M + (int64_t)j * d + i : M, p);
+            }
+            for (int e = tid; e < TK * KI; e += 256) {
+                const int row = e / KI, ii = e - row * KI;
+                const int k = k0 + row;
+                const int64_t i = i0 + ii;
+                const bool p = k < c && i < iend;
+                cp_async8(bdst + row * AS + ii, p ? C + (int64_t)k * d + i : C, p);
+            }
+        }
+        cp_commit();
+    };
+
+    double acc[MJ][NK][2];
+#pragma unroll
+    for (int a = 0; a < MJ; ++a)
+#pragma unroll
+        for (int b = 0; b < NK; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+    double xx[MJ];
+#pragma unroll
+    for (int a = 0; a < MJ; ++a) xx[a] = 0.0;
+
+    if (nch > 0) load(ibeg, 0);
+    for (int ch = 0; ch < nch; ++ch) {
+        if (ch + 1 < nch) {
+            load(ibeg + (int64_t)(ch + 1) * KI, (ch + 1) & 1);
+            cp_wait<1>();
+        } else {
+            cp_wait<0>();
+        }
+        __syncthreads();
+        const T* as = As + (ch & 1) * TJ * AS + (wj * MJ * 8 + g) * AS + t4;
+        const double* bs = Bs + (ch & 1) * TK * AS + (wk * NK * 8 + g) * AS + t4;
+#pragma unroll
+        for (int kk = 0; kk < KI; kk += 4) {
+            double a[MJ], b[NK];
+#pragma unroll
+            for (int x = 0; x < MJ; ++x) a[x] = (double)as[x * 8 * AS + kk];
+#pragma unroll
+            for (int y = 0; y < NK; ++y) b[y] = bs[y * 8 * AS + kk];
+#pragma unroll
+            for (int x = 0; x < MJ; ++x)
+#pragma unroll
+                for (int y = 0; y < NK; ++y) dmma884(acc[x][y][0], acc[x][y][1], a[x], b[y]);
+            if (wk == 0)
+#pragma unroll
+                for (int x = 0; x < MJ; ++x) xx[x] = __fma_rn(a[x], a[x], xx[x]);
+        }
+        __syncthreads();
+    }
+    // epilogue: D[row g][col 2·t4 + {0,1}] of every 8×8 tile
+#pragma unroll
+    for (int x = 0; x < MJ; ++x) {
+        const int j = j0 + (wj * MJ + x) * 8 + g;
+        if (j >= n) continue;
+        double* dst = part + ((int64_t)split * n + j) * c;
+#pragma unroll
+        for (int y = 0; y < NK; ++y) {
+            const int k = k0 + (wk * NK + y) * 8 + 2 * t4;
+            if (k < c) dst[k] = acc[x][y][0];
+            if (k + 1 < c) dst[k + 1] = acc[x][y][1];
+        }
+    }
+    if (wk == 0) {
+#pragma unroll
+        for (int x = 0; x < MJ; ++x) {
+            double v = xx[x];
+            v += __shfl_xor_sync(0xffffffffu, v, 1);
+            v += __shfl_xor_sync(0xffffffffu, v, 2);
+            const int j = j0 + (wj * MJ + x) * 8 + g;
+            if (t4 == 0 && j < n && blockIdx.y == 0) xxp[(int64_t)split * n + j] = v;
+        }
+    }
+}
+
 // Screened distance of (j, k) from the split partials (fixed split order).
 struct Screen {
     const double* part;
@@ -206,6 +354,19 @@ struct Screen {
         }
     }
 };
+
+// debug/test: materialise the screened intervals (approx, half-width)
+__global__ void k_screen_dump(Screen sc, int n, int c, double* __restrict__ approx,
+                              double* __restrict__ err) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)n * c) return;
+    const int j = (int)(e / c), k = (int)(e % c);
+    const double xxj = sc.xx(j);
+    double lo, hi, mid;
+    sc.get(j, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
+    approx[e] = mid;
+    err[e] = hi - mid;
+}
 
 // warp-wide lexicographic argmin on (value, index)
 RESPCA_DEV void warp_argmin(double& v, int& k) {

@@ -69,7 +69,7 @@ struct KMeansEngine {
         // split-K for the screen: aim for >= 2 CTAs per SM
         const int tiles = ceil_div(n, tile_j()) * ceil_div(c, tile_k());
         const int chunks = ceil_div(d, 32);
-        nsplit = std::max(1, std::min(chunks / 4, ceil_div(296, tiles)));
+        nsplit = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
         nsplit = std::min(nsplit, 32);
         part.ensure((size_t)nsplit * n * c);
         xxp.ensure((size_t)nsplit * n);
@@ -87,9 +87,21 @@ struct KMeansEngine {
         errflag.ensure(1);
         scratch.ensure(std::max<int64_t>(c, 64));
     }
-    bool small_k() const { return c <= 16; }
+    // CTA tile of the DMMA screen: 128 columns × TK centroids
+    int tk_tile() const { return c > 32 ? 64 : (c > 16 ? 32 : (c > 8 ? 16 : 8)); }
     int tile_j() const { return 128; }
-    int tile_k() const { return small_k() ? 16 : 64; }
+    int tile_k() const { return tk_tile(); }
+
+    template <int WK, int MJ, int NK>
+    void launch_dmma(const double* C, dim3 grid, int cps) {
+        constexpr int NW = 8, WJ = NW / WK;
+        constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8;
+        static_assert(TJ == 128, "tile");
+        const size_t sm = sizeof(T) * 2 * TJ * 36 + sizeof(double) * 2 * TK * 36;
+        auto kf = k_dist_dmma<T, WK, MJ, NK>;
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        kf<<<grid, 256, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
+    }
 
     // ---- screened distances --------------------------------------------
     void screen(const double* C) {
@@ -97,23 +109,18 @@ struct KMeansEngine {
         const int chunks = ceil_div(d, 32);
         const int cps = ceil_div(chunks, nsplit);
         dim3 grid(ceil_div(n, tile_j()), ceil_div(c, tile_k()), nsplit);
-        if (small_k()) {
-            constexpr int RJ = 4, RK = 2, NTJ = 32, NTK = 8;
-            const size_t sm = sizeof(T) * 2 * 32 * (RJ * NTJ + (sizeof(T) == 8 ? 2 : 4)) +
-                              sizeof(double) * 2 * 32 * (RK * NTK + 2);
-            auto kf = k_dist_screen<T, RJ, RK, NTJ, NTK>;
-            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            kf<<<grid, NTJ * NTK, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
-        } else {
-            constexpr int RJ = 4, RK = 8, NTJ = 32, NTK = 8;
-            const size_t sm = sizeof(T) * 2 * 32 * (RJ * NTJ + (sizeof(T) == 8 ? 2 : 4)) +
-                              sizeof(double) * 2 * 32 * (RK * NTK + 2);
-            auto kf = k_dist_screen<T, RJ, RK, NTJ, NTK>;
-            CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-            kf<<<grid, NTJ * NTK, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
+        switch (tk_tile()) {
+            case 64: launch_dmma<2, 4, 4>(C, grid, cps); break;  // warps 4×2, warp 32×32
+            case 32: launch_dmma<1, 2, 4>(C, grid, cps); break;  // warps 8×1, warp 16×32
+            case 16: launch_dmma<1, 2, 2>(C, grid, cps); break;
+            default: launch_dmma<1, 2, 1>(C, grid, cps); break;
         }
         ln.add(2);
     }
+    // bound factor of the screen (see km.cuh): γ-bounds of the length-d
+    // chains of both the screen (FMA / DMMA accumulation, counted as 2 roundings
+    // per step for safety) and the reference's sequential chain, plus slack
+    double kappa_screen() const { return (3.0 * (double)d + 16.0) * kU * 1.1; }
     Screen screen_view() const {
         Screen s;
         s.part = part.p;
@@ -122,7 +129,7 @@ struct KMeansEngine {
         s.nsplit = nsplit;
         s.n = n;
         s.c = c;
-        s.kappa_d = (2.0 * (double)d + 8.0) * kU * 1.05;
+        s.kappa_d = kappa_screen();
         return s;
     }
 
@@ -278,7 +285,7 @@ struct KMeansEngine {
         CK(cudaMemsetAsync(hs.p, 0, sizeof(HartState), st));
         ln.add(2);
         const int W = 128;
-        const double kappa_d = (2.0 * (double)d + 8.0) * kU * 1.05;
+        const double kappa_d = kappa_screen();
         dim3 rg(W, ceil_div(c, 8));
         scratch.ensure(std::max(c, 64));
         HartState* h = hst.ensure<HartState>(1);

@@ -140,9 +140,10 @@ def _up(a: np.ndarray):
 # solver (solver.hpp:67-88)
 # --------------------------------------------------------------------------
 def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
-          ctx: Optional[N.Context] = None) -> DecompositionResult:
+          ctx: Optional[N.Context] = None, out=None) -> DecompositionResult:
     """respca::solve (solver.cpp:127-210) on the device.  precision "f32" is
-    the API extension of the B200 build (fp32 storage, fp64 arithmetic)."""
+    the API extension of the B200 build (fp32 storage, fp64 arithmetic).
+    `out=(L, S)`: optional preallocated Fortran-ordered outputs (e.g. pinned)."""
     cfg = cfg or SolverConfig()
     ctx = _ctx(ctx)
     dt = np.float32 if precision == "f32" else np.float64
@@ -150,8 +151,14 @@ def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
     d, n = xm.shape
     budget = cfg.fixed_iters if cfg.fixed_iters is not None else cfg.max_iter
     budget = max(int(budget), 1)
-    L = np.empty((d, n), dtype=dt, order="F")
-    S = np.empty((d, n), dtype=dt, order="F")
+    if out is not None:
+        L, S = out
+        for a in (L, S):
+            if a.shape != (d, n) or a.dtype != dt or not a.flags.f_contiguous:
+                raise ValueError("solve: out arrays must be Fortran-ordered (d, n) of the dtype")
+    else:
+        L = np.empty((d, n), dtype=dt, order="F")
+        S = np.empty((d, n), dtype=dt, order="F")
     lab = np.empty(n, dtype=np.uint64)
     arrs = [np.zeros(budget) for _ in range(4)]
     rep = N.CReport()

@@ -50,9 +50,12 @@ def _ptr(a):
 
 
 def rpca(d: int, n: int, r: int, sigma: float, p: float, lo: float = -50.0, hi: float = 50.0,
-         seed: int = 42, with_truth: bool = False):
-    """X = U·Vᵀ + S0 (column-major (d, n) float64).  Returns X or (X, L0, S0)."""
-    X = np.empty((d, n), order="F")
+         seed: int = 42, with_truth: bool = False, out: np.ndarray | None = None):
+    """X = U·Vᵀ + S0 (column-major (d, n) float64).  Returns X or (X, L0, S0).
+    `out`: optional preallocated Fortran-ordered (d, n) float64 (e.g. pinned)."""
+    if out is not None:
+        assert out.shape == (d, n) and out.dtype == np.float64 and out.flags.f_contiguous
+    X = out if out is not None else np.empty((d, n), order="F")
     L0 = np.empty((d, n), order="F") if with_truth else None
     S0 = np.empty((d, n), order="F") if with_truth else None
     spec = _Rpca(d, n, r, sigma, p, lo, hi, seed)
@@ -92,11 +95,11 @@ class Workload:
     seed: int = 42
     extra: dict = field(default_factory=dict)
 
-    def make(self, with_truth: bool = False):
+    def make(self, with_truth: bool = False, out: np.ndarray | None = None):
         if self.kind == "video":
             return video(frames=self.n, seed=self.seed, with_truth=with_truth)
         return rpca(self.d, self.n, self.r, self.sigma, self.p, seed=self.seed,
-                    with_truth=with_truth)
+                    with_truth=with_truth, out=out)
 
     def solver_config(self, **over):
         from .respca import KMeansConfig, SolverConfig

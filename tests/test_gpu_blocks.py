@@ -186,3 +186,30 @@ def test_core_norms(ctx, orc, R):
                                rtol=1e-12)
     with pytest.raises(ValueError, match="empty column set"):
         R.column_mean(m, np.array([], dtype=np.uint64), ctx=ctx)
+
+
+def test_screen_bound_is_rigorous(ctx, orc):
+    """The screened distance interval always contains the reference's exact
+    sequential sq_dist (kmeans.cpp:12-19), across shapes, scales and dtypes of
+    the split-K DMMA kernel; decisions are only ever taken inside it."""
+    import ctypes as C
+
+    from paper_1904_07497_b200 import _native as N
+
+    rng = np.random.default_rng(21)
+    for d, n, c, scale in ((3, 40, 5, 1.0), (37, 130, 9, 1e3), (1000, 300, 50, 1e-3),
+                           (4096, 200, 64, 50.0), (333, 257, 17, 1.0), (64, 500, 100, 1.0)):
+        m = np.asfortranarray(rng.normal(0, scale, (d, n)))
+        Cm = np.asfortranarray(m[:, rng.choice(n, c, replace=False)] + rng.normal(0, scale * 1e-3, (d, c)))
+        a = np.empty(n * c)
+        e = np.empty(n * c)
+        N.check(ctx, N.lib().respca_cu_debug_screen(ctx.handle, m.ctypes.data_as(N.dptr), d, n,
+                                                    Cm.ctypes.data_as(N.dptr), c,
+                                                    a.ctypes.data_as(N.dptr),
+                                                    e.ctypes.data_as(N.dptr)))
+        a, e = a.reshape(n, c), e.reshape(n, c)
+        # exact sequential chains, the reference's order (numpy cumsum is sequential)
+        diff = m[:, :, None] - Cm[:, None, :]
+        exact = np.cumsum(diff * diff, axis=0)[-1]
+        assert (np.abs(exact - a) <= e).all(), (d, n, c, float(np.max(np.abs(exact - a) / e)))
+        assert (e <= 1e-9 * (np.abs(exact) + scale * scale * d)).all()
