@@ -124,6 +124,14 @@ int respca_cu_kmeans_warm(respca_cu_ctx* ctx, const double* m, uint64_t d, uint6
  * reference; a fresh engine with this seed reproduces its first call). */
 int respca_cu_kmeans_pp_init(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
                              uint64_t c, uint64_t seed, double* centroids_out);
+/* Same, drawing from the CALLER's engine through two callbacks (the
+ * reference's kmeans_pp_init advances the std::mt19937_64& it is given):
+ *   draw_first(user, n)   must return uniform_int_distribution<size_t>(0, n-1)(rng)
+ *   draw_real(user, total) must return uniform_real_distribution<double>(0, total)(rng) */
+int respca_cu_kmeans_pp_init_cb(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                                uint64_t c, uint64_t (*draw_first)(void*, uint64_t),
+                                double (*draw_real)(void*, double), void* user,
+                                double* centroids_out);
 int respca_cu_lloyd_step(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
                          const double* centroids, uint64_t c, uint64_t* labels_out,
                          double* next_out);

@@ -46,7 +46,7 @@ class CReport(C.Structure):
 
 
 _lib = None
-_lock = threading.Lock()
+_lock = threading.RLock()
 
 # every symbol include/respca_cu.h declares (checked by tests/test_boundary.py)
 EXPORTS = [
@@ -57,7 +57,7 @@ EXPORTS = [
     "respca_cu_kmeans_pp_init", "respca_cu_lloyd_step", "respca_cu_group_scatter",
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
-    "respca_cu_bench_steps", "respca_cu_debug_screen",
+    "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
 ]
 
 

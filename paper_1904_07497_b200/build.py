@@ -84,6 +84,8 @@ def build_oracle() -> None:
     """CPU checkers (test infrastructure): oracle/liboracle.so always; the
     reference library oracle/_ref/ only where /root/reference exists."""
     _run(["make", "-s", "-C", str(ROOT / "oracle"), "all"])
+    if Path("/root/reference/proj/tests/acceptance.cpp").exists():
+        _run(["make", "-s", "-C", str(ROOT / "oracle"), "acceptance"])
 
 
 def build_all(force: bool = False) -> None:

@@ -822,6 +822,30 @@ int respca_cu_kmeans_pp_init(respca_cu_ctx* ctx, const double* m, uint64_t d, ui
     });
 }
 
+int respca_cu_kmeans_pp_init_cb(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                                uint64_t c, uint64_t (*draw_first)(void*, uint64_t),
+                                double (*draw_real)(void*, double), void* user,
+                                double* centroids_out) {
+    return guarded(ctx, [&] {  // kmeans.cpp:172-224 with the caller's engine
+        check_dims(d, n);
+        if (!draw_first || !draw_real) throw InvalidArg("kmeans_pp_init: null draw callback");
+        if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
+        if (c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
+        KMeansEngine<double> km;
+        Dev64 dm;
+        km_common(ctx, km, dm, m, d, n, c);
+        const std::vector<int> ch = km.pp_init_with(
+            [&](uint64_t nn) { return draw_first(user, nn); },
+            [&](double total) { return draw_real(user, total); });
+        DBuf<double> cen;
+        cen.ensure(d * c);
+        km.gather(ch, cen.p);
+        CK(cudaMemcpyAsync(centroids_out, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToHost,
+                           ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+    });
+}
+
 int respca_cu_lloyd_step(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
                          const double* centroids, uint64_t c, uint64_t* labels_out,
                          double* next_out) {

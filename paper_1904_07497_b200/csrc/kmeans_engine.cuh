@@ -325,12 +325,27 @@ struct KMeansEngine {
 
     // kmeans_pp_init (kmeans.cpp:172-224); RNG stays on the host (libstdc++)
     std::vector<int> pp_init(std::mt19937_64& rng) {
+        return pp_init_with(
+            [&](uint64_t nn) {
+                std::uniform_int_distribution<std::size_t> first(0, (std::size_t)nn - 1);
+                return (uint64_t)first(rng);
+            },
+            [&](double total) {
+                std::uniform_real_distribution<double> u(0.0, total);
+                return u(rng);
+            });
+    }
+    // draw_first(n) = uniform_int_distribution<size_t>(0, n-1)(rng);
+    // draw_real(total) = uniform_real_distribution<double>(0, total)(rng)
+    template <class FirstFn, class RealFn>
+    std::vector<int> pp_init_with(FirstFn&& draw_first, RealFn&& draw_real) {
         if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
         if ((int64_t)c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
         std::vector<int> chosen;
         std::vector<char> is_chosen(n, 0);
-        std::uniform_int_distribution<std::size_t> first(0, (std::size_t)n - 1);
-        chosen.push_back((int)first(rng));
+        const uint64_t f0 = draw_first((uint64_t)n);
+        if (f0 >= (uint64_t)n) throw InvalidArg("kmeans_pp_init: draw out of range");
+        chosen.push_back((int)f0);
         is_chosen[chosen[0]] = 1;
         d2.ensure(n);
         std::vector<double> hd2(n, std::numeric_limits<double>::infinity());
@@ -345,8 +360,7 @@ struct KMeansEngine {
             for (int j = 0; j < n; ++j) total += hd2[j];
             int pick = n;
             if (total > 0.0) {
-                std::uniform_real_distribution<double> u(0.0, total);
-                double r = u(rng);
+                double r = draw_real(total);
                 for (int j = 0; j < n; ++j) {
                     r -= hd2[j];
                     if (r <= 0.0 && !is_chosen[j]) {
