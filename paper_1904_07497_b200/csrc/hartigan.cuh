@@ -1,0 +1,343 @@
+// Exact sequential Hartigan refinement (kmeans.cpp:96-139) on the device.
+//
+// The reference visits columns j = 0..n−1 in order and applies each improving
+// single-point move at once (incremental centroid update, kmeans.cpp:122-135),
+// so every later decision sees the updated centroids and counts.  The device
+// keeps exactly that order:
+//
+//  * columns are processed in blocks of B.  At block start, the screened
+//    distance of every (block column, centroid) pair is computed by the DMMA
+//    screen (km.cuh) — an interval [a − e, a + e] that provably contains the
+//    reference's sq_dist;
+//  * a round (one kernel, CTA per 8 block columns) first refreshes the two
+//    entries of every remaining column that the previous move made stale (its
+//    `from` and `to` centroids), computing the moved centroids' new values on
+//    the fly with the reference's exact update formula (and writing them to
+//    the other slot of a double-buffered centroid store); then one warp per
+//    column decides it on the intervals; the last CTA to finish takes the
+//    FIRST column that is not provably "no move" (all columns before it
+//    provably do not move in the sequential order): a provable move is applied,
+//    an undecidable near-tie is resolved with the exact sequential chain.
+//
+// Labels, counts and centroids are therefore bit-identical to the reference.
+// Rounds run as a CUDA-graph WHILE loop; blocks and passes are stream-ordered
+// and the host only synchronises once per pass.
+#pragma once
+
+#include "km.cuh"
+
+namespace respca_dev {
+
+struct HartState {
+    int cursor;        // next column to visit
+    int bend;          // end of the current block
+    int pass;          // 0..49
+    int improved;      // a move happened in this pass
+    int block_done;
+    int pending_from;  // centroid update of the last move, applied next round (-1: none)
+    int pending_to, pending_j, pending_nf, pending_nt;
+    int act_j;         // column the last CTA acts on
+    unsigned arrive;   // last-CTA election
+    unsigned long long first;  // packed (j, status, to) of the first non-trivial column
+    unsigned long long moves, exact_fallbacks, rounds;
+};
+
+struct HartArrays {
+    double* A;       // [n][c] screened distance
+    double* E;       // [n][c] its half-width
+    double* xx;      // [n]    ‖x_j‖² (screen input)
+    int* labels;
+    int* counts;
+    double* C;       // [2][c][d] centroid slots (slot 0 = the caller's centroids)
+    int* ver;        // [c] current slot of centroid k
+    double* scratch; // [c] exact distances of one column
+    double kappa_d;  // screen bound factor (km.cuh)
+};
+
+RESPCA_DEV double* cslot(const HartArrays& h, int c, int64_t d, int k, int s) {
+    return h.C + ((int64_t)s * c + k) * d;
+}
+
+// Hartigan decision of column j on intervals (one warp):
+//   0 = provably no move, 1 = provably moves to `to`, 2 = undecidable
+template <typename IV>
+RESPCA_DEV int hart_decide_warp(int j, int c, const int* __restrict__ labels,
+                                const int* __restrict__ counts, const IV& iv, int& to) {
+    const int lane = threadIdx.x & 31;
+    const int from = labels[j];
+    const int cf = counts[from];
+    if (cf <= 1) return 0;  // kmeans.cpp:105
+    double flo, fhi, fmid;
+    iv(from, flo, fhi, fmid);
+    const double na = (double)cf;
+    const double wa = na / (na - 1.0);  // kmeans.cpp:107-108
+    const double g_lo = wa * flo, g_hi = wa * fhi, g_mid = wa * fmid;
+    double bd = INFINITY;
+    int bk = 0x7fffffff;
+    bool none = true;
+    for (int k = lane; k < c; k += 32) {
+        if (k == from) continue;
+        double lo, hi, mid;
+        iv(k, lo, hi, mid);
+        const double nb = (double)counts[k];
+        const double wb = nb / (nb + 1.0);  // kmeans.cpp:113-115
+        none &= !(wb * lo - g_hi < -1e-12);
+        const double dmid = wb * mid - g_mid;
+        if (dmid < bd) {
+            bd = dmid;
+            bk = k;
+        }
+    }
+    none = __all_sync(0xffffffffu, none);
+    if (none) return 0;
+    warp_argmin(bd, bk);
+    if (bk >= c) return 2;
+    double blo, bhi, bmid;
+    iv(bk, blo, bhi, bmid);
+    const double nbk = (double)counts[bk];
+    const double dhi_k = (nbk / (nbk + 1.0)) * bhi - g_lo;
+    bool ok = dhi_k < -1e-12;  // kmeans.cpp:116 with best_delta = -1e-12
+    for (int k = lane; k < c; k += 32) {
+        if (k == from || k == bk) continue;
+        double lo, hi, mid;
+        iv(k, lo, hi, mid);
+        const double nb = (double)counts[k];
+        const double dlo = (nb / (nb + 1.0)) * lo - g_hi;
+        if (k < bk) ok &= dhi_k < dlo;  // an earlier k must lose strictly
+        else ok &= dhi_k <= dlo;        // a later k never replaces an equal delta
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) return 2;
+    to = bk;
+    return 1;
+}
+
+RESPCA_DEV unsigned long long pack_first(int j, int status, int to) {
+    return ((unsigned long long)(unsigned)j << 32) | ((unsigned long long)status << 24) |
+           (unsigned long long)(unsigned)(to & 0xffffff);
+}
+
+template <typename T, int CPB>
+__global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
+                                                    HartState* __restrict__ hs, HartArrays h,
+                                                    int64_t d, int n, int c,
+                                                    cudaGraphConditionalHandle cond) {
+    constexpr int NV = 2 + 2 * CPB;
+    __shared__ double red[32 * NV];
+    __shared__ bool s_last;
+    __shared__ int s_st, s_to;
+    if (hs->block_done) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        return;
+    }
+    const int cursor = hs->cursor, bend = hs->bend;
+    const int jb = cursor + blockIdx.x * CPB;  // first column of this CTA
+    const int pf = hs->pending_from;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // ---- phase 1: apply the pending move's centroid update (kmeans.cpp:126-131)
+    //      and refresh the (column, from/to) entries of this CTA's columns
+    if (pf >= 0) {
+        const int pt = hs->pending_to, pm = hs->pending_j;
+        const double dcf = (double)hs->pending_nf, dct = (double)hs->pending_nt;
+        const double na1 = (double)(hs->pending_nf - 1), nb1 = (double)(hs->pending_nt + 1);
+        const int vf = h.ver[pf], vt = h.ver[pt];
+        const double* of = cslot(h, c, d, pf, vf);
+        const double* ot = cslot(h, c, d, pt, vt);
+        double* nf_ = cslot(h, c, d, pf, 1 - vf);
+        double* nt_ = cslot(h, c, d, pt, 1 - vt);
+        const T* xm = M + (int64_t)pm * d;
+        const int64_t slice = (d + gridDim.x - 1) / gridDim.x;
+        const int64_t s0 = (int64_t)blockIdx.x * slice, s1 = s0 + slice;
+        bool active = false;
+        for (int q = 0; q < CPB; ++q) active |= (jb + q < bend);
+        double v[NV];
+#pragma unroll
+        for (int q = 0; q < NV; ++q) v[q] = 0.0;
+        const int64_t ibeg = active ? 0 : s0, iend = active ? d : (s1 < d ? s1 : d);
+#pragma unroll 4
+        for (int64_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) {
+            const double x = (double)xm[i];
+            const double cf = (of[i] * dcf - x) / na1;
+            const double ct = (ot[i] * dct + x) / nb1;
+            if (i >= s0 && i < s1) {
+                nf_[i] = cf;
+                nt_[i] = ct;
+            }
+            if (active) {
+                v[0] = __fma_rn(cf, cf, v[0]);
+                v[1] = __fma_rn(ct, ct, v[1]);
+#pragma unroll
+                for (int q = 0; q < CPB; ++q) {
+                    const int j = jb + q;
+                    if (j < bend) {
+                        const double xj = (double)__ldg(M + (int64_t)j * d + i);
+                        v[2 + 2 * q] = __fma_rn(xj, cf, v[2 + 2 * q]);
+                        v[3 + 2 * q] = __fma_rn(xj, ct, v[3 + 2 * q]);
+                    }
+                }
+            }
+        }
+        if (active) {  // block-uniform
+            block_sum<NV>(v, red);
+            if (threadIdx.x < 2 * CPB) {
+                const int q = threadIdx.x >> 1, which = threadIdx.x & 1;
+                const int j = jb + q;
+                if (j < bend) {
+                    const int k = which ? pt : pf;
+                    double dot = 0.0;
+#pragma unroll
+                    for (int r = 0; r < 2 * CPB; ++r)
+                        if (r == (int)threadIdx.x) dot = v[2 + r];
+                    const double cck = which ? v[1] : v[0];
+                    const double xxj = h.xx[j];
+                    const double mid = (xxj + cck) - 2.0 * dot;
+                    const double e = screen_err(h.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
+                    const int64_t idx = (int64_t)j * c + k;
+                    h.A[idx] = mid;
+                    h.E[idx] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- phase 2: decide this CTA's columns (warp per column)
+    if (warp < CPB) {
+        const int j = jb + warp;
+        if (j < bend) {
+            int to = -1;
+            auto iv = [&](int k, double& lo, double& hi, double& mid) {
+                const int64_t idx = (int64_t)j * c + k;
+                mid = h.A[idx];
+                const double e = h.E[idx];
+                lo = mid - e;
+                hi = mid + e;
+            };
+            const int st = hart_decide_warp(j, c, h.labels, h.counts, iv, to);
+            if (st != 0 && lane == 0) atomicMin(&hs->first, pack_first(j, st, to));
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        s_last = atomicAdd(&hs->arrive, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+
+    // ---- phase 3 (last CTA): settle the round
+    __threadfence();
+    if (threadIdx.x == 0) {
+        hs->arrive = 0;
+        hs->rounds += 1;
+        if (pf >= 0) {  // the new centroid values are complete: switch slots
+            h.ver[pf] ^= 1;
+            h.ver[hs->pending_to] ^= 1;
+            hs->pending_from = -1;
+        }
+        const unsigned long long f = hs->first;
+        hs->first = ~0ULL;
+        if (f == ~0ULL) {
+            s_st = -1;
+            hs->cursor = bend;
+        } else {
+            s_st = (int)((f >> 24) & 0xff);
+            s_to = (int)(f & 0xffffff);
+            hs->act_j = (int)(f >> 32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    if (s_st == 2) {  // near-tie: the reference's own sequential chain (kmeans.cpp:12-19)
+        const int j = hs->act_j;
+        const T* x = M + (int64_t)j * d;
+        for (int k = threadIdx.x; k < c; k += blockDim.x) {
+            const double* cv = cslot(h, c, d, k, h.ver[k]);
+            double s = 0.0;
+            for (int64_t i = 0; i < d; ++i) {
+                const double t = (double)x[i] - cv[i];
+                s += t * t;
+            }
+            h.scratch[k] = s;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            int to = -1;
+            auto iv = [&](int k, double& lo, double& hi, double& mid) {
+                mid = h.scratch[k];
+                lo = hi = mid;
+            };
+            const int st = hart_decide_warp(j, c, h.labels, h.counts, iv, to);
+            if (lane == 0) {
+                s_st = st;
+                s_to = to;
+                hs->exact_fallbacks += 1;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        if (s_st == 0) {
+            hs->cursor = hs->act_j + 1;
+        } else if (s_st == 1) {  // bookkeeping of the move (kmeans.cpp:132-135)
+            const int j = hs->act_j, from = h.labels[j], to = s_to;
+            const int nf = h.counts[from], nt = h.counts[to];
+            h.counts[from] = nf - 1;
+            h.counts[to] = nt + 1;
+            h.labels[j] = to;
+            hs->pending_j = j;
+            hs->pending_from = from;
+            hs->pending_to = to;
+            hs->pending_nf = nf;
+            hs->pending_nt = nt;
+            hs->improved = 1;
+            hs->moves += 1;
+            hs->cursor = j + 1;
+        }
+        const int done = hs->cursor >= bend && hs->pending_from < 0;
+        hs->block_done = done;
+        __threadfence();
+        cudaGraphSetConditional(cond, done ? 0u : 1u);
+    }
+}
+
+// block start: intervals of every (block column, centroid) pair from the screen
+__global__ void k_hart_fill(Screen sc, HartArrays h, int j0, int nb, int c) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= (int64_t)nb * c) return;
+    const int jl = (int)(e / c), k = (int)(e % c);
+    const double xxj = sc.xx(jl);
+    double lo, hi, mid;
+    sc.get(jl, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
+    const int64_t idx = (int64_t)(j0 + jl) * c + k;
+    h.A[idx] = mid;
+    h.E[idx] = isfinite(hi - mid) ? hi - mid : INFINITY;
+    if (k == 0) h.xx[j0 + jl] = xxj;
+}
+
+__global__ void k_hart_block_begin(HartState* hs, int b0, int bend) {
+    hs->cursor = b0;
+    hs->bend = bend;
+    hs->block_done = 0;
+    hs->first = ~0ULL;
+    hs->arrive = 0;
+}
+
+// copy centroids living in slot 1 back to slot 0 (the screen reads slot 0)
+__global__ void k_hart_consolidate(HartArrays h, int64_t d, int c) {
+    for (int k = blockIdx.y; k < c; k += gridDim.y) {
+        if (h.ver[k] == 0) continue;
+        const double* src = h.C + ((int64_t)c + k) * d;
+        double* dst = h.C + (int64_t)k * d;
+        for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
+             i += (int64_t)gridDim.x * blockDim.x)
+            dst[i] = src[i];
+    }
+}
+__global__ void k_hart_ver_reset(HartArrays h, int c) {
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
+        h.ver[k] = 0;
+}
+
+}  // namespace respca_dev

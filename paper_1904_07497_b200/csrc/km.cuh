@@ -739,272 +739,4 @@ __global__ void __launch_bounds__(1024) k_repair(const T* __restrict__ M,
     }
 }
 
-// ---------------------------------------------------------------------------
-// Exact sequential Hartigan refinement (kmeans.cpp:96-139) on the device.
-//
-// The reference visits columns j = 0..n−1 in order and applies each improving
-// single-point move immediately (incremental centroid update, kmeans.cpp:
-// 128-131), so every later decision sees the updated state.  The device
-// version keeps that order with windows: a round refreshes the screened
-// distances of the next W columns (only entries whose centroid changed since
-// they were computed, tracked by per-centroid version stamps), then one CTA
-// evaluates the window's columns in parallel against the current state and
-// takes the FIRST column that moves — all columns before it provably do not
-// move in the sequential order — applies that move exactly, and restarts the
-// window just after it.  Undecidable columns fall back to exact chains.
-// ---------------------------------------------------------------------------
-struct HartState {
-    int cursor;    // next column to visit in this pass
-    int pass;      // 0..49
-    int improved;  // a move happened in this pass
-    int done;
-    int movecount; // global version counter
-    unsigned long long moves, exact_fallbacks;
-};
-
-// refresh window entries: approx[j][k], err[j][k] for stale (j, k)
-template <typename T>
-__global__ void __launch_bounds__(256) k_hart_refresh(const T* __restrict__ M,
-                                                      const double* __restrict__ C,
-                                                      const double* __restrict__ cc,
-                                                      const double* __restrict__ xx, int64_t d,
-                                                      int n, int c, int W,
-                                                      const HartState* __restrict__ hs,
-                                                      const int* __restrict__ modver,
-                                                      int* __restrict__ stamp,
-                                                      double* __restrict__ approx,
-                                                      double* __restrict__ err, double kappa_d) {
-    constexpr int KB = 8;
-    __shared__ double red[32 * KB];
-    if (hs->done) return;
-    const int j = hs->cursor + blockIdx.x;
-    if (j >= n || blockIdx.x >= W) return;
-    const int kbase = blockIdx.y * KB;
-    if (kbase >= c) return;
-    const int mv = hs->movecount;
-    int stale_mask = 0;
-#pragma unroll
-    for (int q = 0; q < KB; ++q) {
-        const int k = kbase + q;
-        if (k < c && stamp[(int64_t)j * c + k] < modver[k]) stale_mask |= 1 << q;
-    }
-    if (!stale_mask) return;
-    const T* x = M + (int64_t)j * d;
-    double v[KB];
-#pragma unroll
-    for (int q = 0; q < KB; ++q) v[q] = 0.0;
-    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-        const double xi = (double)__ldg(x + i);
-#pragma unroll
-        for (int q = 0; q < KB; ++q)
-            if (stale_mask & (1 << q)) v[q] = __fma_rn(xi, C[(int64_t)(kbase + q) * d + i], v[q]);
-    }
-    block_sum<KB>(v, red);
-    if (threadIdx.x < KB && (stale_mask & (1 << threadIdx.x))) {
-        const int k = kbase + threadIdx.x;
-        double dot = 0.0;
-#pragma unroll
-        for (int q = 0; q < KB; ++q)
-            if (q == (int)threadIdx.x) dot = v[q];
-        const double xxj = xx[j];
-        const double mid = (xxj + cc[k]) - 2.0 * dot;
-        const double e = screen_err(kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cc[k])), mid);
-        approx[(int64_t)j * c + k] = mid;
-        err[(int64_t)j * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
-        stamp[(int64_t)j * c + k] = mv;
-    }
-}
-
-// one CTA: decide the window, apply the first move, advance the cursor
-template <typename T>
-__global__ void __launch_bounds__(1024) k_hart_step(const T* __restrict__ M, double* __restrict__ C,
-                                                    double* __restrict__ cc, int64_t d, int n,
-                                                    int c, int W, HartState* __restrict__ hs,
-                                                    int* __restrict__ modver,
-                                                    int* __restrict__ stamp,
-                                                    const double* __restrict__ approx,
-                                                    const double* __restrict__ err,
-                                                    int* __restrict__ labels,
-                                                    int* __restrict__ counts,
-                                                    double* __restrict__ exact_scratch,
-                                                    int max_passes, int has_cond,
-                                                    cudaGraphConditionalHandle cond) {
-    __shared__ int s_first, s_kind, s_to;
-    __shared__ double red[32 * 2];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    if (hs->done) {
-        if (threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
-        return;
-    }
-    const int cursor = hs->cursor;
-    int wend = cursor + W;
-    if (wend > n) wend = n;
-    if (threadIdx.x == 0) s_first = 0x7fffffff;
-    __syncthreads();
-
-    // Hartigan decision of column j on intervals; returns 0 none, 1 move(to), 2 ambiguous
-    auto decide = [&](int j, bool exact, int& to) -> int {
-        const int from = labels[j];
-        const int cf = counts[from];
-        if (cf <= 1) return 0;
-        auto iv = [&](int k, double& lo, double& hi, double& mid) {
-            if (exact) {
-                mid = exact_scratch[k];
-                lo = hi = mid;
-            } else {
-                mid = approx[(int64_t)j * c + k];
-                const double e = err[(int64_t)j * c + k];
-                lo = mid - e;
-                hi = mid + e;
-            }
-        };
-        double flo, fhi, fmid;
-        iv(from, flo, fhi, fmid);
-        const double na = (double)cf;
-        const double wa = na / (na - 1.0);
-        const double g_lo = wa * flo, g_hi = wa * fhi, g_mid = wa * fmid;
-        // candidate: minimal midpoint delta among k != from (first index on ties)
-        double bd = INFINITY;
-        int bk = 0x7fffffff;
-        bool none = true;
-        for (int k = lane; k < c; k += 32) {
-            if (k == from) continue;
-            double lo, hi, mid;
-            iv(k, lo, hi, mid);
-            const double nb = (double)counts[k];
-            const double wb = nb / (nb + 1.0);
-            const double dmid = wb * mid - g_mid;
-            none &= !(wb * lo - g_hi < -1e-12);
-            if (dmid < bd) {
-                bd = dmid;
-                bk = k;
-            }
-        }
-        none = __all_sync(0xffffffffu, none);
-        if (none) return 0;
-        warp_argmin(bd, bk);
-        if (bk >= c) return 2;
-        double blo, bhi, bmid;
-        iv(bk, blo, bhi, bmid);
-        const double nbk = (double)counts[bk];
-        const double dhi_k = (nbk / (nbk + 1.0)) * bhi - g_lo;
-        bool ok = dhi_k < -1e-12;
-        for (int k = lane; k < c; k += 32) {
-            if (k == from || k == bk) continue;
-            double lo, hi, mid;
-            iv(k, lo, hi, mid);
-            const double nb = (double)counts[k];
-            const double dlo = (nb / (nb + 1.0)) * lo - g_hi;
-            if (k < bk) ok &= dhi_k < dlo;
-            else ok &= dhi_k <= dlo;
-        }
-        ok = __all_sync(0xffffffffu, ok);
-        if (!ok) return 2;
-        to = bk;
-        return 1;
-    };
-
-    // each warp takes columns cursor+w, cursor+w+32, ...; find the first non-trivial
-    for (int j = cursor + w; j < wend; j += 32) {
-        int to = -1;
-        const int r = decide(j, false, to);
-        if (r != 0) {
-            if (lane == 0) atomicMin(&s_first, j);
-            break;
-        }
-    }
-    __syncthreads();
-    const int jf = s_first;
-    if (jf == 0x7fffffff) {  // nothing moves in the window
-        if (threadIdx.x == 0) hs->cursor = wend;
-    } else {
-        // resolve column jf: screened decision, exact fallback if needed
-        if (w == 0) {
-            int to = -1;
-            const int r = decide(jf, false, to);
-            if (lane == 0) {
-                s_kind = r;
-                s_to = to;
-            }
-        }
-        __syncthreads();
-        if (s_kind == 2) {
-            const int jj = jf;
-            for (int k = threadIdx.x; k < c; k += blockDim.x) {
-                const double* cv = C + (int64_t)k * d;
-                const T* x = M + (int64_t)jj * d;
-                double s = 0.0;
-                for (int64_t i = 0; i < d; ++i) {
-                    const double t = (double)x[i] - cv[i];
-                    s += t * t;
-                }
-                exact_scratch[k] = s;
-            }
-            __syncthreads();
-            if (w == 0) {
-                int to = -1;
-                const int r = decide(jf, true, to);
-                if (lane == 0) {
-                    s_kind = r;
-                    s_to = to;
-                    hs->exact_fallbacks += 1;
-                }
-            }
-            __syncthreads();
-        }
-        if (s_kind == 0) {
-            if (threadIdx.x == 0) hs->cursor = jf + 1;
-        } else {
-            // apply the move exactly as kmeans.cpp:122-135
-            const int from = labels[jf], to = s_to;
-            const int cfrom = counts[from], cto = counts[to];
-            const double na1 = (double)(cfrom - 1), nb1 = (double)(cto + 1);
-            const double dcf = (double)cfrom, dct = (double)cto;
-            double* cfp = C + (int64_t)from * d;
-            double* ctp = C + (int64_t)to * d;
-            const T* x = M + (int64_t)jf * d;
-            double sf = 0.0, st = 0.0;
-            for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-                const double xi = (double)x[i];
-                const double a = (cfp[i] * dcf - xi) / na1;
-                const double b = (ctp[i] * dct + xi) / nb1;
-                cfp[i] = a;
-                ctp[i] = b;
-                sf = __fma_rn(a, a, sf);
-                st = __fma_rn(b, b, st);
-            }
-            double v[2] = {sf, st};
-            block_sum<2>(v, red);
-            if (threadIdx.x == 0) {
-                cc[from] = v[0];
-                cc[to] = v[1];
-                counts[from] = cfrom - 1;
-                counts[to] = cto + 1;
-                labels[jf] = to;
-                const int mv = hs->movecount + 1;
-                hs->movecount = mv;
-                modver[from] = mv;
-                modver[to] = mv;
-                hs->improved = 1;
-                hs->moves += 1;
-                hs->cursor = jf + 1;
-            }
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        if (hs->cursor >= n) {
-            if (hs->improved && hs->pass + 1 < max_passes) {
-                hs->pass += 1;
-                hs->cursor = 0;
-                hs->improved = 0;
-            } else {
-                hs->done = 1;
-            }
-        }
-        if (has_cond) cudaGraphSetConditional(cond, hs->done ? 0u : 1u);
-    }
-    (void)stamp;
-}
-
 }  // namespace respca_dev

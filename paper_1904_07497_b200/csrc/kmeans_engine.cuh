@@ -3,6 +3,9 @@
 #pragma once
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <limits>
@@ -12,6 +15,7 @@
 #include "alm.cuh"
 #include "engine.cuh"
 #include "km.cuh"
+#include "hartigan.cuh"
 
 namespace respca_host {
 
@@ -41,7 +45,21 @@ struct Groups {
 
 struct Stats {
     uint64_t hartigan_moves = 0, exact_fallbacks = 0, lloyd_steps = 0, hartigan_passes = 0;
+    uint64_t hartigan_rounds = 0, hartigan_refreshes = 0;
+    double t_pp = 0, t_lloyd = 0, t_hart = 0, t_inertia = 0;  // seconds (host clock, synced)
 };
+
+inline bool trace_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("RESPCA_TRACE");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+using HClock = std::chrono::steady_clock;
+inline double since(HClock::time_point t) {
+    return std::chrono::duration<double>(HClock::now() - t).count();
+}
 
 template <typename T>
 struct KMeansEngine {
@@ -93,30 +111,40 @@ struct KMeansEngine {
     int tile_k() const { return tk_tile(); }
 
     template <int WK, int MJ, int NK>
-    void launch_dmma(const double* C, dim3 grid, int cps) {
+    void launch_dmma(const T* Mp, int nn, const double* C, dim3 grid, int cps) {
         constexpr int NW = 8, WJ = NW / WK;
         constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8;
         static_assert(TJ == 128, "tile");
         const size_t sm = sizeof(T) * 2 * TJ * 36 + sizeof(double) * 2 * TK * 36;
         auto kf = k_dist_dmma<T, WK, MJ, NK>;
         CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        kf<<<grid, 256, sm, st>>>(M, C, d, n, c, cps, part.p, xxp.p);
+        kf<<<grid, 256, sm, st>>>(Mp, C, d, nn, c, cps, part.p, xxp.p);
     }
 
     // ---- screened distances --------------------------------------------
-    void screen(const double* C) {
+    // columns [0, nn) of Mp against C; split-K sized for >= 2 CTAs per SM
+    int scr_n = 0, scr_split = 1;
+    void screen_cols(const T* Mp, int nn, const double* C) {
         k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p);
+        const int tiles = ceil_div(nn, tile_j()) * ceil_div(c, tile_k());
         const int chunks = ceil_div(d, 32);
-        const int cps = ceil_div(chunks, nsplit);
-        dim3 grid(ceil_div(n, tile_j()), ceil_div(c, tile_k()), nsplit);
+        int ns = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
+        ns = std::min(ns, 64);
+        part.ensure((size_t)ns * nn * c);
+        xxp.ensure((size_t)ns * nn);
+        const int cps = ceil_div(chunks, ns);
+        dim3 grid(ceil_div(nn, tile_j()), ceil_div(c, tile_k()), ns);
         switch (tk_tile()) {
-            case 64: launch_dmma<2, 4, 4>(C, grid, cps); break;  // warps 4×2, warp 32×32
-            case 32: launch_dmma<1, 2, 4>(C, grid, cps); break;  // warps 8×1, warp 16×32
-            case 16: launch_dmma<1, 2, 2>(C, grid, cps); break;
-            default: launch_dmma<1, 2, 1>(C, grid, cps); break;
+            case 64: launch_dmma<2, 4, 4>(Mp, nn, C, grid, cps); break;  // warps 4×2, warp 32×32
+            case 32: launch_dmma<1, 2, 4>(Mp, nn, C, grid, cps); break;  // warps 8×1, warp 16×32
+            case 16: launch_dmma<1, 2, 2>(Mp, nn, C, grid, cps); break;
+            default: launch_dmma<1, 2, 1>(Mp, nn, C, grid, cps); break;
         }
         ln.add(2);
+        scr_n = nn;
+        scr_split = ns;
     }
+    void screen(const double* C) { screen_cols(M, n, C); }
     // bound factor of the screen (see km.cuh): γ-bounds of the length-d
     // chains of both the screen (FMA / DMMA accumulation, counted as 2 roundings
     // per step for safety) and the reference's sequential chain, plus slack
@@ -126,8 +154,8 @@ struct KMeansEngine {
         s.part = part.p;
         s.xxp = xxp.p;
         s.cc = cc.p;
-        s.nsplit = nsplit;
-        s.n = n;
+        s.nsplit = scr_split;
+        s.n = scr_n;
         s.c = c;
         s.kappa_d = kappa_screen();
         return s;
@@ -243,6 +271,7 @@ struct KMeansEngine {
         uint64_t it = 0;
         double* cur = C;
         double* nxt = nextC.p;
+        const auto t_lloyd0 = HClock::now();
         for (; it < max_iters; ++it) {
             assign(cur, labels);
             fetch_labels(labels);
@@ -257,7 +286,13 @@ struct KMeansEngine {
             }
         }
         if (cur != C) CK(cudaMemcpyAsync(C, cur, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        if (stats) {
+            CK(cudaStreamSynchronize(st));
+            stats->t_lloyd += since(t_lloyd0);
+        }
+        const auto t_h0 = HClock::now();
         hartigan(C, labels);
+        if (stats) stats->t_hart += since(t_h0);
         fetch_labels(labels);
         groups.build(h_labels.data(), n, c);
         for (int k = 0; k < c; ++k)
@@ -267,45 +302,89 @@ struct KMeansEngine {
     }
 
     // hartigan_refine (kmeans.cpp:96-139), exact sequential semantics
+    // (hartigan.cuh).  Blocks of columns, one CUDA-graph WHILE loop of rounds
+    // per block; the host synchronises once per pass.
+    DBuf<double> hA, hE, hxx, hC2;
+    DBuf<int> hver;
+    WhileGraph hgraph;
+    HartArrays harr{};
+    const void* hkey = nullptr;
+    int hB = 0;
+
     void hartigan(double* C, int* labels) {
         if (c <= 1) return;  // no candidate target: never moves
         groups.build(h_labels.data(), n, c);
         CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
                            cudaMemcpyHostToDevice, st));
-        approx.ensure((size_t)n * c);
-        err.ensure((size_t)n * c);
-        stamp.ensure((size_t)n * c);
-        modver.ensure(c);
-        xx.ensure(n);
+        const size_t nc = (size_t)n * c;
+        hA.ensure(nc);
+        hE.ensure(nc);
+        hxx.ensure(n);
+        hC2.ensure((size_t)2 * d * c);
+        hver.ensure(c);
         hs.ensure(1);
-        k_col_sq_fma_T(M, n, xx.p);
-        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p);
-        CK(cudaMemsetAsync(stamp.p, 0xff, sizeof(int) * (size_t)n * c, st));  // all stale
-        CK(cudaMemsetAsync(modver.p, 0, sizeof(int) * c, st));
-        CK(cudaMemsetAsync(hs.p, 0, sizeof(HartState), st));
-        ln.add(2);
-        const int W = 128;
-        const double kappa_d = kappa_screen();
-        dim3 rg(W, ceil_div(c, 8));
         scratch.ensure(std::max(c, 64));
-        HartState* h = hst.ensure<HartState>(1);
-        for (;;) {
-            for (int r = 0; r < 64; ++r) {
-                k_hart_refresh<T><<<rg, 256, 0, st>>>(M, C, cc.p, xx.p, d, n, c, W, hs.p,
-                                                      modver.p, stamp.p, approx.p, err.p, kappa_d);
-                k_hart_step<T><<<1, 1024, 0, st>>>(M, C, cc.p, d, n, c, W, hs.p, modver.p,
-                                                   stamp.p, approx.p, err.p, labels, counts.p,
-                                                   scratch.p, 50, 0, cudaGraphConditionalHandle{});
-            }
-            ln.add(128);
-            CK(cudaMemcpyAsync(h, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            if (h->done) break;
+        CK(cudaMemcpyAsync(hC2.p, C, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(hver.p, 0, sizeof(int) * c, st));
+        HartArrays h{};
+        h.A = hA.p;
+        h.E = hE.p;
+        h.xx = hxx.p;
+        h.labels = labels;
+        h.counts = counts.p;
+        h.C = hC2.p;
+        h.ver = hver.p;
+        h.scratch = scratch.p;
+        h.kappa_d = kappa_screen();
+        const int B = std::min(n, 512);
+        constexpr int CPB = 8;
+        if (!hgraph.ready() || hkey != (const void*)M || hB != B ||
+            std::memcmp(&h, &harr, sizeof(h)) != 0) {
+            hgraph.begin(st);
+            k_hart_round<T, CPB><<<ceil_div(B, CPB), 512, 0, st>>>(M, hs.p, h, d, n, c,
+                                                                   hgraph.handle);
+            hgraph.end(st);
+            hkey = M;
+            hB = B;
+            harr = h;
         }
+        HartState* hh = hst.ensure<HartState>(1);
+        std::memset(hh, 0, sizeof(HartState));
+        hh->pending_from = -1;
+        hh->first = ~0ULL;
+        CK(cudaMemcpyAsync(hs.p, hh, sizeof(HartState), cudaMemcpyHostToDevice, st));
+        uint64_t rounds0 = 0;
+        int pass = 0;
+        const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
+        for (; pass < 50; ++pass) {
+            for (int b0 = 0; b0 < n; b0 += B) {
+                const int nb = std::min(B, n - b0);
+                k_hart_consolidate<<<cg, 256, 0, st>>>(h, d, c);
+                k_hart_ver_reset<<<1, 256, 0, st>>>(h, c);
+                screen_cols(M + (int64_t)b0 * d, nb, h.C);
+                k_hart_fill<<<ceil_div((int64_t)nb * c, 256), 256, 0, st>>>(screen_view(), h, b0,
+                                                                           nb, c);
+                k_hart_block_begin<<<1, 1, 0, st>>>(hs.p, b0, b0 + nb);
+                ln.add(4);
+                hgraph.launch(st);
+            }
+            CK(cudaMemcpyAsync(hh, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            ln.add(ceil_div(B, CPB) > 0 ? (hh->rounds - rounds0) : 0);
+            rounds0 = hh->rounds;
+            if (!hh->improved) break;
+            hh->improved = 0;
+            CK(cudaMemcpyAsync(hs.p, hh, sizeof(HartState), cudaMemcpyHostToDevice, st));
+        }
+        k_hart_consolidate<<<cg, 256, 0, st>>>(h, d, c);
+        k_hart_ver_reset<<<1, 256, 0, st>>>(h, c);
+        CK(cudaMemcpyAsync(C, hC2.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        ln.add(2);
         if (stats) {
-            stats->hartigan_moves += h->moves;
-            stats->exact_fallbacks += h->exact_fallbacks;
-            stats->hartigan_passes += (uint64_t)h->pass + 1;
+            stats->hartigan_moves += hh->moves;
+            stats->exact_fallbacks += hh->exact_fallbacks;
+            stats->hartigan_passes += (uint64_t)std::min(pass + 1, 50);
+            stats->hartigan_rounds += hh->rounds;
         }
     }
 
@@ -402,10 +481,14 @@ struct KMeansEngine {
         cen.ensure((size_t)d * c);
         bool have = false;
         for (uint64_t r = 0; r < n_restarts; ++r) {
+            const auto tp = HClock::now();
             const std::vector<int> chosen = pp_init(rng);
             gather(chosen, cen.p);
+            if (stats) stats->t_pp += since(tp);
             const uint64_t it = lloyd_run(cen.p, lab.p, max_iters, tol);
+            const auto ti = HClock::now();
             const double in = inertia(cen.p, lab.p);
+            if (stats) stats->t_inertia += since(ti);
             if (in < best) {
                 best = in;
                 have = true;
@@ -416,6 +499,17 @@ struct KMeansEngine {
             }
         }
         CK(cudaStreamSynchronize(st));
+        if (stats && trace_on())
+            std::fprintf(stderr,
+                         "[respca] kmeans(X): pp %.3fs lloyd %.3fs (%llu steps) hartigan %.3fs "
+                         "(%llu rounds, %llu moves, %llu passes, %llu refreshes) inertia %.3fs "
+                         "fallbacks %llu\n",
+                         stats->t_pp, stats->t_lloyd, (unsigned long long)stats->lloyd_steps,
+                         stats->t_hart, (unsigned long long)stats->hartigan_rounds,
+                         (unsigned long long)stats->hartigan_moves,
+                         (unsigned long long)stats->hartigan_passes,
+                         (unsigned long long)stats->hartigan_refreshes, stats->t_inertia,
+                         (unsigned long long)stats->exact_fallbacks);
         if (!have && n_restarts > 0) {
             // every restart had a NaN inertia: the reference returns the
             // default-constructed result; mirror that as an error
