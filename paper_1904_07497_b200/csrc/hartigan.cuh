@@ -40,7 +40,15 @@ struct HartState {
     unsigned arrive;   // last-CTA election
     unsigned long long first;  // packed (j, status, to) of the first non-trivial column
     unsigned long long moves, exact_fallbacks, rounds;
+    unsigned long long t0, tsum;  // globaltimer: earliest CTA start of a round, summed round spans
+    unsigned long long tp1, tp2, sp1, sp2, sp3s;  // phase-end stamps (max over CTAs) and sums
 };
+
+RESPCA_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
 
 struct HartArrays {
     double* A;       // [n][c] screened distance
@@ -126,10 +134,12 @@ __global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
     __shared__ double red[32 * NV];
     __shared__ bool s_last;
     __shared__ int s_st, s_to;
+    const bool has_cond = cond != 0;
     if (hs->block_done) {
-        if (blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+        if (blockIdx.x == 0 && threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
         return;
     }
+    if (threadIdx.x == 0) atomicMin(&hs->t0, gtimer());
     const int cursor = hs->cursor, bend = hs->bend;
     const int jb = cursor + blockIdx.x * CPB;  // first column of this CTA
     const int pf = hs->pending_from;
@@ -202,6 +212,7 @@ __global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
         __syncthreads();
     }
 
+    if (threadIdx.x == 0) atomicMax(&hs->tp1, gtimer());
     // ---- phase 2: decide this CTA's columns (warp per column)
     if (warp < CPB) {
         const int j = jb + warp;
@@ -220,6 +231,7 @@ __global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
     }
     __syncthreads();
     if (threadIdx.x == 0) {
+        atomicMax(&hs->tp2, gtimer());
         __threadfence();
         s_last = atomicAdd(&hs->arrive, 1u) == gridDim.x - 1;
     }
@@ -229,6 +241,12 @@ __global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
     // ---- phase 3 (last CTA): settle the round
     __threadfence();
     if (threadIdx.x == 0) {
+        const unsigned long long t3 = gtimer();
+        hs->sp1 += hs->tp1 - hs->t0;
+        hs->sp2 += hs->tp2 - hs->t0;
+        hs->sp3s += t3 - hs->t0;
+        hs->tp1 = 0;
+        hs->tp2 = 0;
         hs->arrive = 0;
         hs->rounds += 1;
         if (pf >= 0) {  // the new centroid values are complete: switch slots
@@ -297,8 +315,10 @@ __global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
         }
         const int done = hs->cursor >= bend && hs->pending_from < 0;
         hs->block_done = done;
+        hs->tsum += gtimer() - hs->t0;
+        hs->t0 = ~0ULL;
         __threadfence();
-        cudaGraphSetConditional(cond, done ? 0u : 1u);
+        if (has_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
     }
 }
 
@@ -322,6 +342,7 @@ __global__ void k_hart_block_begin(HartState* hs, int b0, int bend) {
     hs->block_done = 0;
     hs->first = ~0ULL;
     hs->arrive = 0;
+    hs->t0 = ~0ULL;
 }
 
 // copy centroids living in slot 1 back to slot 0 (the screen reads slot 0)

@@ -47,6 +47,7 @@ struct Stats {
     uint64_t hartigan_moves = 0, exact_fallbacks = 0, lloyd_steps = 0, hartigan_passes = 0;
     uint64_t hartigan_rounds = 0, hartigan_refreshes = 0;
     double t_pp = 0, t_lloyd = 0, t_hart = 0, t_inertia = 0;  // seconds (host clock, synced)
+    double t_hart_kernel = 0;  // device span of the Hartigan round kernels
 };
 
 inline bool trace_on() {
@@ -349,6 +350,8 @@ struct KMeansEngine {
             harr = h;
         }
         HartState* hh = hst.ensure<HartState>(1);
+        const char* ng = std::getenv("RESPCA_HART_NOGRAPH");
+        const bool nograph = ng && ng[0] == '1';
         std::memset(hh, 0, sizeof(HartState));
         hh->pending_from = -1;
         hh->first = ~0ULL;
@@ -366,7 +369,20 @@ struct KMeansEngine {
                                                                            nb, c);
                 k_hart_block_begin<<<1, 1, 0, st>>>(hs.p, b0, b0 + nb);
                 ln.add(4);
-                hgraph.launch(st);
+                if (!nograph) {
+                    hgraph.launch(st);
+                    continue;
+                }
+                // diagnostic path (RESPCA_HART_NOGRAPH=1): plain launches so
+                // profilers can see each round kernel
+                for (;;) {
+                    for (int r = 0; r < 64; ++r)
+                        k_hart_round<T, CPB><<<ceil_div(B, CPB), 512, 0, st>>>(
+                            M, hs.p, h, d, n, c, cudaGraphConditionalHandle{});
+                    CK(cudaMemcpyAsync(hh, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
+                    CK(cudaStreamSynchronize(st));
+                    if (hh->block_done) break;
+                }
             }
             CK(cudaMemcpyAsync(hh, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -385,6 +401,12 @@ struct KMeansEngine {
             stats->exact_fallbacks += hh->exact_fallbacks;
             stats->hartigan_passes += (uint64_t)std::min(pass + 1, 50);
             stats->hartigan_rounds += hh->rounds;
+            stats->t_hart_kernel += 1e-9 * (double)hh->tsum;
+            if (trace_on())
+                std::fprintf(stderr, "[respca] hartigan rounds %llu: phase1 end %.2fus phase2 end %.2fus phase3 start %.2fus round end %.2fus (mean from first CTA start)\n",
+                             (unsigned long long)hh->rounds, 1e-3 * hh->sp1 / hh->rounds,
+                             1e-3 * hh->sp2 / hh->rounds, 1e-3 * hh->sp3s / hh->rounds,
+                             1e-3 * hh->tsum / hh->rounds);
         }
     }
 
@@ -502,13 +524,14 @@ struct KMeansEngine {
         if (stats && trace_on())
             std::fprintf(stderr,
                          "[respca] kmeans(X): pp %.3fs lloyd %.3fs (%llu steps) hartigan %.3fs "
-                         "(%llu rounds, %llu moves, %llu passes, %llu refreshes) inertia %.3fs "
+                         "(%llu rounds, %llu moves, %llu passes, %llu refreshes, round kernels %.3fs) inertia %.3fs "
                          "fallbacks %llu\n",
                          stats->t_pp, stats->t_lloyd, (unsigned long long)stats->lloyd_steps,
                          stats->t_hart, (unsigned long long)stats->hartigan_rounds,
                          (unsigned long long)stats->hartigan_moves,
                          (unsigned long long)stats->hartigan_passes,
-                         (unsigned long long)stats->hartigan_refreshes, stats->t_inertia,
+                         (unsigned long long)stats->hartigan_refreshes, stats->t_hart_kernel,
+                         stats->t_inertia,
                          (unsigned long long)stats->exact_fallbacks);
         if (!have && n_restarts > 0) {
             // every restart had a NaN inertia: the reference returns the
