@@ -303,17 +303,17 @@ struct KMeansEngine {
     }
 
     // hartigan_refine (kmeans.cpp:96-139), exact sequential semantics
-    // (hartigan.cuh).  Blocks of columns, one CUDA-graph WHILE loop of rounds
-    // per block; the host synchronises once per pass.
+    // (hartigan.cuh): one persistent cooperative launch per block of columns
+    // (owned columns cached in shared memory, one grid barrier per round); the
+    // host synchronises once per pass.
     DBuf<double> hA, hE, hxx, hC2;
     DBuf<int> hver;
-    WhileGraph hgraph;
-    HartArrays harr{};
-    const void* hkey = nullptr;
-    int hB = 0;
+    DBuf<HartGlobal> hglob;
+    DBuf<double> hccpart;
 
     void hartigan(double* C, int* labels) {
         if (c <= 1) return;  // no candidate target: never moves
+        if (c >= 32768) throw InvalidArg("hartigan: c >= 32768 is not supported");
         groups.build(h_labels.data(), n, c);
         CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
                            cudaMemcpyHostToDevice, st));
@@ -323,10 +323,12 @@ struct KMeansEngine {
         hxx.ensure(n);
         hC2.ensure((size_t)2 * d * c);
         hver.ensure(c);
-        hs.ensure(1);
+        hglob.ensure(1);
+        hccpart.ensure(2 * 1024);
         scratch.ensure(std::max(c, 64));
         CK(cudaMemcpyAsync(hC2.p, C, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemsetAsync(hver.p, 0, sizeof(int) * c, st));
+        CK(cudaMemsetAsync(hglob.p, 0, sizeof(HartGlobal), st));
         HartArrays h{};
         h.A = hA.p;
         h.E = hE.p;
@@ -337,28 +339,32 @@ struct KMeansEngine {
         h.ver = hver.p;
         h.scratch = scratch.p;
         h.kappa_d = kappa_screen();
-        const int B = std::min(n, 512);
-        constexpr int CPB = 8;
-        if (!hgraph.ready() || hkey != (const void*)M || hB != B ||
-            std::memcmp(&h, &harr, sizeof(h)) != 0) {
-            hgraph.begin(st);
-            k_hart_round<T, CPB><<<ceil_div(B, CPB), 512, 0, st>>>(M, hs.p, h, d, n, c,
-                                                                   hgraph.handle);
-            hgraph.end(st);
-            hkey = M;
-            hB = B;
-            harr = h;
+        // geometry: one CTA per SM, owned columns cached in shared memory when they fit
+        int dev = 0, nsm = 148, smem_optin = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        const size_t fixed = sizeof(double) * (2 * c + 32 * 16) + sizeof(int) * 2 * c + 1024;
+        auto need = [&](int cpb, bool cache) {
+            return (cache ? (size_t)cpb * d * sizeof(T) + 16 : 0) +
+                   sizeof(double) * 2 * (size_t)cpb * c + fixed;
+        };
+        int cpb = 8;
+        bool cache = true;
+        while (cpb > 1 && need(cpb, true) > (size_t)smem_optin) --cpb;
+        if (need(cpb, true) > (size_t)smem_optin) {  // a column does not fit: stream it
+            cache = false;
+            cpb = 4;
+            while (cpb > 1 && need(cpb, false) > (size_t)smem_optin) --cpb;
         }
-        HartState* hh = hst.ensure<HartState>(1);
-        const char* ng = std::getenv("RESPCA_HART_NOGRAPH");
-        const bool nograph = ng && ng[0] == '1';
-        std::memset(hh, 0, sizeof(HartState));
-        hh->pending_from = -1;
-        hh->first = ~0ULL;
-        CK(cudaMemcpyAsync(hs.p, hh, sizeof(HartState), cudaMemcpyHostToDevice, st));
-        uint64_t rounds0 = 0;
-        int pass = 0;
+        const int G = std::max(1, std::min(nsm, ceil_div(n, cpb)));
+        const int B = G * cpb;
+        const size_t smem = need(cpb, cache);
+        auto kf = cpb <= 2 ? k_hart_block<T, 2> : (cpb <= 4 ? k_hart_block<T, 4> : k_hart_block<T, 8>);
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        HartGlobal* hh = hst.ensure<HartGlobal>(1);
         const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
+        int pass = 0;
         for (; pass < 50; ++pass) {
             for (int b0 = 0; b0 < n; b0 += B) {
                 const int nb = std::min(B, n - b0);
@@ -367,30 +373,36 @@ struct KMeansEngine {
                 screen_cols(M + (int64_t)b0 * d, nb, h.C);
                 k_hart_fill<<<ceil_div((int64_t)nb * c, 256), 256, 0, st>>>(screen_view(), h, b0,
                                                                            nb, c);
-                k_hart_block_begin<<<1, 1, 0, st>>>(hs.p, b0, b0 + nb);
-                ln.add(4);
-                if (!nograph) {
-                    hgraph.launch(st);
-                    continue;
-                }
-                // diagnostic path (RESPCA_HART_NOGRAPH=1): plain launches so
-                // profilers can see each round kernel
-                for (;;) {
-                    for (int r = 0; r < 64; ++r)
-                        k_hart_round<T, CPB><<<ceil_div(B, CPB), 512, 0, st>>>(
-                            M, hs.p, h, d, n, c, cudaGraphConditionalHandle{});
-                    CK(cudaMemcpyAsync(hh, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
-                    CK(cudaStreamSynchronize(st));
-                    if (hh->block_done) break;
-                }
+                k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
+                const int gb = std::min(G, ceil_div(nb, cpb));
+                const T* Mp = M;
+                HartGlobal* hgp = hglob.p;
+                int* lp = labels;
+                int* cp_ = counts.p;
+                double* csp = hC2.p;
+                int* vp = hver.p;
+                const double* ap = hA.p;
+                const double* ep = hE.p;
+                const double* xp = hxx.p;
+                double* sp = scratch.p;
+                double* ccp = hccpart.p;
+                int64_t dd = d;
+                int cc_ = c, b0_ = b0, be = b0 + nb, cpb_ = cpb, cache_ = cache ? 1 : 0;
+                double kd = h.kappa_d;
+                static const int dbgv = [] {
+                    const char* e = std::getenv("RESPCA_HART_DBG");
+                    return e ? std::atoi(e) : 0;
+                }();
+                int dbg = dbgv;
+                void* args[] = {&Mp, &hgp, &lp, &cp_, &csp, &vp, &ap, &ep, &xp, &sp, &ccp,
+                                &dd, &cc_, &b0_, &be, &cpb_, &cache_, &kd, &dbg};
+                CK(cudaLaunchCooperativeKernel((const void*)kf, dim3(gb), dim3(512), args, smem, st));
+                ln.add(5);
             }
-            CK(cudaMemcpyAsync(hh, hs.p, sizeof(HartState), cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hh, hglob.p, sizeof(HartGlobal), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            ln.add(ceil_div(B, CPB) > 0 ? (hh->rounds - rounds0) : 0);
-            rounds0 = hh->rounds;
             if (!hh->improved) break;
-            hh->improved = 0;
-            CK(cudaMemcpyAsync(hs.p, hh, sizeof(HartState), cudaMemcpyHostToDevice, st));
+            k_hart_improved_reset<<<1, 1, 0, st>>>(hglob.p);
         }
         k_hart_consolidate<<<cg, 256, 0, st>>>(h, d, c);
         k_hart_ver_reset<<<1, 256, 0, st>>>(h, c);
@@ -401,12 +413,16 @@ struct KMeansEngine {
             stats->exact_fallbacks += hh->exact_fallbacks;
             stats->hartigan_passes += (uint64_t)std::min(pass + 1, 50);
             stats->hartigan_rounds += hh->rounds;
-            stats->t_hart_kernel += 1e-9 * (double)hh->tsum;
+            stats->t_hart_kernel += 1e-9 * (double)hh->t_kernel;
             if (trace_on())
-                std::fprintf(stderr, "[respca] hartigan rounds %llu: phase1 end %.2fus phase2 end %.2fus phase3 start %.2fus round end %.2fus (mean from first CTA start)\n",
-                             (unsigned long long)hh->rounds, 1e-3 * hh->sp1 / hh->rounds,
-                             1e-3 * hh->sp2 / hh->rounds, 1e-3 * hh->sp3s / hh->rounds,
-                             1e-3 * hh->tsum / hh->rounds);
+                std::fprintf(stderr, "[respca] hartigan: %llu rounds, kernels %.3fs (phase1 %.3fs, max-CTA phase1/block %.1fus, decide %.3fs, rest = barrier+settle)\n",
+                             (unsigned long long)hh->rounds, 1e-9 * hh->t_kernel,
+                             1e-9 * hh->t_phase1, 1e-3 * hh->t_phase1_max, 1e-9 * hh->t_phase2);
+            if (trace_on())
+                std::fprintf(stderr, "[respca] hartigan per-round CTA-mean us: 1a %.2f barA %.2f 1b(+1a+barA) %.2f decide %.2f barB %.2f settle %.2f\n",
+                             1e-3 * hh->tmax[0] / (double)hh->rounds / G, 1e-3 * hh->tmax[1] / (double)hh->rounds / G,
+                             1e-3 * hh->tmax[2] / (double)hh->rounds / G, 1e-3 * hh->tmax[3] / (double)hh->rounds / G,
+                             1e-3 * hh->tmax[4] / (double)hh->rounds / G, 1e-3 * hh->tmax[5] / (double)hh->rounds / G);
         }
     }
 
