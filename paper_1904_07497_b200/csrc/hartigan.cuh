@@ -519,8 +519,7 @@ template <typename T, int MAXQ>
 __global__ void __launch_bounds__(512, 1) k_hart_block(
     const T* __restrict__ M, HartGlobal* __restrict__ hg, int* __restrict__ labels,
     int* __restrict__ counts, double* __restrict__ Cs, int* __restrict__ ver,
-    const double* __restrict__ A, const double* __restrict__ E, const double* __restrict__ xxg,
-    double* __restrict__ scratch, double* __restrict__ ccpart, int64_t d, int c, int b0,
+    Screen scr, double* __restrict__ scratch, double* __restrict__ ccpart, int64_t d, int c, int b0,
     int bend, int cpb, int cache_cols, double kappa_d, int dbg) {
     extern __shared__ __align__(16) unsigned char sm[];
     // ---- shared memory carve-up
@@ -553,9 +552,16 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
         for (int q = 0; q < nown; ++q)
             for (int64_t i = tid; i < d; i += blockDim.x)
                 colc[(int64_t)q * d + i] = M[(int64_t)(jown + q) * d + i];
+    // intervals of the owned columns from the block's screen (split-K partials
+    // summed in fixed order; km.cuh bound)
     for (int e = tid; e < nown * c; e += blockDim.x) {
-        As[e] = A[(int64_t)jown * c + e];
-        Es[e] = E[(int64_t)jown * c + e];
+        const int q = e / c, k = e - (e / c) * c;
+        const int jl = jown - b0 + q;
+        const double xxj = scr.xx(jl);
+        double lo, hi, mid;
+        scr.get(jl, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
+        As[e] = mid;
+        Es[e] = isfinite(hi - mid) ? hi - mid : INFINITY;
     }
     for (int k = tid; k < c; k += blockDim.x) {
         const int ck = __ldcg(counts + k);
@@ -566,7 +572,7 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
         vs[k] = __ldcg(ver + k);
     }
     if (tid < nown) {
-        s_xx[tid] = xxg[jown + tid];
+        s_xx[tid] = scr.xx(jown - b0 + tid);
         s_lab[tid] = __ldcg(labels + jown + tid);
     }
     __syncthreads();
@@ -774,6 +780,11 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
         atomicMax(&hg->t_phase1_max, tph1);
         for (int q = 0; q < 6; ++q) atomicAdd(&hg->tmax[q], ts[q]);  // summed over CTAs
     }
+    // every CTA is past its last read of the election slots: reset them for
+    // the next block launch
+    grid_barrier(hg);
+    if (blockIdx.x == 0 && tid == 0)
+        hg->first[0][0] = hg->first[1][0] = hg->first[2][0] = ~0ULL;
     // publish the replicated state
     if (blockIdx.x == 0) {
         for (int k = tid; k < c; k += blockDim.x) {

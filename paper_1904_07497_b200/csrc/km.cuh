@@ -53,12 +53,15 @@ RESPCA_DEV void cp_wait() {
 // ‖c_k‖² for the screen (FMA chain; only ever used inside the bound)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_col_sq_fma(const double* __restrict__ C, int64_t d,
-                                                    double* __restrict__ out) {
+                                                    double* __restrict__ out,
+                                                    const int* __restrict__ ver = nullptr,
+                                                    int c = 0) {
     __shared__ double red[32];
     const int k = blockIdx.x;
+    const double* ck = C + ((int64_t)(ver ? ver[k] : 0) * c + k) * d;
     double s = 0.0;
     for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-        const double v = C[(int64_t)k * d + i];
+        const double v = ck[i];
         s = __fma_rn(v, v, s);
     }
     double v[1] = {s};
@@ -199,7 +202,8 @@ RESPCA_DEV void cp_async16(void* smem, const void* gmem, int bytes) {
 
 template <typename T, int WK, int MJ, int NK>
 __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
-                                                     const double* __restrict__ C, int64_t d,
+                                                     const double* __restrict__ C,
+                                                     const int* __restrict__ ver, int64_t d,
                                                      int n, int c, int chunks_per_split,
                                                      double* __restrict__ part,
                                                      double* __restrict__ xxp) {
@@ -242,7 +246,8 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
                 const int64_t i = i0 + v * 2;
                 int bytes = 0;
                 if (k < c && i < iend) bytes = (int)(8 * ((iend - i) < 2 ? (iend - i) : 2));
-                cp_async16(bdst + row * AS + v * 2, bytes ? C + (int64_t)k * d + i : C, bytes);
+                const double* ck = C + ((int64_t)(ver && k < c ? ver[k] : 0) * c + k) * d;
+                cp_async16(bdst + row * AS + v * 2, bytes ? ck + i : C, bytes);
             }
         } else {
             for (int e = tid; e < TJ * KI; e += 256) {
@@ -258,7 +263,8 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
                 const int k = k0 + row;
                 const int64_t i = i0 + ii;
                 const bool p = k < c && i < iend;
-                cp_async8(bdst + row * AS + ii, p ? C + (int64_t)k * d + i : C, p);
+                const double* ck = C + ((int64_t)(ver && k < c ? ver[k] : 0) * c + k) * d;
+                cp_async8(bdst + row * AS + ii, p ? ck + i : C, p);
             }
         }
         cp_commit();

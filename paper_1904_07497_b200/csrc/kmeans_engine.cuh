@@ -112,21 +112,22 @@ struct KMeansEngine {
     int tile_k() const { return tk_tile(); }
 
     template <int WK, int MJ, int NK>
-    void launch_dmma(const T* Mp, int nn, const double* C, dim3 grid, int cps) {
+    void launch_dmma(const T* Mp, int nn, const double* C, const int* ver, dim3 grid, int cps) {
         constexpr int NW = 8, WJ = NW / WK;
         constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8;
         static_assert(TJ == 128, "tile");
         const size_t sm = sizeof(T) * 2 * TJ * 36 + sizeof(double) * 2 * TK * 36;
         auto kf = k_dist_dmma<T, WK, MJ, NK>;
         CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        kf<<<grid, 256, sm, st>>>(Mp, C, d, nn, c, cps, part.p, xxp.p);
+        kf<<<grid, 256, sm, st>>>(Mp, C, ver, d, nn, c, cps, part.p, xxp.p);
     }
 
     // ---- screened distances --------------------------------------------
     // columns [0, nn) of Mp against C; split-K sized for >= 2 CTAs per SM
     int scr_n = 0, scr_split = 1;
-    void screen_cols(const T* Mp, int nn, const double* C) {
-        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p);
+    // ver != nullptr: centroid k lives in slot ver[k] of a [2][c][d] store
+    void screen_cols(const T* Mp, int nn, const double* C, const int* ver = nullptr) {
+        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p, ver, c);
         const int tiles = ceil_div(nn, tile_j()) * ceil_div(c, tile_k());
         const int chunks = ceil_div(d, 32);
         int ns = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
@@ -136,10 +137,10 @@ struct KMeansEngine {
         const int cps = ceil_div(chunks, ns);
         dim3 grid(ceil_div(nn, tile_j()), ceil_div(c, tile_k()), ns);
         switch (tk_tile()) {
-            case 64: launch_dmma<2, 4, 4>(Mp, nn, C, grid, cps); break;  // warps 4×2, warp 32×32
-            case 32: launch_dmma<1, 2, 4>(Mp, nn, C, grid, cps); break;  // warps 8×1, warp 16×32
-            case 16: launch_dmma<1, 2, 2>(Mp, nn, C, grid, cps); break;
-            default: launch_dmma<1, 2, 1>(Mp, nn, C, grid, cps); break;
+            case 64: launch_dmma<2, 4, 4>(Mp, nn, C, ver, grid, cps); break;  // warps 4×2, warp 32×32
+            case 32: launch_dmma<1, 2, 4>(Mp, nn, C, ver, grid, cps); break;  // warps 8×1, warp 16×32
+            case 16: launch_dmma<1, 2, 2>(Mp, nn, C, ver, grid, cps); break;
+            default: launch_dmma<1, 2, 1>(Mp, nn, C, ver, grid, cps); break;
         }
         ln.add(2);
         scr_n = nn;
@@ -365,15 +366,13 @@ struct KMeansEngine {
         HartGlobal* hh = hst.ensure<HartGlobal>(1);
         const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
         int pass = 0;
+        k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
+        ln.add();
         for (; pass < 50; ++pass) {
             for (int b0 = 0; b0 < n; b0 += B) {
                 const int nb = std::min(B, n - b0);
-                k_hart_consolidate<<<cg, 256, 0, st>>>(h, d, c);
-                k_hart_ver_reset<<<1, 256, 0, st>>>(h, c);
-                screen_cols(M + (int64_t)b0 * d, nb, h.C);
-                k_hart_fill<<<ceil_div((int64_t)nb * c, 256), 256, 0, st>>>(screen_view(), h, b0,
-                                                                           nb, c);
-                k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
+                // screen the block against the CURRENT centroid slots
+                screen_cols(M + (int64_t)b0 * d, nb, hC2.p, hver.p);
                 const int gb = std::min(G, ceil_div(nb, cpb));
                 const T* Mp = M;
                 HartGlobal* hgp = hglob.p;
@@ -381,9 +380,7 @@ struct KMeansEngine {
                 int* cp_ = counts.p;
                 double* csp = hC2.p;
                 int* vp = hver.p;
-                const double* ap = hA.p;
-                const double* ep = hE.p;
-                const double* xp = hxx.p;
+                Screen scr = screen_view();
                 double* sp = scratch.p;
                 double* ccp = hccpart.p;
                 int64_t dd = d;
@@ -394,10 +391,10 @@ struct KMeansEngine {
                     return e ? std::atoi(e) : 0;
                 }();
                 int dbg = dbgv;
-                void* args[] = {&Mp, &hgp, &lp, &cp_, &csp, &vp, &ap, &ep, &xp, &sp, &ccp,
+                void* args[] = {&Mp, &hgp, &lp, &cp_, &csp, &vp, &scr, &sp, &ccp,
                                 &dd, &cc_, &b0_, &be, &cpb_, &cache_, &kd, &dbg};
                 CK(cudaLaunchCooperativeKernel((const void*)kf, dim3(gb), dim3(512), args, smem, st));
-                ln.add(5);
+                ln.add(1);
             }
             CK(cudaMemcpyAsync(hh, hglob.p, sizeof(HartGlobal), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
