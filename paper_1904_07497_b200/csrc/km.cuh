@@ -560,26 +560,49 @@ __global__ void k_fast_verdict(Ctl* __restrict__ ctl) {
 // Warp-transposed exact chains: lane = column, 32×32 tiles read coalesced.
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(128) k_pp_d2(const T* __restrict__ M, int64_t d, int n,
-                                               int last, double* __restrict__ d2) {
-    __shared__ double tile[4][32][33];
-    __shared__ double lastv[4][32];
+__global__ void __launch_bounds__(64) k_pp_d2(const T* __restrict__ M, int64_t d, int n, int last,
+                                              double* __restrict__ d2) {
+    // lane = column; rows stream through a PD-deep cp.async ring of 32×32
+    // tiles per warp so the per-column sequential chain (the latency floor:
+    // d dependent adds) is not also waiting on memory
+    constexpr int PD = 4, W = 2;
+    extern __shared__ __align__(16) unsigned char pp_sm[];
+    auto tile = reinterpret_cast<T(*)[PD][32][33]>(pp_sm);                       // [W][PD][32][33]
+    auto lastv = reinterpret_cast<T(*)[PD][32]>(pp_sm + sizeof(T) * W * PD * 32 * 33);  // [W][PD][32]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int j0 = (blockIdx.x * 4 + w) * 32;
+    const int j0 = (blockIdx.x * W + w) * 32;
     if (j0 >= n) return;
-    double s = 0.0;
-    for (int64_t i0 = 0; i0 < d; i0 += 32) {
-        const int64_t i = i0 + lane;
-        lastv[w][lane] = i < d ? (double)M[(int64_t)last * d + i] : 0.0;
+    const int64_t ntile = (d + 31) / 32;
+    auto issue = [&](int64_t t) {
+        const int slot = (int)(t % PD);
+        const int64_t i = t * 32 + lane;
+        const bool okr = i < d;
+        if (sizeof(T) == 8) cp_async8(&lastv[w][slot][lane], okr ? M + (int64_t)last * d + i : M, okr);
+        else cp_async4(&lastv[w][slot][lane], okr ? M + (int64_t)last * d + i : M, okr);
         for (int cc = 0; cc < 32; ++cc) {
             const int j = j0 + cc;
-            tile[w][cc][lane] = (j < n && i < d) ? (double)M[(int64_t)j * d + i] : 0.0;
+            const bool ok = okr && j < n;
+            const T* src = ok ? M + (int64_t)j * d + i : M;
+            if (sizeof(T) == 8) cp_async8(&tile[w][slot][cc][lane], src, ok);
+            else cp_async4(&tile[w][slot][cc][lane], src, ok);
         }
+        cp_commit();
+    };
+    for (int64_t t = 0; t < PD - 1; ++t) {
+        if (t < ntile) issue(t);
+        else cp_commit();
+    }
+    double s = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + PD - 1 < ntile) issue(t + PD - 1);
+        else cp_commit();
+        cp_wait<PD - 1>();
         __syncwarp();
-        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
+        const int slot = (int)(t % PD);
+        const int lim = (int)((d - t * 32) < 32 ? (d - t * 32) : 32);
         for (int r = 0; r < lim; ++r) {
-            const double t = tile[w][lane][r] - lastv[w][r];
-            s += t * t;
+            const double tt = (double)tile[w][slot][lane][r] - (double)lastv[w][slot][r];
+            s += tt * tt;
         }
         __syncwarp();
     }

@@ -466,7 +466,9 @@ struct KMeansEngine {
         CK(cudaMemcpyAsync(d2.p, hd2.data(), sizeof(double) * n, cudaMemcpyHostToDevice, st));
         while ((int)chosen.size() < c) {
             const int last = chosen.back();
-            k_pp_d2<T><<<ceil_div(n, 128), 128, 0, st>>>(M, d, n, last, d2.p);
+            const size_t ppsm = sizeof(T) * 2 * 4 * (32 * 33 + 32);
+            CK(cudaFuncSetAttribute(k_pp_d2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ppsm));
+            k_pp_d2<T><<<ceil_div(n, 64), 64, ppsm, st>>>(M, d, n, last, d2.p);
             ln.add();
             CK(cudaMemcpyAsync(hd2.data(), d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
