@@ -155,6 +155,11 @@ int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint
                            const double* centroids, uint64_t c, double* approx_out,
                            double* err_out);
 
+/* Same for the tcgen05 BF16 screen used by the ALM fast path (c <= 64). */
+int respca_cu_debug_screen_tc(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                              const double* centroids, uint64_t c, double* approx_out,
+                              double* err_out);
+
 /* --- benchmark hooks (device-resident state, no host copies) ------------- */
 /* Upload X and run validation + the one-time initial clustering; leaves the
  * context ready to step the ALM loop.  init_ms receives the device time. */

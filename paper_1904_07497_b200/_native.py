@@ -58,6 +58,7 @@ EXPORTS = [
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
     "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
+    "respca_cu_debug_screen_tc",
 ]
 
 
@@ -107,6 +108,7 @@ def lib() -> C.CDLL:
                                                   dptr]
             L.respca_cu_bench_steps.argtypes = [vp, u64, dptr, dptr, dptr, u64ptr]
             L.respca_cu_debug_screen.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
+            L.respca_cu_debug_screen_tc.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             _lib = L
         return _lib
 

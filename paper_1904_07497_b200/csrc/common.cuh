@@ -38,6 +38,7 @@ struct Ctl {
     unsigned int changed, moves, ambiguous;  // counters of the decide pass
     int amb_list_len;
     double last_l1;   // ‖S‖₁ of the last finalized iteration (objective patch-up)
+    unsigned int margin_hist[6];  // diagnostics: columns whose relative decision margin < 1e-1..1e-6
     unsigned long long exact_fallbacks;
 };
 

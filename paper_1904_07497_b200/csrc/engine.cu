@@ -94,6 +94,10 @@ struct Alm : AlmBase {
     WhileGraph wg;
     PlainGraph rest;
     double init_ms = 0.0, xnorm = 0.0;
+    bool use_tc = [] {
+        const char* e = std::getenv("RESPCA_TC_SCREEN");
+        return !(e && e[0] == '0');
+    }();
 
     explicit Alm(respca_cu_ctx* cx) : ctx(cx), st(cx->st), ln{&cx->launches} {
         km.st = st;
@@ -231,7 +235,8 @@ struct Alm : AlmBase {
     }
     void launch_pass_a() {
         if (c <= 1) return;
-        km.screen(Cw.p);
+        if (use_tc && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05 BF16 screen
+        else km.screen(Cw.p);                           // FP64 DMMA screen
         km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);
         k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
         ln.add();
@@ -301,6 +306,13 @@ struct Alm : AlmBase {
 
     void download(T* Lo, T* So, uint64_t* lab, respca_cu_report* rep_out) {
         const Ctl h = read_ctl();
+        if (trace_on())
+            std::fprintf(stderr,
+                         "[respca] loop: %d iterations; columns x iterations with Hartigan margin "
+                         "/ (|x|+|c|)^2 below 1e-1..1e-6: %u %u %u %u %u %u (of %lld)\n",
+                         h.iter, h.margin_hist[0], h.margin_hist[1], h.margin_hist[2],
+                         h.margin_hist[3], h.margin_hist[4], h.margin_hist[5],
+                         (long long)h.iter * n);
         const int64_t N = d * n;
         CK(cudaMemcpyAsync(Lo, L.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
         CK(cudaMemcpyAsync(So, S.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
@@ -986,6 +998,32 @@ int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint
         CK(cudaMemcpyAsync(approx_out, a.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaMemcpyAsync(err_out, e.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+int respca_cu_debug_screen_tc(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,
+                              const double* centroids, uint64_t c, double* approx_out,
+                              double* err_out) {
+    return guarded(ctx, [&] {  // test hook: the tcgen05 BF16 screen and its bound
+        check_dims(d, n);
+        if (c > (uint64_t)TC_N) throw InvalidArg("debug_screen_tc: c > 64");
+        KMeansEngine<double> km;
+        Dev64 dm, dc;
+        km_common(ctx, km, dm, m, d, n, c);
+        const double* C = dc.up(ctx->st, centroids, d * c);
+        km.screen_tc(C);
+        DBuf<double> a, e;
+        a.ensure(n * c);
+        e.ensure(n * c);
+        k_screen_dump<<<ceil_div((int64_t)n * c, 256), 256, 0, ctx->st>>>(km.screen_view(), (int)n,
+                                                                          (int)c, a.p, e.p);
+        ctx->launches++;
+        int errv = 0;
+        CK(cudaMemcpyAsync(&errv, km.tcerr.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(approx_out, a.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaMemcpyAsync(err_out, e.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
+        CK(cudaStreamSynchronize(ctx->st));
+        if (errv) throw CudaErr("tcgen05 screen pipeline timed out (code " + std::to_string(errv) + ")");
     });
 }
 

@@ -195,6 +195,17 @@ RESPCA_DEV void dmma884(double& d0, double& d1, double a, double b) {
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
+// m16n8k8 f64 (sm_90+): A 16×8 row-major (a0 (g,t) a1 (g+8,t) a2 (g,t+4)
+// a3 (g+8,t+4)), B 8×8 col-major (b0 (t,g) b1 (t+4,g)), C/D 16×8
+// (c0,c1 (g, 2t..2t+1), c2,c3 (g+8, 2t..2t+1)); g = lane/4, t = lane%4
+RESPCA_DEV void dmma1688(double& c0, double& c1, double& c2, double& c3, double a0, double a1,
+                         double a2, double a3, double b0, double b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+d"(c0), "+d"(c1), "+d"(c2), "+d"(c3)
+        : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+}
 RESPCA_DEV void cp_async16(void* smem, const void* gmem, int bytes) {
     const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
@@ -291,19 +302,30 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
         const T* as = As + (ch & 1) * TJ * AS + (wj * MJ * 8 + g) * AS + t4;
         const double* bs = Bs + (ch & 1) * TK * AS + (wk * NK * 8 + g) * AS + t4;
 #pragma unroll
-        for (int kk = 0; kk < KI; kk += 4) {
-            double a[MJ], b[NK];
+        for (int kk = 0; kk < KI; kk += 8) {
+            // m16n8k8: 8-row groups 2x2 and 2x2+1 form one 16-row A tile
+            double a[MJ][2], b[NK][2];
 #pragma unroll
-            for (int x = 0; x < MJ; ++x) a[x] = (double)as[x * 8 * AS + kk];
+            for (int x = 0; x < MJ; ++x) {
+                a[x][0] = (double)as[x * 8 * AS + kk];
+                a[x][1] = (double)as[x * 8 * AS + kk + 4];
+            }
 #pragma unroll
-            for (int y = 0; y < NK; ++y) b[y] = bs[y * 8 * AS + kk];
+            for (int y = 0; y < NK; ++y) {
+                b[y][0] = bs[y * 8 * AS + kk];
+                b[y][1] = bs[y * 8 * AS + kk + 4];
+            }
 #pragma unroll
-            for (int x = 0; x < MJ; ++x)
+            for (int x2 = 0; x2 < MJ / 2; ++x2)
 #pragma unroll
-                for (int y = 0; y < NK; ++y) dmma884(acc[x][y][0], acc[x][y][1], a[x], b[y]);
+                for (int y = 0; y < NK; ++y)
+                    dmma1688(acc[2 * x2][y][0], acc[2 * x2][y][1], acc[2 * x2 + 1][y][0],
+                             acc[2 * x2 + 1][y][1], a[2 * x2][0], a[2 * x2 + 1][0], a[2 * x2][1],
+                             a[2 * x2 + 1][1], b[y][0], b[y][1]);
             if (wk == 0)
 #pragma unroll
-                for (int x = 0; x < MJ; ++x) xx[x] = __fma_rn(a[x], a[x], xx[x]);
+                for (int x = 0; x < MJ; ++x)
+                    xx[x] = __fma_rn(a[x][1], a[x][1], __fma_rn(a[x][0], a[x][0], xx[x]));
         }
         __syncthreads();
     }
@@ -481,6 +503,29 @@ __global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
     const int old = old_labels ? old_labels[j] : -1;
     int nl = old;
     const int st = decide_column(j, c, old, counts, mode == 1, fn, nl);
+    if (mode == 1 && old >= 0 && counts[old] > 1) {
+        // diagnostics: smallest Hartigan/argmin margin of this column relative
+        // to (‖x‖ + ‖c‖)² — what a lower-precision screen would have to resolve
+        double flo, fhi, fmid;
+        fn(j, old, flo, fhi, fmid);
+        const double na = (double)counts[old];
+        const double ga = na / (na - 1.0) * fmid;
+        double mrel = INFINITY;
+        for (int k = lane; k < c; k += 32) {
+            if (k == old) continue;
+            double lo, hi, mid;
+            fn(j, k, lo, hi, mid);
+            const double nb = (double)counts[k];
+            const double delta = nb / (nb + 1.0) * mid - ga;
+            const double sc_ = nx + sqrt(fabs(sc.cc[k]));
+            mrel = fmin(mrel, fabs(delta + 1e-12) / (sc_ * sc_));
+        }
+        mrel = warp_min(mrel);
+        if (lane == 0)
+            for (int q = 0; q < 6; ++q)
+                if (mrel < 0.1 / (double)(q == 0 ? 1 : (q == 1 ? 10 : (q == 2 ? 100 : (q == 3 ? 1000 : (q == 4 ? 10000 : 100000))))))
+                    atomicAdd(&ctl->margin_hist[q], 1u);
+    }
     if (lane == 0) {
         new_labels[j] = st == ST_AMBIG ? old : nl;
         if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);

@@ -16,6 +16,7 @@
 #include "engine.cuh"
 #include "km.cuh"
 #include "hartigan.cuh"
+#include "tc_screen.cuh"
 
 namespace respca_host {
 
@@ -145,12 +146,41 @@ struct KMeansEngine {
         ln.add(2);
         scr_n = nn;
         scr_split = ns;
+        tc_mode = false;
     }
     void screen(const double* C) { screen_cols(M, n, C); }
     // bound factor of the screen (see km.cuh): γ-bounds of the length-d
     // chains of both the screen (FMA / DMMA accumulation, counted as 2 roundings
     // per step for safety) and the reference's sequential chain, plus slack
     double kappa_screen() const { return (3.0 * (double)d + 16.0) * kU * 1.1; }
+    // ---- tensor-core (tcgen05, BF16) screen: the ALM fast path --------------
+    // valid for c <= 64; intervals use the BF16 bound (tc_screen.cuh)
+    DBuf<__nv_bfloat16> tcCb;
+    DBuf<int> tcerr;
+    bool tc_mode = false;
+    bool tc_ok() const { return c <= TC_N; }
+    void screen_tc(const double* C) {
+        const int64_t d_pad = ((d + TC_KB - 1) / TC_KB) * TC_KB;
+        tcCb.ensure((size_t)TC_N * d_pad);
+        tcerr.ensure(1);
+        k_tc_prep_centroids<<<TC_N, 256, 0, st>>>(C, d, c, d_pad, tcCb.p, cc.p);
+        const int tiles = ceil_div(n, TC_M);
+        const int64_t total_kb = d_pad / TC_KB;
+        // two CTAs fit per SM (smem ~100 KB): one wave of <= 2·148 CTAs
+        int ns = (int)std::max<int64_t>(1, std::min<int64_t>(total_kb / 4, (2 * 148) / tiles));
+        ns = std::max(1, std::min(ns, 16));
+        const int kbps = (int)((total_kb + ns - 1) / ns);
+        part.ensure((size_t)ns * n * c);
+        xxp.ensure((size_t)ns * n);
+        auto kf = k_screen_tc<T>;
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+        kf<<<dim3(tiles, ns), TC_THREADS, TC_SMEM, st>>>(M, tcCb.p, d, d_pad, n, c, kbps, part.p,
+                                                         xxp.p, tcerr.p);
+        ln.add(2);
+        scr_n = n;
+        scr_split = ns;
+        tc_mode = true;
+    }
     Screen screen_view() const {
         Screen s;
         s.part = part.p;
@@ -159,7 +189,7 @@ struct KMeansEngine {
         s.nsplit = scr_split;
         s.n = scr_n;
         s.c = c;
-        s.kappa_d = kappa_screen();
+        s.kappa_d = tc_mode ? tc_bf16_kappa((double)d) + kappa_screen() : kappa_screen();
         return s;
     }
 

@@ -213,3 +213,29 @@ def test_screen_bound_is_rigorous(ctx, orc):
         exact = np.cumsum(diff * diff, axis=0)[-1]
         assert (np.abs(exact - a) <= e).all(), (d, n, c, float(np.max(np.abs(exact - a) / e)))
         assert (e <= 1e-9 * (np.abs(exact) + scale * scale * d)).all()
+
+
+def test_tc_screen_bound_is_rigorous(ctx):
+    """The tcgen05 BF16 screen (ALM fast path): its interval always contains the
+    reference's exact sequential sq_dist."""
+    from paper_1904_07497_b200 import _native as N
+
+    rng = np.random.default_rng(22)
+    for d, n, c, scale in ((3, 40, 5, 1.0), (130, 300, 50, 1e2), (1000, 257, 64, 1e-3),
+                           (4096, 200, 17, 5.0), (64, 129, 1, 1.0), (10000, 160, 50, 0.14)):
+        m = np.asfortranarray(rng.normal(0, scale, (d, n)))
+        Cm = np.asfortranarray(m[:, rng.choice(n, c, replace=False)] * 0.5 +
+                               rng.normal(0, scale, (d, c)))
+        a = np.empty(n * c)
+        e = np.empty(n * c)
+        N.check(ctx, N.lib().respca_cu_debug_screen_tc(ctx.handle, m.ctypes.data_as(N.dptr), d, n,
+                                                       Cm.ctypes.data_as(N.dptr), c,
+                                                       a.ctypes.data_as(N.dptr),
+                                                       e.ctypes.data_as(N.dptr)))
+        a, e = a.reshape(n, c), e.reshape(n, c)
+        diff = m[:, :, None] - Cm[:, None, :]
+        exact = np.cumsum(diff * diff, axis=0)[-1]
+        err = np.abs(exact - a)
+        assert (err <= e).all(), (d, n, c, float(np.max(err / e)))
+        # the screen is informative: its error is far below the distances
+        assert np.median(err / np.maximum(exact, 1e-300)) < 1e-2
