@@ -483,6 +483,77 @@ RESPCA_DEV int decide_column(int j, int c, int old_label, const int* __restrict_
     return ST_AMBIG;
 }
 
+// Same decision with each lane's intervals (k = lane + 32q, q < KPL) computed
+// once into registers; the candidate's interval is broadcast by shuffle.
+template <int KPL>
+RESPCA_DEV int decide_column_cached(int c, int old_label, const int* __restrict__ counts,
+                                    bool hart, const double (&lo)[KPL], const double (&hi)[KPL],
+                                    const double (&mid)[KPL], int& new_label) {
+    const int lane = threadIdx.x & 31;
+    double bv = INFINITY;
+    int bk = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k < c && mid[q] < bv) {
+            bv = mid[q];
+            bk = k;
+        }
+    }
+    warp_argmin(bv, bk);
+    if (bk >= c) bk = 0;
+    auto fetch = [&](int k, double& l, double& h, double& m) {
+        const int q = k >> 5, src = k & 31;
+        double tl = 0.0, th = 0.0, tm = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < KPL; ++qq)
+            if (qq == q) {
+                tl = lo[qq];
+                th = hi[qq];
+                tm = mid[qq];
+            }
+        l = __shfl_sync(0xffffffffu, tl, src);
+        h = __shfl_sync(0xffffffffu, th, src);
+        m = __shfl_sync(0xffffffffu, tm, src);
+    };
+    double klo, khi, kmid;
+    fetch(bk, klo, khi, kmid);
+    bool ok = true;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= c || k == bk) continue;
+        if (k < bk) ok &= khi < lo[q];
+        else ok &= khi <= lo[q];
+    }
+    ok = __all_sync(0xffffffffu, ok) && isfinite(khi);
+    if (!ok) return ST_AMBIG;
+    new_label = bk;
+    if (bk != old_label) return ST_CHANGED;
+    if (!hart) return ST_STABLE;
+    const int from = bk;
+    const int cf = counts[from];
+    if (cf <= 1) return ST_STABLE;  // kmeans.cpp:105
+    const double na = (double)cf;
+    const double wa = na / (na - 1.0);
+    const double gain_hi = wa * khi, gain_lo = wa * klo;
+    bool surely_none = true, surely_move = false;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= c || k == from) continue;
+        const double nb = (double)counts[k];
+        const double wb = nb / (nb + 1.0);
+        surely_none &= !(wb * lo[q] - gain_hi < -1e-12);
+        surely_move |= (wb * hi[q] - gain_lo) < -1e-12;
+    }
+    surely_none = __all_sync(0xffffffffu, surely_none);
+    surely_move = __any_sync(0xffffffffu, surely_move);
+    if (surely_none) return ST_STABLE;
+    if (surely_move) return ST_MOVE;
+    return ST_AMBIG;
+}
+
 // Decide all columns from the screen.  mode: 0 = Lloyd assignment only,
 // 1 = ALM fast-path check (assignment + first Hartigan pass).
 // Output labels are written to new_labels; ambiguous columns are appended to
@@ -491,7 +562,8 @@ __global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
                                                 const int* __restrict__ old_labels,
                                                 const int* __restrict__ counts, int mode,
                                                 int* __restrict__ new_labels,
-                                                int* __restrict__ amb_list, Ctl* __restrict__ ctl) {
+                                                int* __restrict__ amb_list, Ctl* __restrict__ ctl,
+                                                int diag) {
     const int lane = threadIdx.x & 31;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (j >= n || ctl->done) return;
@@ -502,8 +574,20 @@ __global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
     };
     const int old = old_labels ? old_labels[j] : -1;
     int nl = old;
-    const int st = decide_column(j, c, old, counts, mode == 1, fn, nl);
-    if (mode == 1 && old >= 0 && counts[old] > 1) {
+    int st;
+    if (c <= 128) {  // intervals computed once per lane (KPL = 4)
+        double lo[4], hi[4], mid[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int k = lane + 32 * q;
+            if (k < c) fn(j, k, lo[q], hi[q], mid[q]);
+            else lo[q] = hi[q] = mid[q] = INFINITY;
+        }
+        st = decide_column_cached<4>(c, old, counts, mode == 1, lo, hi, mid, nl);
+    } else {
+        st = decide_column(j, c, old, counts, mode == 1, fn, nl);
+    }
+    if (diag && mode == 1 && old >= 0 && counts[old] > 1) {
         // diagnostics: smallest Hartigan/argmin margin of this column relative
         // to (‖x‖ + ‖c‖)² — what a lower-precision screen would have to resolve
         double flo, fhi, fmid;

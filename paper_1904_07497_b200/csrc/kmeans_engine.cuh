@@ -198,7 +198,7 @@ struct KMeansEngine {
                 Ctl* ctl) {
         k_decide<<<ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(screen_view(), n, c, old_labels,
                                                                  cnts, mode, out_labels, amb.p,
-                                                                 ctl);
+                                                                 ctl, trace_on() ? 1 : 0);
         k_exact_cols<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous,
                                                              exact.p);
         k_redecide<<<std::min(ceil_div((int64_t)n * 32, 256), 4 * 148), 256, 0, st>>>(

@@ -170,40 +170,45 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_screen_tc(
             unsigned char* A = stage_base + (size_t)s * TC_STAGE_BYTES;
             unsigned char* B = A + TC_A_BYTES;
             const int64_t i0 = (kb0 + it) * TC_KB;
-            // A: each lane converts elements (2·lane, 2·lane+1) of every row
-            double2 v[RPW];
+            // A: each lane converts elements (2·lane, 2·lane+1) of every row,
+            // in batches of RB rows (all loads of a batch in flight together)
+            constexpr int RB = 8;
 #pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const int row = warp + r * TC_PRODUCERS;
-                const int j = j0 + row;
-                const int64_t i = i0 + 2 * lane;
-                double x0 = 0.0, x1 = 0.0;
-                if (j < n) {
-                    const T* src = M + (int64_t)j * d + i;
-                    if (i + 1 < d) {
-                        if (sizeof(T) == 8 && (d % 2) == 0) {
-                            const double2 t = __ldcs(reinterpret_cast<const double2*>(src));
-                            x0 = t.x;
-                            x1 = t.y;
-                        } else {
+            for (int rb = 0; rb < RPW; rb += RB) {
+                double2 v[RB];
+#pragma unroll
+                for (int r = 0; r < RB; ++r) {
+                    const int row = warp + (rb + r) * TC_PRODUCERS;
+                    const int j = j0 + row;
+                    const int64_t i = i0 + 2 * lane;
+                    double x0 = 0.0, x1 = 0.0;
+                    if (j < n) {
+                        const T* src = M + (int64_t)j * d + i;
+                        if (i + 1 < d) {
+                            if (sizeof(T) == 8 && (d % 2) == 0) {
+                                const double2 t = __ldcs(reinterpret_cast<const double2*>(src));
+                                x0 = t.x;
+                                x1 = t.y;
+                            } else {
+                                x0 = (double)src[0];
+                                x1 = (double)src[1];
+                            }
+                        } else if (i < d) {
                             x0 = (double)src[0];
-                            x1 = (double)src[1];
                         }
-                    } else if (i < d) {
-                        x0 = (double)src[0];
                     }
+                    v[r] = make_double2(x0, x1);
                 }
-                v[r] = make_double2(x0, x1);
-            }
 #pragma unroll
-            for (int r = 0; r < RPW; ++r) {
-                const int row = warp + r * TC_PRODUCERS;
-                xxr[r] = __fma_rn(v[r].y, v[r].y, __fma_rn(v[r].x, v[r].x, xxr[r]));
-                __nv_bfloat162 b2;
-                b2.x = __double2bfloat16(v[r].x);
-                b2.y = __double2bfloat16(v[r].y);
-                // lane → K elements 2·lane..2·lane+1 = chunk lane/4, byte (lane%4)*4
-                *reinterpret_cast<__nv_bfloat162*>(A + sw128(row, lane >> 2) + (lane & 3) * 4) = b2;
+                for (int r = 0; r < RB; ++r) {
+                    const int row = warp + (rb + r) * TC_PRODUCERS;
+                    xxr[rb + r] = __fma_rn(v[r].y, v[r].y, __fma_rn(v[r].x, v[r].x, xxr[rb + r]));
+                    __nv_bfloat162 b2;
+                    b2.x = __double2bfloat16(v[r].x);
+                    b2.y = __double2bfloat16(v[r].y);
+                    // lane → K elements 2·lane..2·lane+1 = chunk lane/4, byte (lane%4)*4
+                    *reinterpret_cast<__nv_bfloat162*>(A + sw128(row, lane >> 2) + (lane & 3) * 4) = b2;
+                }
             }
             // B: 64 rows × 8 chunks of 16 B from the BF16 centroid copy
             for (int e = threadIdx.x; e < TC_N * 8; e += TC_PRODUCERS * 32) {
