@@ -111,8 +111,8 @@ struct Vec<float, 4> {
 // Traffic: reads X, S, Θ, L_t; writes L', S', Θ' — 7·d·n·sizeof(T).
 // L, S, Θ are updated in place (each element is owned by one thread).
 // ---------------------------------------------------------------------------
-template <typename T, int R, int U>
-__global__ void __launch_bounds__(256) k_pass_f(
+template <typename T, int R, int U, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_pass_f(
     const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members,
     // G0/G1 and Gn0/Gn1 are the same two buffers: G_t is read from

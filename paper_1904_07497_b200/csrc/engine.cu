@@ -221,16 +221,35 @@ struct Alm : AlmBase {
     }
 
     // ---- one iteration of the fast path, captured ----------------------
-    void launch_pass_f() {
+    // Pass F variants (RESPCA_PASSF, tuning only): members per batch U / min
+    // blocks per SM.  Default 4 = U 8, 1 block/SM: 89% of measured HBM peak at C3
+    // (U 4: 79%, U 2 with 2 blocks/SM: 87%, U 12/16 spill).
+    int passf_variant = [] {
+        const char* e = std::getenv("RESPCA_PASSF");
+        return e ? std::atoi(e) : 4;
+    }();
+    template <int RR, int U, int MB>
+    void launch_pf() {
         double* G1 = G.p + (size_t)d * c;
-        if (R == 2)
-            k_pass_f<T, 2, 4><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
-                                                   G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
-                                                   partials.p, d, rowblocks);
-        else
-            k_pass_f<T, 1, 4><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
-                                                   G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
-                                                   partials.p, d, rowblocks);
+        k_pass_f<T, RR, U, MB><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                    G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
+                                                    partials.p, d, rowblocks);
+    }
+    void launch_pass_f() {
+        if (R == 2) {
+            switch (passf_variant) {
+                case 1: launch_pf<2, 4, 2>(); break;
+                case 2: launch_pf<2, 2, 2>(); break;
+                case 3: launch_pf<2, 2, 3>(); break;
+                case 4: launch_pf<2, 8, 1>(); break;
+                case 5: launch_pf<2, 6, 1>(); break;
+                case 6: launch_pf<2, 12, 1>(); break;
+                case 7: launch_pf<2, 16, 1>(); break;
+                default: launch_pf<2, 4, 1>(); break;
+            }
+        } else {
+            launch_pf<1, 4, 1>();
+        }
         ln.add();
     }
     void launch_pass_a() {
