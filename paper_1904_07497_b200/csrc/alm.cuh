@@ -221,6 +221,183 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
 }
 
 // ---------------------------------------------------------------------------
+// ℓ2,1 variant of the iteration (sparse_norm = L21, solver.cpp:90-102), split
+// around the column norms of B that the shrinkage needs:
+//   F1: D-form, L' (+ Cw sums, dL and scatter partials)          reads 4N, writes 1N
+//   column norms ‖B_j‖ = sqrt(Σ_i B_ij²), B = (x − L') + θ/ρ, sequential over i
+//   F2: S' = ‖B_j‖ <= 1/ρ ? 0 : (1 − (1/ρ)/‖B_j‖)·B_j, Θ', G_{t+1}, feas/dS partials
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_pass_f1(
+    const T* __restrict__ X, T* __restrict__ L, const T* __restrict__ S, const T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members, const double* G0,
+    const double* G1, double* __restrict__ Cw, const double* __restrict__ mean_w,
+    const Ctl* __restrict__ ctl, double* __restrict__ partials, int64_t d, int rowblocks) {
+    __shared__ double red[32 * 5];
+    if (ctl->done) return;
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
+    const bool active = i0 < d;
+    const double* Gc = ctl->parity ? G1 : G0;
+    const double rho = ctl->rho, own_w = ctl->own_w, mw = mean_w[g];
+    const int beg = goff[g], end = goff[g + 1];
+    const double ng = (double)(end - beg);
+    const double mscale = own_w / ng + mw;
+    double pl = 0.0, psc = 0.0;
+    if (active) {
+        double G[R], cacc[R], mt[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            G[r] = Gc[(int64_t)g * d + i0 + r];
+            mt[r] = G[r] * mscale;
+            cacc[r] = 0.0;
+        }
+        for (int t = beg; t < end; ++t) {
+            const int64_t off = (int64_t)__ldg(members + t) * d + i0;
+            Vec<T, R> xv, sv, tv, lv;
+            xv.load(X + off);
+            sv.load(S + off);
+            tv.load(Th + off);
+            lv.load_cs(L + off);
+            double lo[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double dv = (xv.v[r] - sv.v[r]) + tv.v[r] / rho;   // solver.cpp:163-164
+                const double ln = own_w * dv + mw * G[r];                   // solver.cpp:72
+                cacc[r] += ln;
+                const double dl = ln - lv.v[r];
+                pl += dl * dl;
+                const double dm = ln - mt[r];
+                psc += dm * dm;
+                lo[r] = ln;
+            }
+            Vec<T, R>::store(L + off, lo);
+        }
+        const double inv = 1.0 / ng;
+#pragma unroll
+        for (int r = 0; r < R; ++r) Cw[(int64_t)g * d + i0 + r] = cacc[r] * inv;
+    }
+    double v[5] = {0.0, pl, 0.0, 0.0, psc};
+    block_sum<5>(v, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
+}
+
+// ‖B_j‖ for the ℓ2,1 shrinkage: exact sequential chain per column, warp-
+// transposed tiles (lane = column), ρ read from the control block
+template <typename T>
+__global__ void __launch_bounds__(128) k_bnorms(const T* __restrict__ X, const T* __restrict__ L,
+                                                const T* __restrict__ Th,
+                                                const Ctl* __restrict__ ctl, int64_t d, int64_t n,
+                                                double* __restrict__ out) {
+    __shared__ double tile[4][32][33];
+    if (ctl->done) return;
+    const double rho = ctl->rho;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int64_t j0 = ((int64_t)blockIdx.x * 4 + w) * 32;
+    if (j0 >= n) return;
+    double acc = 0.0;
+    for (int64_t i0 = 0; i0 < d; i0 += 32) {
+        const int64_t i = i0 + lane;
+        for (int cc = 0; cc < 32; ++cc) {
+            const int64_t j = j0 + cc;
+            double v = 0.0;
+            if (j < n && i < d) {
+                const int64_t e = j * d + i;
+                v = (ld(X + e) - ld(L + e)) + ld(Th + e) / rho;  // solver.cpp:172-173
+            }
+            tile[w][cc][lane] = v;
+        }
+        __syncwarp();
+        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
+        for (int r = 0; r < lim; ++r) {
+            const double v = tile[w][lane][r];
+            acc += v * v;  // column_l2_norms, matrix.cpp:117-125
+        }
+        __syncwarp();
+    }
+    if (j0 + lane < n) out[j0 + lane] = sqrt(acc);
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_pass_f2(
+    const T* __restrict__ X, const T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members, const double* __restrict__ bn,
+    double* Gn0, double* Gn1, const Ctl* __restrict__ ctl, double* __restrict__ partials,
+    int64_t d, int rowblocks) {
+    __shared__ double red[32 * 5];
+    if (ctl->done) return;
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
+    const bool active = i0 < d;
+    double* Gn = ctl->parity ? Gn0 : Gn1;
+    const double rho = ctl->rho, rho_n = ctl->rho_next, thr = ctl->thr;
+    const int beg = goff[g], end = goff[g + 1];
+    double pf = 0.0, ps = 0.0;
+    if (active) {
+        double gacc[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) gacc[r] = 0.0;
+        for (int t = beg; t < end; ++t) {
+            const int jm = __ldg(members + t);
+            const int64_t off = (int64_t)jm * d + i0;
+            const double nrm = __ldg(bn + jm);
+            const bool zero = nrm <= thr;                        // solver.cpp:95
+            const double scale = zero ? 0.0 : 1.0 - thr / nrm;   // solver.cpp:96
+            Vec<T, R> xv, lv, sv, tv;
+            xv.load(X + off);
+            lv.load(L + off);
+            sv.load_cs(S + off);
+            tv.load_cs(Th + off);
+            double so[R], to[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double x = xv.v[r], th = tv.v[r];
+                const double xl = x - lv.v[r];
+                const double b = xl + th / rho;
+                const double sn = zero ? 0.0 : scale * b;        // solver.cpp:99
+                const double rr = xl - sn;
+                const double tn = th + rho * rr;                 // solver.cpp:107-108
+                gacc[r] += (x - sn) + tn / rho_n;
+                pf += rr * rr;
+                const double ds = sn - sv.v[r];
+                ps += ds * ds;
+                so[r] = sn;
+                to[r] = tn;
+            }
+            Vec<T, R>::store(S + off, so);
+            Vec<T, R>::store(Th + off, to);
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r) Gn[(int64_t)g * d + i0 + r] = gacc[r];
+    }
+    double v[2] = {pf, ps};
+    block_sum<2>(v, red);
+    if (threadIdx.x == 0) {
+        partials[(int64_t)blockIdx.x * 5 + 0] += v[0];
+        partials[(int64_t)blockIdx.x * 5 + 2] += v[1];
+    }
+}
+
+// Σ_j ‖S'_j‖ (report-only ℓ2,1 term): ‖S'_j‖ = max(0, 1 − t/‖B_j‖)·‖B_j‖
+__global__ void k_l21_term(const double* __restrict__ bn, int64_t n, Ctl* __restrict__ ctl) {
+    __shared__ double red[32];
+    if (ctl->done) return;
+    const double thr = ctl->thr;
+    double s = 0.0;
+    for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+        const double nr = bn[j];
+        if (!(nr <= thr)) s += (1.0 - thr / nr) * nr;
+    }
+    double v[1] = {s};
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) ctl->sparse_term = v[0];
+}
+
+// ---------------------------------------------------------------------------
 // Ordered group sums: out[i,g] = Σ_{j∈g, ascending} f(j, i), with
 //   mode 0 (D-form):  f = (x − s) + θ/ρ   (solver.cpp:163-164, summed at 61-65)
 //   mode 1 (plain):   f = m[i,j]          (means_of / column_mean sums, kmeans.cpp:70-75)
@@ -305,8 +482,9 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
         const double feas = sqrt(v[0]) / k.xnorm;  // solver.cpp:20, 30
         const double dl = sqrt(v[1]) / k.xnorm;
         const double ds = sqrt(v[2]) / k.xnorm;
-        const double obj = k.lambda * v[4] + v[3];  // solver.cpp:194-195
-        k.last_l1 = v[3];
+        const double sparse = k.l21 ? k.sparse_term : v[3];  // elementwise_l1 | l21_norm
+        const double obj = k.lambda * v[4] + sparse;  // solver.cpp:191-195
+        k.last_l1 = sparse;
         k.changed = 0;
         k.moves = 0;
         k.ambiguous = 0;

@@ -39,6 +39,8 @@ struct Ctl {
     int amb_list_len;
     double last_l1;   // ‖S‖₁ of the last finalized iteration (objective patch-up)
     unsigned int margin_hist[6];  // diagnostics: columns whose relative decision margin < 1e-1..1e-6
+    int l21;          // sparse_norm = L21: the sparse term comes from `sparse_term`
+    double sparse_term;
     unsigned long long exact_fallbacks;
 };
 

@@ -87,7 +87,8 @@ struct Alm : AlmBase {
     int R = 1, rowblocks = 0, nbF = 0;
 
     DBuf<T> X, L, S, Th;
-    DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm;
+    DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm, bn;
+    bool l21 = false;
     DBuf<int> labels, labels_new;
     DBuf<Ctl> ctl;
     KMeansEngine<T> km;
@@ -174,6 +175,8 @@ struct Alm : AlmBase {
         h.iter = 0;
         h.budget = (int)std::min<uint64_t>(budget, 0x7fffffff);
         h.fixed = cfg.has_fixed_iters ? 1 : 0;
+        l21 = cfg.sparse_norm == RESPCA_L21;
+        h.l21 = l21 ? 1 : 0;
         write_ctl(h);
     }
 
@@ -236,6 +239,19 @@ struct Alm : AlmBase {
                                                     partials.p, d, rowblocks);
     }
     void launch_pass_f() {
+        if (l21) {  // ℓ2,1: F1 only (the S/Θ half runs after the column norms)
+            double* G1 = G.p + (size_t)d * c;
+            if (R == 2)
+                k_pass_f1<T, 2><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                    G.p, G1, Cw.p, mean_w.p, ctl.p, partials.p, d,
+                                                    rowblocks);
+            else
+                k_pass_f1<T, 1><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                    G.p, G1, Cw.p, mean_w.p, ctl.p, partials.p, d,
+                                                    rowblocks);
+            ln.add();
+            return;
+        }
         if (R == 2) {
             switch (passf_variant) {
                 case 1: launch_pf<2, 4, 2>(); break;
@@ -260,12 +276,27 @@ struct Alm : AlmBase {
         k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
         ln.add();
     }
+    // ℓ2,1 second half: ‖B_j‖, S'/Θ'/G_{t+1}, the ℓ2,1 report term
+    void launch_post() {
+        if (!l21) return;
+        bn.ensure(n);
+        double* G1 = G.p + (size_t)d * c;
+        k_bnorms<T><<<ceil_div(n, 128), 128, 0, st>>>(X.p, L.p, Th.p, ctl.p, d, n, bn.p);
+        if (R == 2)
+            k_pass_f2<T, 2><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                bn.p, G.p, G1, ctl.p, partials.p, d, rowblocks);
+        else
+            k_pass_f2<T, 1><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                                bn.p, G.p, G1, ctl.p, partials.p, d, rowblocks);
+        k_l21_term<<<1, 1024, 0, st>>>(bn.p, n, ctl.p);
+        ln.add(3);
+    }
     void launch_finalize(bool cond) {
         k_finalize<<<1, 1024, 0, st>>>(ctl.p, partials.p, nbF, km.goff.p, mean_w.p, c, rep.p,
                                        cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
         ln.add();
     }
-    int kernels_per_iter() const { return 1 + (c > 1 ? 6 : 0) + 1; }
+    int kernels_per_iter() const { return 1 + (c > 1 ? 6 : 0) + 1 + (l21 ? 3 : 0); }
 
     void capture() {
         const uint64_t saved = *ln.counter;  // captured launches are not executions
@@ -273,11 +304,13 @@ struct Alm : AlmBase {
         wg.begin(st);
         launch_pass_f();
         launch_pass_a();
+        launch_post();
         launch_finalize(true);
         wg.end(st);
         // plain graph of everything after Pass F (bench timing of Pass F by events)
         rest.begin(st);
         launch_pass_a();
+        launch_post();
         launch_finalize(false);
         rest.end(st);
         *ln.counter = saved;
@@ -583,8 +616,8 @@ int respca_cu_solve(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, i
                     respca_cu_report* rep) {
     return guarded(ctx, [&] {
         if (!x || !cfg || !L_out || !S_out || !labels_out) throw InvalidArg("respca_cu_solve: null pointer");
-        if (cfg->sparse_norm != RESPCA_L1)
-            throw InvalidArg("respca_cu_solve: sparse_norm L21 is not implemented on the device path yet");
+        if (cfg->sparse_norm != RESPCA_L1 && cfg->sparse_norm != RESPCA_L21)
+            throw InvalidArg("respca_cu_solve: unknown sparse_norm");
         if (dtype == RESPCA_F64)
             solve_impl<double>(ctx, (const double*)x, d, n, *cfg, (double*)L_out, (double*)S_out,
                                labels_out, rep);

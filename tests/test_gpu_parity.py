@@ -124,3 +124,22 @@ def test_kernel_launch_accounting(ctx):
     X = synth.rpca(64, 64, 3, 1.0, 0.05, seed=1)
     res = _solve(ctx, X, SolverConfig(c=3, tol=1e-6))
     assert ctx.launches() - before >= res.report.iters  # ≥ one kernel per iteration
+
+
+@pytest.mark.parametrize("seed,d,n,c", [(1, 40, 60, 3), (2, 37, 91, 4), (3, 120, 80, 1), (4, 64, 200, 8)])
+def test_l21_solve_bitwise(ctx, orc, seed, d, n, c):
+    """sparse_norm = L21 (solver.cpp:90-102, 176-178, 191-193) on the device:
+    bit-identical L, S, labels and iteration count vs the oracle."""
+    from paper_1904_07497_b200 import synth
+    from paper_1904_07497_b200.respca import SolverConfig
+
+    X = synth.rpca(d, n, 3, 1.0, 0.05, seed=seed)
+    for lam in (None, 0.3):
+        cfg = SolverConfig(c=c, tol=1e-7, sparse_norm="L21", lambda_=lam)
+        a = _solve(ctx, X, cfg)
+        b = orc.solve(X, cfg)
+        assert a.report.iters == b.iters
+        assert (a.assignment == b.labels).all()
+        assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
+        np.testing.assert_allclose(a.report.objective, b.objective, rtol=1e-9)
+        np.testing.assert_allclose(a.report.feas, b.feas, rtol=1e-10)
