@@ -79,6 +79,33 @@ def solve_case(name: str, gen: dict, X: np.ndarray, cfg: SolverConfig) -> dict:
     }
 
 
+def sketch_mats(d: int, n: int, k: int = 16, seed: int = 7):
+    """Seeded ±1 sketch matrices Ψ (d×k), Ω (n×k); relative Frobenius errors
+    are estimated as ‖Ψᵀ(A − B)Ω‖_F / ‖ΨᵀBΩ‖_F (JL-style, k² samples)."""
+    rng = np.random.default_rng(seed)
+    return (rng.integers(0, 2, (d, k)) * 2.0 - 1.0, rng.integers(0, 2, (n, k)) * 2.0 - 1.0)
+
+
+def sketch(a: np.ndarray, psi: np.ndarray, omega: np.ndarray) -> np.ndarray:
+    return psi.T @ (np.asarray(a, dtype=np.float64) @ omega)
+
+
+def workload_sketch(name: str) -> dict:
+    """Reference solve of a workload with tolerance fingerprints (for fp32 runs
+    that are compared within 1e-4 instead of bitwise)."""
+    w = synth.WORKLOADS[name]
+    X = w.make()
+    X = X.astype(np.float32).astype(np.float64)
+    r = O.reference().solve(X, w.solver_config())
+    psi, om = sketch_mats(*X.shape)
+    return {"case": name, "x_sha256": sha(X), "iters": r.iters,
+            "L_fro": float(np.linalg.norm(r.L)), "S_fro": float(np.linalg.norm(r.S)),
+            "L_sketch": sketch(r.L, psi, om).ravel().tolist(),
+            "S_sketch": sketch(r.S, psi, om).ravel().tolist(),
+            "S_nnz": int(np.count_nonzero(r.S)),
+            "S_support_hash": hashlib.sha256(np.packbits(np.asfortranarray(r.S) != 0).tobytes()).hexdigest()}
+
+
 def workload_case(name: str) -> dict:
     w = synth.WORKLOADS[name]
     X = w.make()
@@ -123,6 +150,11 @@ def main(argv: list[str]) -> None:
             cases = small_cases()
             (OUT / "small_solves.json").write_text(json.dumps(cases, indent=1))
             print("wrote small_solves.json", len(cases))
+        elif arg.startswith("sketch-"):
+            name = arg[len("sketch-"):]
+            rec = workload_sketch(name)
+            (OUT / f"sketch_{name}.json").write_text(json.dumps(rec))
+            print("wrote sketch", name)
         elif arg.startswith("init-"):
             # the reference's one-time kmeans(X) labels (solver.cpp:145-148):
             # the bench's reference arm replays the ALM loop from them
