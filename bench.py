@@ -136,6 +136,17 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def ncu_traffic(workload):
+    """DRAM bytes per Pass-F launch from the committed ncu capture
+    (profiles/ncu_traffic.json), or None when this workload was not captured."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            t = json.load(f).get(workload)
+        return None if t is None else t["read_bytes"] + t["write_bytes"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def dist_setup(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -367,7 +378,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
             "dtype": w.dtype, "data": "synthetic (seeded, respca-synth-1)",
             "config": {**workload_config(w), "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
-                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                         "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),
                          "kernel": "k_pass_f (fused L/S/Θ update + group sums + residuals)",
                          "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": pf_avg,
                          "peak_src": pk["src"],
