@@ -50,7 +50,7 @@ def build_cuda(force: bool = False) -> Path:
     deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [INC / "respca_cu.h"]
     if force or _stale(out, deps):
         _run([NVCC, *ARCH, *NVFLAGS, f"-I{INC}", f"-I{CSRC}", "-shared",
-              str(CSRC / "engine.cu"), "-o", str(out), "-lcudart"],
+              str(CSRC / "engine.cu"), "-o", str(out), "-lcudart", "-Xcompiler", "-pthread"],
              log=LIB / "ptxas_engine.log")
     return out
 

@@ -1,48 +1,35 @@
 // Exact sequential Hartigan refinement (kmeans.cpp:96-139) on the device.
 //
-// The reference visits columns j = 0..n−1 in order and applies each improving
-// single-point move at once (incremental centroid update, kmeans.cpp:122-135),
-// so every later decision sees the updated centroids and counts.  The device
-// keeps exactly that order:
+// The reference visits columns j = 0..n−1 in order, pass after pass (≤ 50),
+// and applies each improving single-point move at once (incremental centroid
+// update, kmeans.cpp:122-135), so every later decision sees the updated
+// centroids and counts.  The device keeps exactly that order with ONE
+// persistent cooperative kernel for the whole refinement (all passes):
 //
-//  * columns are processed in blocks of B.  At block start, the screened
-//    distance of every (block column, centroid) pair is computed by the DMMA
-//    screen (km.cuh) — an interval [a − e, a + e] that provably contains the
-//    reference's sq_dist;
-//  * a round (one kernel, CTA per 8 block columns) first refreshes the two
-//    entries of every remaining column that the previous move made stale (its
-//    `from` and `to` centroids), computing the moved centroids' new values on
-//    the fly with the reference's exact update formula (and writing them to
-//    the other slot of a double-buffered centroid store); then one warp per
-//    column decides it on the intervals; the last CTA to finish takes the
-//    FIRST column that is not provably "no move" (all columns before it
-//    provably do not move in the sequential order): a provable move is applied,
-//    an undecidable near-tie is resolved with the exact sequential chain.
+//  * every CTA owns `cpb` columns of the current block of B = G·cpb columns,
+//    cached in shared memory with their interval rows [a − e, a + e] (a
+//    screened sq_dist that provably contains the reference's value, km.cuh);
+//  * interval rows live in HBM between visits with a per-entry stamp: entry
+//    (j, k) is valid while centroid k has not moved since it was computed.  On
+//    entering a block a CTA recomputes only its stale entries (lazy refresh:
+//    late passes, with few moves, refresh almost nothing);
+//  * a round: (1a) every CTA writes one row slice of the previous move's two
+//    updated centroids (the reference's exact formula, into the other slot of
+//    a double-buffered store) plus the slice's ‖c′‖² partial; grid barrier;
+//    (1b) the owned columns still to visit refresh their two stale entries;
+//    (2) one warp per owned column decides it on the intervals and the
+//    smallest column that is not provably "no move" is elected (atomicMin);
+//    grid barrier; (3) every CTA settles the elected column identically — a
+//    provable move is applied to the replicated counts, an undecidable
+//    near-tie is resolved with the reference's own sequential chain.
 //
 // Labels, counts and centroids are therefore bit-identical to the reference.
-// Rounds run as a CUDA-graph WHILE loop; blocks and passes are stream-ordered
-// and the host only synchronises once per pass.
 #pragma once
 
 #include "km.cuh"
+#include "tc_screen.cuh"
 
 namespace respca_dev {
-
-struct HartState {
-    int cursor;        // next column to visit
-    int bend;          // end of the current block
-    int pass;          // 0..49
-    int improved;      // a move happened in this pass
-    int block_done;
-    int pending_from;  // centroid update of the last move, applied next round (-1: none)
-    int pending_to, pending_j, pending_nf, pending_nt;
-    int act_j;         // column the last CTA acts on
-    unsigned arrive;   // last-CTA election
-    unsigned long long first;  // packed (j, status, to) of the first non-trivial column
-    unsigned long long moves, exact_fallbacks, rounds;
-    unsigned long long t0, tsum;  // globaltimer: earliest CTA start of a round, summed round spans
-    unsigned long long tp1, tp2, sp1, sp2, sp3s;  // phase-end stamps (max over CTAs) and sums
-};
 
 RESPCA_DEV unsigned long long gtimer() {
     unsigned long long t;
@@ -50,78 +37,10 @@ RESPCA_DEV unsigned long long gtimer() {
     return t;
 }
 
-struct HartArrays {
-    double* A;       // [n][c] screened distance
-    double* E;       // [n][c] its half-width
-    double* xx;      // [n]    ‖x_j‖² (screen input)
-    int* labels;
-    int* counts;
-    double* C;       // [2][c][d] centroid slots (slot 0 = the caller's centroids)
-    int* ver;        // [c] current slot of centroid k
-    double* scratch; // [c] exact distances of one column
-    double kappa_d;  // screen bound factor (km.cuh)
-};
-
-RESPCA_DEV double* cslot(const HartArrays& h, int c, int64_t d, int k, int s) {
-    return h.C + ((int64_t)s * c + k) * d;
-}
-
-// Hartigan decision of column j on intervals (one warp):
+// Hartigan decision of one column on intervals (one warp), with the weights
+// wa[k] = n_k/(n_k−1), wb[k] = n_k/(n_k+1) (the reference's correctly-rounded
+// divisions, kmeans.cpp:107, 114):
 //   0 = provably no move, 1 = provably moves to `to`, 2 = undecidable
-template <typename IV>
-RESPCA_DEV int hart_decide_warp(int j, int c, const int* __restrict__ labels,
-                                const int* __restrict__ counts, const IV& iv, int& to) {
-    const int lane = threadIdx.x & 31;
-    const int from = labels[j];
-    const int cf = counts[from];
-    if (cf <= 1) return 0;  // kmeans.cpp:105
-    double flo, fhi, fmid;
-    iv(from, flo, fhi, fmid);
-    const double na = (double)cf;
-    const double wa = na / (na - 1.0);  // kmeans.cpp:107-108
-    const double g_lo = wa * flo, g_hi = wa * fhi, g_mid = wa * fmid;
-    double bd = INFINITY;
-    int bk = 0x7fffffff;
-    bool none = true;
-    for (int k = lane; k < c; k += 32) {
-        if (k == from) continue;
-        double lo, hi, mid;
-        iv(k, lo, hi, mid);
-        const double nb = (double)counts[k];
-        const double wb = nb / (nb + 1.0);  // kmeans.cpp:113-115
-        none &= !(wb * lo - g_hi < -1e-12);
-        const double dmid = wb * mid - g_mid;
-        if (dmid < bd) {
-            bd = dmid;
-            bk = k;
-        }
-    }
-    none = __all_sync(0xffffffffu, none);
-    if (none) return 0;
-    warp_argmin(bd, bk);
-    if (bk >= c) return 2;
-    double blo, bhi, bmid;
-    iv(bk, blo, bhi, bmid);
-    const double nbk = (double)counts[bk];
-    const double dhi_k = (nbk / (nbk + 1.0)) * bhi - g_lo;
-    bool ok = dhi_k < -1e-12;  // kmeans.cpp:116 with best_delta = -1e-12
-    for (int k = lane; k < c; k += 32) {
-        if (k == from || k == bk) continue;
-        double lo, hi, mid;
-        iv(k, lo, hi, mid);
-        const double nb = (double)counts[k];
-        const double dlo = (nb / (nb + 1.0)) * lo - g_hi;
-        if (k < bk) ok &= dhi_k < dlo;  // an earlier k must lose strictly
-        else ok &= dhi_k <= dlo;        // a later k never replaces an equal delta
-    }
-    ok = __all_sync(0xffffffffu, ok);
-    if (!ok) return 2;
-    to = bk;
-    return 1;
-}
-
-// same decision with precomputed weights wa[k] = n_k/(n_k−1), wb[k] = n_k/(n_k+1)
-// (the identical correctly-rounded divisions) and per-CTA counts
 template <typename IV>
 RESPCA_DEV int hart_decide_warp_w(int from, int c, const int* cnt, const double* wa,
                                   const double* wb, const IV& iv, int& to) {
@@ -139,7 +58,7 @@ RESPCA_DEV int hart_decide_warp_w(int from, int c, const int* cnt, const double*
         double lo, hi, mid;
         iv(k, lo, hi, mid);
         const double w_b = wb[k];
-        none &= !(w_b * lo - g_hi < -1e-12);
+        none &= !(w_b * lo - g_hi < -1e-12);  // kmeans.cpp:116, best_delta = -1e-12
         const double dmid = w_b * mid - g_mid;
         if (dmid < bd) {
             bd = dmid;
@@ -159,8 +78,8 @@ RESPCA_DEV int hart_decide_warp_w(int from, int c, const int* cnt, const double*
         double lo, hi, mid;
         iv(k, lo, hi, mid);
         const double dlo = wb[k] * lo - g_hi;
-        if (k < bk) ok &= dhi_k < dlo;
-        else ok &= dhi_k <= dlo;
+        if (k < bk) ok &= dhi_k < dlo;  // an earlier k must lose strictly
+        else ok &= dhi_k <= dlo;        // a later k never replaces an equal delta
     }
     ok = __all_sync(0xffffffffu, ok);
     if (!ok) return 2;
@@ -168,259 +87,33 @@ RESPCA_DEV int hart_decide_warp_w(int from, int c, const int* cnt, const double*
     return 1;
 }
 
-RESPCA_DEV unsigned long long pack_first(int j, int status, int to) {
-    return ((unsigned long long)(unsigned)j << 32) | ((unsigned long long)status << 24) |
-           (unsigned long long)(unsigned)(to & 0xffffff);
-}
-
-template <typename T, int CPB>
-__global__ void __launch_bounds__(512) k_hart_round(const T* __restrict__ M,
-                                                    HartState* __restrict__ hs, HartArrays h,
-                                                    int64_t d, int n, int c,
-                                                    cudaGraphConditionalHandle cond) {
-    constexpr int NV = 2 + 2 * CPB;
-    __shared__ double red[32 * NV];
-    __shared__ bool s_last;
-    __shared__ int s_st, s_to;
-    const bool has_cond = cond != 0;
-    if (hs->block_done) {
-        if (blockIdx.x == 0 && threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
-        return;
-    }
-    if (threadIdx.x == 0) atomicMin(&hs->t0, gtimer());
-    const int cursor = hs->cursor, bend = hs->bend;
-    const int jb = cursor + blockIdx.x * CPB;  // first column of this CTA
-    const int pf = hs->pending_from;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-
-    // ---- phase 1: apply the pending move's centroid update (kmeans.cpp:126-131)
-    //      and refresh the (column, from/to) entries of this CTA's columns
-    if (pf >= 0) {
-        const int pt = hs->pending_to, pm = hs->pending_j;
-        const double dcf = (double)hs->pending_nf, dct = (double)hs->pending_nt;
-        const double na1 = (double)(hs->pending_nf - 1), nb1 = (double)(hs->pending_nt + 1);
-        const int vf = h.ver[pf], vt = h.ver[pt];
-        const double* of = cslot(h, c, d, pf, vf);
-        const double* ot = cslot(h, c, d, pt, vt);
-        double* nf_ = cslot(h, c, d, pf, 1 - vf);
-        double* nt_ = cslot(h, c, d, pt, 1 - vt);
-        const T* xm = M + (int64_t)pm * d;
-        const int64_t slice = (d + gridDim.x - 1) / gridDim.x;
-        const int64_t s0 = (int64_t)blockIdx.x * slice, s1 = s0 + slice;
-        bool active = false;
-        for (int q = 0; q < CPB; ++q) active |= (jb + q < bend);
-        double v[NV];
-#pragma unroll
-        for (int q = 0; q < NV; ++q) v[q] = 0.0;
-        const int64_t ibeg = active ? 0 : s0, iend = active ? d : (s1 < d ? s1 : d);
-#pragma unroll 4
-        for (int64_t i = ibeg + threadIdx.x; i < iend; i += blockDim.x) {
-            const double x = (double)xm[i];
-            const double cf = (of[i] * dcf - x) / na1;
-            const double ct = (ot[i] * dct + x) / nb1;
-            if (i >= s0 && i < s1) {
-                nf_[i] = cf;
-                nt_[i] = ct;
-            }
-            if (active) {
-                v[0] = __fma_rn(cf, cf, v[0]);
-                v[1] = __fma_rn(ct, ct, v[1]);
-#pragma unroll
-                for (int q = 0; q < CPB; ++q) {
-                    const int j = jb + q;
-                    if (j < bend) {
-                        const double xj = (double)__ldg(M + (int64_t)j * d + i);
-                        v[2 + 2 * q] = __fma_rn(xj, cf, v[2 + 2 * q]);
-                        v[3 + 2 * q] = __fma_rn(xj, ct, v[3 + 2 * q]);
-                    }
-                }
-            }
-        }
-        if (active) {  // block-uniform
-            block_sum<NV>(v, red);
-            if (threadIdx.x < 2 * CPB) {
-                const int q = threadIdx.x >> 1, which = threadIdx.x & 1;
-                const int j = jb + q;
-                if (j < bend) {
-                    const int k = which ? pt : pf;
-                    double dot = 0.0;
-#pragma unroll
-                    for (int r = 0; r < 2 * CPB; ++r)
-                        if (r == (int)threadIdx.x) dot = v[2 + r];
-                    const double cck = which ? v[1] : v[0];
-                    const double xxj = h.xx[j];
-                    const double mid = (xxj + cck) - 2.0 * dot;
-                    const double e = screen_err(h.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
-                    const int64_t idx = (int64_t)j * c + k;
-                    h.A[idx] = mid;
-                    h.E[idx] = isfinite(mid) && isfinite(e) ? e : INFINITY;
-                }
-            }
-        }
-        __syncthreads();
-    }
-
-    if (threadIdx.x == 0) atomicMax(&hs->tp1, gtimer());
-    // ---- phase 2: decide this CTA's columns (warp per column)
-    if (warp < CPB) {
-        const int j = jb + warp;
-        if (j < bend) {
-            int to = -1;
-            auto iv = [&](int k, double& lo, double& hi, double& mid) {
-                const int64_t idx = (int64_t)j * c + k;
-                mid = h.A[idx];
-                const double e = h.E[idx];
-                lo = mid - e;
-                hi = mid + e;
-            };
-            const int st = hart_decide_warp(j, c, h.labels, h.counts, iv, to);
-            if (st != 0 && lane == 0) atomicMin(&hs->first, pack_first(j, st, to));
-        }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        atomicMax(&hs->tp2, gtimer());
-        __threadfence();
-        s_last = atomicAdd(&hs->arrive, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (!s_last) return;
-
-    // ---- phase 3 (last CTA): settle the round
-    __threadfence();
-    if (threadIdx.x == 0) {
-        const unsigned long long t3 = gtimer();
-        hs->sp1 += hs->tp1 - hs->t0;
-        hs->sp2 += hs->tp2 - hs->t0;
-        hs->sp3s += t3 - hs->t0;
-        hs->tp1 = 0;
-        hs->tp2 = 0;
-        hs->arrive = 0;
-        hs->rounds += 1;
-        if (pf >= 0) {  // the new centroid values are complete: switch slots
-            h.ver[pf] ^= 1;
-            h.ver[hs->pending_to] ^= 1;
-            hs->pending_from = -1;
-        }
-        const unsigned long long f = hs->first;
-        hs->first = ~0ULL;
-        if (f == ~0ULL) {
-            s_st = -1;
-            hs->cursor = bend;
-        } else {
-            s_st = (int)((f >> 24) & 0xff);
-            s_to = (int)(f & 0xffffff);
-            hs->act_j = (int)(f >> 32);
-        }
-        __threadfence();
-    }
-    __syncthreads();
-    if (s_st == 2) {  // near-tie: the reference's own sequential chain (kmeans.cpp:12-19)
-        const int j = hs->act_j;
-        const T* x = M + (int64_t)j * d;
-        for (int k = threadIdx.x; k < c; k += blockDim.x) {
-            const double* cv = cslot(h, c, d, k, h.ver[k]);
-            double s = 0.0;
-            for (int64_t i = 0; i < d; ++i) {
-                const double t = (double)x[i] - cv[i];
-                s += t * t;
-            }
-            h.scratch[k] = s;
-        }
-        __syncthreads();
-        if (warp == 0) {
-            int to = -1;
-            auto iv = [&](int k, double& lo, double& hi, double& mid) {
-                mid = h.scratch[k];
-                lo = hi = mid;
-            };
-            const int st = hart_decide_warp(j, c, h.labels, h.counts, iv, to);
-            if (lane == 0) {
-                s_st = st;
-                s_to = to;
-                hs->exact_fallbacks += 1;
-            }
-        }
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-        if (s_st == 0) {
-            hs->cursor = hs->act_j + 1;
-        } else if (s_st == 1) {  // bookkeeping of the move (kmeans.cpp:132-135)
-            const int j = hs->act_j, from = h.labels[j], to = s_to;
-            const int nf = h.counts[from], nt = h.counts[to];
-            h.counts[from] = nf - 1;
-            h.counts[to] = nt + 1;
-            h.labels[j] = to;
-            hs->pending_j = j;
-            hs->pending_from = from;
-            hs->pending_to = to;
-            hs->pending_nf = nf;
-            hs->pending_nt = nt;
-            hs->improved = 1;
-            hs->moves += 1;
-            hs->cursor = j + 1;
-        }
-        const int done = hs->cursor >= bend && hs->pending_from < 0;
-        hs->block_done = done;
-        hs->tsum += gtimer() - hs->t0;
-        hs->t0 = ~0ULL;
-        __threadfence();
-        if (has_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
-    }
-}
-
-// block start: intervals of every (block column, centroid) pair from the screen
-__global__ void k_hart_fill(Screen sc, HartArrays h, int j0, int nb, int c) {
+// intervals of every (column, centroid) pair from a full screen (start state)
+__global__ void k_hart_fill(Screen sc, double* __restrict__ A, double* __restrict__ E,
+                            double* __restrict__ xx, int n, int c) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= (int64_t)nb * c) return;
-    const int jl = (int)(e / c), k = (int)(e % c);
-    const double xxj = sc.xx(jl);
+    if (e >= (int64_t)n * c) return;
+    const int j = (int)(e / c), k = (int)(e % c);
+    const double xxj = sc.xx(j);
     double lo, hi, mid;
-    sc.get(jl, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
-    const int64_t idx = (int64_t)(j0 + jl) * c + k;
-    h.A[idx] = mid;
-    h.E[idx] = isfinite(hi - mid) ? hi - mid : INFINITY;
-    if (k == 0) h.xx[j0 + jl] = xxj;
+    sc.get(j, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
+    A[e] = mid;
+    E[e] = isfinite(hi - mid) ? hi - mid : INFINITY;
+    if (k == 0) xx[j] = xxj;
 }
 
-__global__ void k_hart_block_begin(HartState* hs, int b0, int bend) {
-    hs->cursor = b0;
-    hs->bend = bend;
-    hs->block_done = 0;
-    hs->first = ~0ULL;
-    hs->arrive = 0;
-    hs->t0 = ~0ULL;
-}
-
-// copy centroids living in slot 1 back to slot 0 (the screen reads slot 0)
-__global__ void k_hart_consolidate(HartArrays h, int64_t d, int c) {
+// copy centroids living in slot 1 back to slot 0, reset the slot map
+__global__ void k_hart_consolidate(double* __restrict__ Cs, const int* __restrict__ ver, int64_t d,
+                                   int c) {
     for (int k = blockIdx.y; k < c; k += gridDim.y) {
-        if (h.ver[k] == 0) continue;
-        const double* src = h.C + ((int64_t)c + k) * d;
-        double* dst = h.C + (int64_t)k * d;
+        if (ver[k] == 0) continue;
+        const double* src = Cs + ((int64_t)c + k) * d;
+        double* dst = Cs + (int64_t)k * d;
         for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d;
              i += (int64_t)gridDim.x * blockDim.x)
             dst[i] = src[i];
     }
 }
-__global__ void k_hart_ver_reset(HartArrays h, int c) {
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < c; k += gridDim.x * blockDim.x)
-        h.ver[k] = 0;
-}
 
-}  // namespace respca_dev
-
-namespace respca_dev {
-
-// ---------------------------------------------------------------------------
-// Persistent cooperative variant: one launch per block of columns, every CTA
-// resident (cudaLaunchCooperativeKernel), rounds separated by ONE grid barrier.
-// Each CTA owns up to `cpb` block columns, caches them in shared memory, keeps
-// their interval rows in shared memory, and replicates the small sequential
-// state (counts, Hartigan weights, slot versions, cursor, pending move) so
-// that every CTA settles a round identically from the elected first column.
-// ---------------------------------------------------------------------------
 struct HartGlobal {
     // each hot word on its own 128-byte line: the barrier spin, the barrier
     // arrivals and the per-round election slots must not share L2 lines
@@ -428,11 +121,10 @@ struct HartGlobal {
     alignas(128) unsigned bar_gen;
     alignas(128) unsigned long long first[3][16];  // per-round election slots, round r uses r % 3
     alignas(128) unsigned long long xres;          // exact-fallback verdict broadcast
-    alignas(128) int cursor, improved;
-    unsigned long long moves, exact_fallbacks, rounds;
-    unsigned long long t_kernel, t_phase1, t_phase2;  // globaltimer sums (CTA 0)
-    unsigned long long t_phase1_max;                  // max over CTAs of summed phase-1 time
-    unsigned long long tmax[6];  // per-CTA sums, max over CTAs: 1a, barrier A, 1b, decide, barrier B, settle
+    alignas(128) unsigned long long moves, exact_fallbacks, rounds, passes, blocks, refreshed;
+    unsigned long long t_kernel, t_load, t_cols;  // globaltimer (CTA 0): whole kernel, block loads, column fills
+    unsigned long long stale_sum, heavy_blocks;   // CTA 0: stale centroids over all block entries, entries with > 8
+    unsigned long long tm[8];  // CTA 0 phase sums: 1, entry tiles, entry barrier, entry reduce, decide, barrier, settle
 };
 
 RESPCA_DEV void grid_barrier(HartGlobal* g) {
@@ -462,66 +154,148 @@ RESPCA_DEV unsigned long long pack4(int j, int st, int from, int to) {
 __global__ void k_hart_first_reset(HartGlobal* g) {
     g->first[0][0] = g->first[1][0] = g->first[2][0] = ~0ULL;
 }
-__global__ void k_hart_improved_reset(HartGlobal* g) { g->improved = 0; }
 
-// v[2q], v[2q+1] += Σ_i x_{q0+q}[i]·f[i], x·t[i] for the NQ active owned columns
-// (thread-strided rows, FMA chains; only ever used inside the screen bound)
-template <typename T, int NQ>
-RESPCA_DEV void hart_dots(double* v, const double* __restrict__ f, const double* __restrict__ t,
-                          const T* colc, const T* __restrict__ M, int jown, int q0, int nact,
-                          int64_t d, int cache_cols) {
-    // v[2q], v[2q+1] = Σ_i x_{q0+q}[i]·f[i], ·t[i] for the nact (≤ NQ) active owned
-    // columns (FMA chains; only ever used inside the screen bound)
-    double acc[2 * NQ];
-#pragma unroll
-    for (int q = 0; q < 2 * NQ; ++q) acc[q] = 0.0;
-    const T* base[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int qq = q < nact ? q0 + q : q0;
-        base[q] = cache_cols ? colc + (int64_t)qq * d : M + (int64_t)(jown + qq) * d;
+// bulk global→shared copy (async proxy), completion counted on `bar`
+RESPCA_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+RESPCA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+RESPCA_DEV void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+struct HartArgs {
+    HartGlobal* g;
+    int* labels;          // [n]   (device copy, written by CTA 0)
+    int* counts;          // [c]   in: start counts, out: final counts
+    double* Cs;           // [2][c][d] centroid slots; slot 0 holds the start centroids
+    int* ver;             // [c]   out: slot of each final centroid
+    double* A;            // [n][c] interval mid-points
+    double* E;            // [n][c] interval half-widths
+    int* ebuf;            // [blocks] move count at the last entry of each block (0)
+    double* part;         // [G][B][c] row-slice partial dots of the block refresh
+    const double* xx;     // [n]   ‖x_j‖² (screen)
+    const double* cc0;    // [c]   ‖c_k‖² of the start centroids (screen)
+    double* scratch;      // [c]   exact distances of one column (near-tie)
+    int64_t d;
+    int n, c, cpb, cache_cols, max_pass, stage_rows;
+    double kappa_d;       // screen bound factor (km.cuh) + the reciprocal-update term
+};
+
+constexpr int HART_RED = 32 * 24;  // block_sum scratch (≤ 24 sums)
+constexpr int HART_MAXG = 160;     // max CTAs of the Hartigan kernel (partials per entry)
+
+constexpr int HART_NST = 4;  // cp.async stages of the block refresh
+
+RESPCA_DEV void cp_wait_dyn(int pending) {
+    switch (pending) {
+        case 0: cp_wait<0>(); break;
+        case 1: cp_wait<1>(); break;
+        case 2: cp_wait<2>(); break;
+        default: cp_wait<3>(); break;
     }
-    constexpr int UR = 4;
-    const int64_t step = (int64_t)blockDim.x;
-    int64_t i = threadIdx.x;
-    for (; i + (UR - 1) * step < d; i += UR * step) {
-        double fb[UR], tb[UR];
-#pragma unroll
-        for (int u = 0; u < UR; ++u) {
-            fb[u] = __ldcg(f + i + u * step);
-            tb[u] = __ldcg(t + i + u * step);
+}
+
+// Block refresh partials of one CTA: its row slice [s0, s1) of
+// x_jb · c_stale[t] for every block column jb < nb and stale centroid t, as
+// TQ×TK register tiles (a tile's columns / centroids strided by ntq / ntk so
+// that a warp reads consecutive shared words).  Row chunks of R rows stream
+// through HART_NST cp.async stages.  Output: part[(jb·c + t)·G + CTA].
+template <typename T, int TQ, int TK>
+RESPCA_DEV void hart_entry_tiles(const T* __restrict__ M, const HartArgs& a, const int* vs,
+                                 const int* stale, int nstale, int b0, int nb, int B, int64_t s0,
+                                 int64_t s1, int R, T* stc, double* sce) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int c = a.c, G = gridDim.x;
+    const int64_t d = a.d;
+    const int ntq = (nb + TQ - 1) / TQ, ntk = (nstale + TK - 1) / TK, ntiles = ntq * ntk;
+    const int nch = s1 > s0 ? (int)((s1 - s0 + R - 1) / R) : 0;
+    auto issue = [&](int ch) {
+        const int64_t c0 = s0 + (int64_t)ch * R;
+        const int rows = (int)(s1 - c0 < R ? s1 - c0 : R);
+        T* sb = stc + (size_t)(ch % HART_NST) * R * B;
+        double* cb = sce + (size_t)(ch % HART_NST) * R * c;
+        for (int e = tid; e < nb * rows; e += nt) {
+            const int jb = e / rows, rr = e - (e / rows) * rows;
+            const T* src = M + (int64_t)(b0 + jb) * d + c0 + rr;
+            if (sizeof(T) == 8) cp_async8(sb + rr * B + jb, src, true);
+            else cp_async4(sb + rr * B + jb, src, true);
         }
+        for (int e = tid; e < nstale * rows; e += nt) {
+            const int t = e / rows, rr = e - (e / rows) * rows;
+            const int k = stale[t];
+            cp_async8(cb + rr * c + t, a.Cs + ((int64_t)vs[k] * c + k) * d + c0 + rr, true);
+        }
+        cp_commit();
+    };
+    for (int tr0 = 0; tr0 < ntiles; tr0 += nt) {
+        const int tile = tr0 + tid;
+        const bool act = tile < ntiles;
+        const int tq = act ? tile / ntk : 0, tk = act ? tile - (tile / ntk) * ntk : 0;
+        double acc[TQ * TK];
 #pragma unroll
-        for (int u = 0; u < UR; ++u)
+        for (int e = 0; e < TQ * TK; ++e) acc[e] = 0.0;
+        __syncthreads();  // stage buffers free
+        int issued = 0;
+        for (; issued < nch && issued < HART_NST - 1; ++issued) issue(issued);
+        for (int ch = 0; ch < nch; ++ch) {
+            if (issued < nch) issue(issued++);  // refills the stage chunk ch−1 used
+            cp_wait_dyn(issued - ch - 1);
+            __syncthreads();
+            if (act) {
+                const int64_t c0 = s0 + (int64_t)ch * R;
+                const int rows = (int)(s1 - c0 < R ? s1 - c0 : R);
+                const T* sb = stc + (size_t)(ch % HART_NST) * R * B;
+                const double* cb = sce + (size_t)(ch % HART_NST) * R * c;
+                for (int rr = 0; rr < rows; ++rr) {
+                    double xq[TQ], ck[TK];
 #pragma unroll
-            for (int q = 0; q < NQ; ++q)
-                if (q < nact) {
-                    const double x = (double)base[q][i + u * step];
-                    acc[2 * q] = __fma_rn(x, fb[u], acc[2 * q]);
-                    acc[2 * q + 1] = __fma_rn(x, tb[u], acc[2 * q + 1]);
+                    for (int u = 0; u < TQ; ++u) {
+                        const int jb = tq + u * ntq;
+                        xq[u] = jb < nb ? (double)sb[rr * B + jb] : 0.0;
+                    }
+#pragma unroll
+                    for (int w = 0; w < TK; ++w) {
+                        const int t = tk + w * ntk;
+                        ck[w] = t < nstale ? cb[rr * c + t] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < TQ; ++u)
+#pragma unroll
+                        for (int w = 0; w < TK; ++w) acc[u * TK + w] = __fma_rn(xq[u], ck[w], acc[u * TK + w]);
                 }
-    }
-    for (; i < d; i += step) {
-        const double fv = __ldcg(f + i), tv = __ldcg(t + i);
-#pragma unroll
-        for (int q = 0; q < NQ; ++q)
-            if (q < nact) {
-                const double x = (double)base[q][i];
-                acc[2 * q] = __fma_rn(x, fv, acc[2 * q]);
-                acc[2 * q + 1] = __fma_rn(x, tv, acc[2 * q + 1]);
             }
-    }
+            __syncthreads();  // chunk consumed before its stage is refilled
+        }
+        if (act) {
 #pragma unroll
-    for (int q = 0; q < 2 * NQ; ++q) v[q] = acc[q];
+            for (int u = 0; u < TQ; ++u)
+#pragma unroll
+                for (int w = 0; w < TK; ++w) {
+                    const int jb = tq + u * ntq, t = tk + w * ntk;
+                    if (jb < nb && t < nstale)
+                        __stcg(a.part + ((size_t)jb * c + t) * G + blockIdx.x, acc[u * TK + w]);
+                }
+        }
+    }
 }
 
 template <typename T, int MAXQ>
-__global__ void __launch_bounds__(512, 1) k_hart_block(
-    const T* __restrict__ M, HartGlobal* __restrict__ hg, int* __restrict__ labels,
-    int* __restrict__ counts, double* __restrict__ Cs, int* __restrict__ ver,
-    Screen scr, double* __restrict__ scratch, double* __restrict__ ccpart, int64_t d, int c, int b0,
-    int bend, int cpb, int cache_cols, double kappa_d, int dbg) {
+__global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, HartArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
+    const int64_t d = a.d;
+    const int c = a.c, n = a.n, cpb = a.cpb, cache_cols = a.cache_cols;
+    HartGlobal* hg = a.g;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int nwarps = blockDim.x >> 5;
+    const int G = gridDim.x, B = G * cpb, R = a.stage_rows;
     // ---- shared memory carve-up
     T* colc = reinterpret_cast<T*>(sm);
     size_t off = cache_cols ? (size_t)cpb * d * sizeof(T) : 0;
@@ -534,141 +308,323 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
     off += sizeof(double) * c;
     double* wb = reinterpret_cast<double*>(sm + off);
     off += sizeof(double) * c;
+    double* ccs = reinterpret_cast<double*>(sm + off);
+    off += sizeof(double) * c;
     double* red = reinterpret_cast<double*>(sm + off);
-    off += sizeof(double) * 32 * (2 * MAXQ);
+    off += sizeof(double) * HART_RED;
+    T* stc = reinterpret_cast<T*>(sm + off);  // [HART_NST][R][B] block-column row chunks
+    off += HART_NST * sizeof(double) * (size_t)R * B;
+    double* sce = reinterpret_cast<double*>(sm + off);  // [HART_NST][R][c] stale-centroid row chunks
+    off += HART_NST * sizeof(double) * (size_t)R * c;
+    int* stale = reinterpret_cast<int*>(sm + off);
+    off += sizeof(int) * c;
     int* cnt = reinterpret_cast<int*>(sm + off);
     off += sizeof(int) * c;
     int* vs = reinterpret_cast<int*>(sm + off);
+    off += sizeof(int) * c;
+    int* mv = reinterpret_cast<int*>(sm + off);
     __shared__ double s_xx[MAXQ];
     __shared__ int s_lab[MAXQ];
+    __shared__ int s_nstale;
+    __shared__ __align__(8) uint64_t s_bar;  // column fills (bulk copies)
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int jown = b0 + blockIdx.x * cpb;  // first owned column
-    int nown = bend - jown;
-    nown = nown < 0 ? 0 : (nown > cpb ? cpb : nown);
-
-    // ---- load owned columns, interval rows, replicated state
-    if (cache_cols)
-        for (int q = 0; q < nown; ++q)
-            for (int64_t i = tid; i < d; i += blockDim.x)
-                colc[(int64_t)q * d + i] = M[(int64_t)(jown + q) * d + i];
-    // intervals of the owned columns from the block's screen (split-K partials
-    // summed in fixed order; km.cuh bound)
-    for (int e = tid; e < nown * c; e += blockDim.x) {
-        const int q = e / c, k = e - (e / c) * c;
-        const int jl = jown - b0 + q;
-        const double xxj = scr.xx(jl);
-        double lo, hi, mid;
-        scr.get(jl, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
-        As[e] = mid;
-        Es[e] = isfinite(hi - mid) ? hi - mid : INFINITY;
+    const uint32_t col_bytes = (uint32_t)(d * (int64_t)sizeof(T));
+    const bool bulk = cache_cols && (col_bytes % 16 == 0) && ((uintptr_t)M % 16 == 0);
+    uint32_t bar_phase = 0;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
     }
+    // ---- replicated sequential state
     for (int k = tid; k < c; k += blockDim.x) {
-        const int ck = __ldcg(counts + k);
+        const int ck = __ldcg(a.counts + k);
         cnt[k] = ck;
         const double nk = (double)ck;
         wa[k] = nk / (nk - 1.0);  // kmeans.cpp:107
         wb[k] = nk / (nk + 1.0);  // kmeans.cpp:114
-        vs[k] = __ldcg(ver + k);
-    }
-    if (tid < nown) {
-        s_xx[tid] = scr.xx(jown - b0 + tid);
-        s_lab[tid] = __ldcg(labels + jown + tid);
+        vs[k] = 0;
+        mv[k] = 0;
+        ccs[k] = __ldcg(a.cc0 + k);
     }
     __syncthreads();
-    auto colv = [&](int q, int64_t i) -> double {
-        return cache_cols ? (double)colc[(int64_t)q * d + i] : (double)__ldg(M + (int64_t)(jown + q) * d + i);
+    auto colv = [&](int jo, int q, int64_t i) -> double {
+        return cache_cols ? (double)colc[(int64_t)q * d + i] : (double)__ldg(M + (int64_t)(jo + q) * d + i);
     };
 
-    int cursor = b0;
+    int pass = 0, improved = 0;
+    int b0 = -1, bend = 0, cursor = 0, jown = 0, nown = 0;
     int pf = -1, pt = -1, pm = -1, pnf = 0, pnt = 0;
-    const int64_t slice = (d + gridDim.x - 1) / gridDim.x;
-    const int64_t s0 = (int64_t)blockIdx.x * slice;
+    int mvcount = 0;  // move counter (thread 0 stamps the replicated versions)
+    // this CTA's row slice: it alone stores those rows of every updated centroid
+    const int64_t slice = (d + G - 1) / G;
+    const int64_t s0 = (int64_t)blockIdx.x * slice < d ? (int64_t)blockIdx.x * slice : d;
     const int64_t s1 = s0 + slice < d ? s0 + slice : d;
-    unsigned long long rounds = 0;
-
+    unsigned long long rounds = 0, blocks = 0, refreshed = 0, t_load = 0, t_cols = 0;
+    unsigned long long stale_sum = 0, heavy = 0;
+    unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tmark = gtimer();
+    auto lap = [&](int slot) {
+        if (tid == 0) {
+            const unsigned long long t = gtimer();
+            tm[slot] += t - tmark;
+            tmark = t;
+        }
+    };
     const unsigned long long tk0 = gtimer();
-    unsigned long long tph1 = 0, tph2 = 0;
-    unsigned long long ts[6] = {0, 0, 0, 0, 0, 0};
-    unsigned long long act_rounds = 0;
+
     for (int r = 0;; ++r) {
-        const unsigned long long tr0 = gtimer();
-        // ---- phase 1a: the pending move's centroid update (kmeans.cpp:126-131),
-        //      each CTA computing ONE row slice (exact division), plus that
-        //      slice's partial ‖c'‖² sums
+        lap(7);
+        // ---- phase 1: the pending move (kmeans.cpp:126-131).  Every CTA runs
+        //      the update over all rows: its own row slice with the reference's
+        //      exact formula (stored to the other slot), every row with a
+        //      reciprocal multiply for ‖c′‖² and the dots of its owned columns
+        //      still to visit (within the bound, kappa_d).  No grid barrier: a
+        //      slot's slices are read by other CTAs only after the next one.
         if (pf >= 0) {
-            const double* of = Cs + ((int64_t)vs[pf] * c + pf) * d;
-            const double* ot = Cs + ((int64_t)vs[pt] * c + pt) * d;
-            double* nfp = Cs + ((int64_t)(1 - vs[pf]) * c + pf) * d;
-            double* ntp = Cs + ((int64_t)(1 - vs[pt]) * c + pt) * d;
+            const double* of = a.Cs + ((int64_t)vs[pf] * c + pf) * d;
+            const double* ot = a.Cs + ((int64_t)vs[pt] * c + pt) * d;
+            double* nfp = a.Cs + ((int64_t)(1 - vs[pf]) * c + pf) * d;
+            double* ntp = a.Cs + ((int64_t)(1 - vs[pt]) * c + pt) * d;
             const T* xm = M + (int64_t)pm * d;
             const double dcf = (double)pnf, dct = (double)pnt;
             const double na1 = (double)(pnf - 1), nb1 = (double)(pnt + 1);
-            double v2[2] = {0.0, 0.0};
-            for (int64_t i = s0 + tid; i < s1; i += blockDim.x) {
-                const double x = (double)__ldg(xm + i);
-                const double cf = (__ldcg(of + i) * dcf - x) / na1;
-                const double ct = (__ldcg(ot + i) * dct + x) / nb1;
-                __stcg(nfp + i, cf);
-                __stcg(ntp + i, ct);
-                v2[0] = __fma_rn(cf, cf, v2[0]);
-                v2[1] = __fma_rn(ct, ct, v2[1]);
-            }
-            block_sum<2>(v2, red);
-            if (tid == 0) {
-                __stcg(ccpart + 2 * blockIdx.x, v2[0]);
-                __stcg(ccpart + 2 * blockIdx.x + 1, v2[1]);
-            }
-            const unsigned long long ta = gtimer();
-            ts[0] += ta - tr0;
-            grid_barrier(hg);
-            const unsigned long long tb = gtimer();
-            ts[1] += tb - ta;
-            // ---- phase 1b: refresh the (column, from/to) intervals of the owned
-            //      columns still to be decided, reading the new slots (L2)
+            const double rf = 1.0 / na1, rt = 1.0 / nb1;
             int nact = 0;
             for (int q = 0; q < nown; ++q) nact += (jown + q >= cursor);
-            if (nact && !(dbg & 1)) {
-                act_rounds++;
-                // slice partials of ‖c'‖²: one load per thread, fixed-order tree
-                double cc2[2] = {0.0, 0.0};
-                for (unsigned b = tid; b < gridDim.x; b += blockDim.x) {
-                    cc2[0] += __ldcg(ccpart + 2 * b);
-                    cc2[1] += __ldcg(ccpart + 2 * b + 1);
+            const int q0 = nown - nact;  // active owned columns: the suffix q0..nown-1
+            double acc[2 + 2 * MAXQ];
+#pragma unroll
+            for (int e = 0; e < 2 + 2 * MAXQ; ++e) acc[e] = 0.0;
+            auto row = [&](int64_t i, double x, double ofv, double otv) {
+                const double uf = ofv * dcf - x;  // kmeans.cpp:128-129 operation order
+                const double ut = otv * dct + x;
+                if (i >= s0 && i < s1) {
+                    __stcg(nfp + i, uf / na1);
+                    __stcg(ntp + i, ut / nb1);
                 }
-                block_sum<2>(cc2, red);
-                const double ccf = cc2[0], cct = cc2[1];
-                double v[2 * MAXQ];
+                const double cf = uf * rf, ct = ut * rt;
+                acc[0] = __fma_rn(cf, cf, acc[0]);
+                acc[1] = __fma_rn(ct, ct, acc[1]);
 #pragma unroll
-                for (int q = 0; q < 2 * MAXQ; ++q) v[q] = 0.0;
-                // active owned columns are the suffix q0..nown-1 of the owned range
-                const int q0 = nown - nact;
-                hart_dots<T, MAXQ>(v, nfp, ntp, colc, M, jown, q0, nact, d, cache_cols);
-                block_sum<2 * MAXQ>(v, red);
-                if (tid < 2 * nown) {
-                    const int q = tid >> 1, which = tid & 1;
-                    if (jown + q >= cursor) {
-                        const int idx = 2 * (q - q0) + which;  // hart_dots packs actives first
-                        double dot = 0.0;
+                for (int q = 0; q < MAXQ; ++q)
+                    if (q < nact) {
+                        const double xq = colv(jown, q0 + q, i);
+                        acc[2 + 2 * q] = __fma_rn(xq, cf, acc[2 + 2 * q]);
+                        acc[3 + 2 * q] = __fma_rn(xq, ct, acc[3 + 2 * q]);
+                    }
+            };
+            const int64_t step = blockDim.x;
+            if (sizeof(T) == 8 && (d & 1) == 0) {
+                // 16-byte loads, 4 in flight per array per thread
+                const double2* x2 = reinterpret_cast<const double2*>(xm);
+                const double2* f2 = reinterpret_cast<const double2*>(of);
+                const double2* t2 = reinterpret_cast<const double2*>(ot);
+                const int64_t dh = d >> 1;
+                int64_t i = tid;
+                for (; i + 3 * step < dh; i += 4 * step) {
+                    double2 xv[4], fv[4], tv[4];
 #pragma unroll
-                        for (int rr = 0; rr < 2 * MAXQ; ++rr)
-                            if (rr == idx) dot = v[rr];
-                        const double cck = which ? cct : ccf;
-                        const double xxj = s_xx[q];
-                        const double mid = (xxj + cck) - 2.0 * dot;
-                        const double e = screen_err(kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
-                        const int k = which ? pt : pf;
-                        As[q * c + k] = mid;
-                        Es[q * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+                    for (int u = 0; u < 4; ++u) {
+                        xv[u] = __ldg(x2 + i + u * step);
+                        fv[u] = __ldcg(f2 + i + u * step);
+                        tv[u] = __ldcg(t2 + i + u * step);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        row(2 * (i + u * step), xv[u].x, fv[u].x, tv[u].x);
+                        row(2 * (i + u * step) + 1, xv[u].y, fv[u].y, tv[u].y);
+                    }
+                }
+                for (; i < dh; i += step) {
+                    const double2 xv = __ldg(x2 + i), fv = __ldcg(f2 + i), tv = __ldcg(t2 + i);
+                    row(2 * i, xv.x, fv.x, tv.x);
+                    row(2 * i + 1, xv.y, fv.y, tv.y);
+                }
+            } else {
+                int64_t i = tid;
+                for (; i + 3 * step < d; i += 4 * step) {
+                    double xv[4], fv[4], tv[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        xv[u] = (double)__ldg(xm + i + u * step);
+                        fv[u] = __ldcg(of + i + u * step);
+                        tv[u] = __ldcg(ot + i + u * step);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) row(i + u * step, xv[u], fv[u], tv[u]);
+                }
+                for (; i < d; i += step) row(i, (double)__ldg(xm + i), __ldcg(of + i), __ldcg(ot + i));
+            }
+            block_sum<2 + 2 * MAXQ>(acc, red);
+            if (tid < 2 * nact) {
+                const int qa = tid >> 1, which = tid & 1, q = q0 + qa;
+                double dot = 0.0;
+#pragma unroll
+                for (int e = 0; e < 2 * MAXQ; ++e)
+                    if (e == tid) dot = acc[2 + e];
+                const double cck = which ? acc[1] : acc[0];
+                const double xxj = s_xx[q];
+                const double mid = (xxj + cck) - 2.0 * dot;
+                const double e = screen_err(a.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
+                const int k = which ? pt : pf;
+                As[q * c + k] = mid;
+                Es[q * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+            }
+            if (tid == 0) {
+                ccs[pf] = acc[0];
+                ccs[pt] = acc[1];
+                vs[pf] ^= 1;  // this CTA's slices of the new values are stored
+                vs[pt] ^= 1;
+            }
+            __syncthreads();
+            pf = -1;
+        }
+        lap(0);
+
+        if (cursor >= bend) {
+            // ---- leave the block: its interval rows go back to HBM
+            for (int e = tid; e < nown * c; e += blockDim.x) {
+                const int64_t idx = (int64_t)jown * c + e;
+                __stcg(a.A + idx, As[e]);
+                __stcg(a.E + idx, Es[e]);
+            }
+            int nb0 = b0 < 0 ? 0 : bend;
+            if (nb0 >= n) {  // end of a pass (kmeans.cpp:137)
+                ++pass;
+                if (!improved || pass >= a.max_pass) break;
+                improved = 0;
+                nb0 = 0;
+            }
+            const unsigned long long tl0 = gtimer();
+            b0 = nb0;
+            bend = b0 + B < n ? b0 + B : n;
+            const int nb = bend - b0, blk = b0 / B;
+            cursor = b0;
+            jown = b0 + blockIdx.x * cpb;
+            nown = bend - jown;
+            nown = nown < 0 ? 0 : (nown > cpb ? cpb : nown);
+            ++blocks;
+            __syncthreads();
+            // ---- enter the block: owned columns (bulk copies when aligned),
+            //      interval rows, labels; the next block's columns go to L2
+            if (bulk) {
+                if (tid == 0 && nown > 0) {
+                    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                    mbar_expect_tx(&s_bar, col_bytes * (uint32_t)nown);
+                    for (int q = 0; q < nown; ++q) {
+                        const unsigned char* src = reinterpret_cast<const unsigned char*>(M + (int64_t)(jown + q) * d);
+                        unsigned char* dst = reinterpret_cast<unsigned char*>(colc + (int64_t)q * d);
+                        for (uint32_t o = 0; o < col_bytes; o += 65536u) {
+                            const uint32_t len = col_bytes - o < 65536u ? col_bytes - o : 65536u;
+                            bulk_g2s(dst + o, src + o, len, &s_bar);
+                        }
+                    }
+                }
+                if (tid == 32) {
+                    const int nj = (bend < n ? bend : 0) + blockIdx.x * cpb;
+                    for (int q = 0; q < cpb && nj + q < n; ++q) {
+                        const unsigned char* src = reinterpret_cast<const unsigned char*>(M + (int64_t)(nj + q) * d);
+                        for (uint32_t o = 0; o < col_bytes; o += 65536u)
+                            bulk_prefetch_l2(src + o, col_bytes - o < 65536u ? col_bytes - o : 65536u);
+                    }
+                }
+            } else if (cache_cols) {
+                for (int q = 0; q < nown; ++q)
+                    for (int64_t i = tid; i < d; i += blockDim.x)
+                        colc[(int64_t)q * d + i] = __ldg(M + (int64_t)(jown + q) * d + i);
+            }
+            for (int e = tid; e < nown * c; e += blockDim.x) {
+                const int64_t idx = (int64_t)jown * c + e;
+                As[e] = __ldcg(a.A + idx);
+                Es[e] = __ldcg(a.E + idx);
+            }
+            if (tid < nown) {
+                s_xx[tid] = __ldcg(a.xx + jown + tid);
+                s_lab[tid] = __ldcg(a.labels + jown + tid);
+            }
+            // centroids moved since this block's last entry (every column's
+            // entries are valid as of then), ascending
+            const int eb = __ldcg(a.ebuf + blk);
+            if (warp == 0) {
+                int cv = 0;
+                for (int k0 = 0; k0 < c; k0 += 32) {
+                    const int k = k0 + lane;
+                    const bool sk = k < c && mv[k] > eb;
+                    const unsigned bal = __ballot_sync(0xffffffffu, sk);
+                    if (sk) stale[cv + __popc(bal & ((1u << lane) - 1u))] = k;
+                    cv += __popc(bal);
+                }
+                if (lane == 0) s_nstale = cv;
+            }
+            __syncthreads();
+            const int nstale = s_nstale;
+            if (tid == 0) {
+                stale_sum += nstale;
+                heavy += nstale > 8;
+            }
+            if (nstale > 0) {
+                // ---- block refresh, split over rows: this CTA's row slice of
+                //      (every block column) · (every stale centroid) → HBM
+                //      partials; then each owned column sums its G partials
+                const int nb2 = (nb + 1) >> 1, nb4 = (nb + 3) >> 2;
+                const int ns2 = (nstale + 1) >> 1;
+                const int nt = (int)blockDim.x;
+                if (nb2 * ns2 <= nt)
+                    hart_entry_tiles<T, 2, 2>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
+                else if (nb4 * ns2 <= nt)
+                    hart_entry_tiles<T, 4, 2>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
+                else  // 4×4 tiles, several tile rounds when the block is large
+                    hart_entry_tiles<T, 4, 4>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
+                lap(1);
+                grid_barrier(hg);
+                lap(2);
+                // ---- owned columns: the G slice partials (contiguous) in fixed
+                //      order; two pairs per warp in flight
+                const int npairs = nown * nstale;
+                for (int p0 = warp; p0 < npairs; p0 += 2 * nwarps) {
+                    double v[2][HART_MAXG / 32];
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const int p = p0 + m * nwarps;
+                        const int q = p / nstale, t = p - (p / nstale) * nstale;
+                        const double* base = a.part + ((size_t)(jown - b0 + q) * c + t) * G;
+#pragma unroll
+                        for (int u = 0; u < HART_MAXG / 32; ++u) {
+                            const int g = lane + 32 * u;
+                            v[m][u] = (p < npairs && g < G) ? __ldcg(base + g) : 0.0;
+                        }
+                    }
+#pragma unroll
+                    for (int m = 0; m < 2; ++m) {
+                        const int p = p0 + m * nwarps;
+                        double sdot = 0.0;
+#pragma unroll
+                        for (int u = 0; u < HART_MAXG / 32; ++u) sdot += v[m][u];
+                        sdot = warp_sum(sdot);
+                        if (lane == 0 && p < npairs) {
+                            const int q = p / nstale, t = p - (p / nstale) * nstale;
+                            const int k = stale[t];
+                            const double cck = ccs[k], xxj = s_xx[q];
+                            const double mid = (xxj + cck) - 2.0 * sdot;
+                            const double e = screen_err(a.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
+                            As[q * c + k] = mid;
+                            Es[q * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+                            ++refreshed;
+                        }
                     }
                 }
             }
+            lap(3);
+            if (blockIdx.x == 0 && tid == 0) __stcg(a.ebuf + blk, mvcount);
+            if (bulk && nown > 0) {
+                if (!mbar_wait(&s_bar, bar_phase)) __trap();
+                bar_phase ^= 1;
+            }
             __syncthreads();
+            if (tid == 0) t_load += gtimer() - tl0;
         }
-        const unsigned long long tr1 = gtimer();
-        tph1 += tr1 - tr0;
-        if (pf >= 0) ts[2] += tr1 - (tr0 + 0);
-        // ---- phase 2: decide owned columns (warp per column)
+
+        // ---- phase 2: decide owned columns (warp per column), elect the first
         if (warp < nown) {
             const int j = jown + warp;
             if (j >= cursor) {
@@ -687,23 +643,13 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
         // slot (r+1)%3 is next written after this barrier and last read before
         // barrier r-1 completed, so resetting it here cannot race
         if (blockIdx.x == 0 && tid == 0) hg->first[(r + 1) % 3][0] = ~0ULL;
-        const unsigned long long td = gtimer();
-        tph2 += td - tr1;
-        ts[3] += td - tr1;
+        lap(4);
         grid_barrier(hg);
-        const unsigned long long te = gtimer();
-        ts[4] += te - td;
-        // ---- settle (identically in every CTA)
+        lap(5);
+
+        // ---- phase 3: settle (identically in every CTA)
         ++rounds;
         const unsigned long long f = __ldcg(&hg->first[r % 3][0]);
-        if (pf >= 0) {
-            if (tid == 0) {
-                vs[pf] ^= 1;
-                vs[pt] ^= 1;
-            }
-            pf = -1;
-        }
-        __syncthreads();
         if (f == ~0ULL) {
             cursor = bend;
         } else {
@@ -718,19 +664,19 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
                 if ((int)blockIdx.x == owner) {
                     const int q = j - jown;
                     for (int k = tid; k < c; k += blockDim.x) {
-                        const double* cv = Cs + ((int64_t)vs[k] * c + k) * d;
+                        const double* cv = a.Cs + ((int64_t)vs[k] * c + k) * d;
                         double s = 0.0;
                         for (int64_t i = 0; i < d; ++i) {
-                            const double t = colv(q, i) - __ldcg(cv + i);
+                            const double t = colv(jown, q, i) - __ldcg(cv + i);
                             s += t * t;
                         }
-                        scratch[k] = s;
+                        a.scratch[k] = s;
                     }
                     __syncthreads();
                     if (warp == 0) {
                         int t2 = -1;
                         auto iv = [&](int k, double& lo, double& hi, double& mid) {
-                            mid = __ldcg(scratch + k);
+                            mid = __ldcg(a.scratch + k);
                             lo = hi = mid;
                         };
                         const int s2 = hart_decide_warp_w(from, c, cnt, wa, wb, iv, t2);
@@ -751,18 +697,19 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
                 if (tid == 0) {
                     cnt[from] = nf - 1;
                     cnt[to] = nt + 1;
-                    const double a = (double)(nf - 1), b = (double)(nt + 1);
-                    wa[from] = a / (a - 1.0);
-                    wb[from] = a / (a + 1.0);
-                    wa[to] = b / (b - 1.0);
-                    wb[to] = b / (b + 1.0);
+                    const double fa = (double)(nf - 1), fb = (double)(nt + 1);
+                    wa[from] = fa / (fa - 1.0);
+                    wb[from] = fa / (fa + 1.0);
+                    wa[to] = fb / (fb - 1.0);
+                    wb[to] = fb / (fb + 1.0);
+                    mv[from] = mv[to] = ++mvcount;
                     if (j >= jown && j < jown + nown) s_lab[j - jown] = to;
                 }
                 if (blockIdx.x == 0 && tid == 0) {
-                    labels[j] = to;
+                    __stcg(a.labels + j, to);
                     hg->moves += 1;
-                    hg->improved = 1;
                 }
+                improved = 1;
                 pf = from;
                 pt = to;
                 pm = j;
@@ -772,33 +719,28 @@ __global__ void __launch_bounds__(512, 1) k_hart_block(
             cursor = j + 1;
         }
         __syncthreads();
-        ts[5] += gtimer() - te;
-        if (cursor >= bend && pf < 0) break;
-        if (cursor >= bend) cursor = bend;  // one more round applies the pending update
     }
-    if (tid == 0) {
-        atomicMax(&hg->t_phase1_max, tph1);
-        for (int q = 0; q < 6; ++q) atomicAdd(&hg->tmax[q], ts[q]);  // summed over CTAs
-    }
-    // every CTA is past its last read of the election slots: reset them for
-    // the next block launch
-    grid_barrier(hg);
-    if (blockIdx.x == 0 && tid == 0)
-        hg->first[0][0] = hg->first[1][0] = hg->first[2][0] = ~0ULL;
-    // publish the replicated state
+
+    // ---- publish (CTA 0): final counts and slot map.  The last move's slices
+    //      were stored in this round; the kernel boundary publishes them.
     if (blockIdx.x == 0) {
         for (int k = tid; k < c; k += blockDim.x) {
-            counts[k] = cnt[k];
-            ver[k] = vs[k];
+            a.counts[k] = cnt[k];
+            a.ver[k] = vs[k];
         }
         if (tid == 0) {
-            hg->cursor = cursor;
-            hg->rounds += rounds;
-            hg->t_kernel += gtimer() - tk0;
-            hg->t_phase1 += tph1;
-            hg->t_phase2 += tph2;
+            hg->rounds = rounds;
+            hg->passes = (unsigned long long)pass;
+            hg->blocks = blocks;
+            hg->t_kernel = gtimer() - tk0;
+            hg->t_load = t_load;
+            hg->t_cols = t_cols;
+            hg->stale_sum = stale_sum;
+            hg->heavy_blocks = heavy;
+            for (int q = 0; q < 8; ++q) hg->tm[q] = tm[q];
         }
     }
+    if (lane == 0 && refreshed) atomicAdd(&hg->refreshed, refreshed);
 }
 
 }  // namespace respca_dev

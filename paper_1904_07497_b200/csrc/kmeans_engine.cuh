@@ -7,9 +7,15 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <condition_variable>
 #include <cstring>
+#include <exception>
+#include <functional>
 #include <limits>
+#include <memory>
+#include <mutex>
 #include <random>
+#include <thread>
 #include <vector>
 
 #include "alm.cuh"
@@ -76,7 +82,6 @@ struct KMeansEngine {
     DBuf<double> part, xxp, cc, nextC, exact, own, msp, approx, err, d2, xx, scratch;
     DBuf<int> newlab, amb, counts, goff, members, modver, stamp, gidx, errflag;
     DBuf<Ctl> kctl;
-    DBuf<HartState> hs;
     HBuf hst;
     Groups groups;
     std::vector<int> h_labels;
@@ -322,6 +327,7 @@ struct KMeansEngine {
             CK(cudaStreamSynchronize(st));
             stats->t_lloyd += since(t_lloyd0);
         }
+        if (before_hartigan) before_hartigan();
         const auto t_h0 = HClock::now();
         hartigan(C, labels);
         if (stats) stats->t_hart += since(t_h0);
@@ -334,13 +340,67 @@ struct KMeansEngine {
     }
 
     // hartigan_refine (kmeans.cpp:96-139), exact sequential semantics
-    // (hartigan.cuh): one persistent cooperative launch per block of columns
-    // (owned columns cached in shared memory, one grid barrier per round); the
-    // host synchronises once per pass.
-    DBuf<double> hA, hE, hxx, hC2;
-    DBuf<int> hver;
+    // (hartigan.cuh): ONE persistent cooperative launch for every pass; the
+    // start intervals come from one full screen, later ones from the kernel's
+    // lazy per-entry refresh.
+    DBuf<double> hA, hE, hxx, hC2, hpart;
+    DBuf<int> hver, hebuf;
     DBuf<HartGlobal> hglob;
-    DBuf<double> hccpart;
+    int hart_ctas = 0;  // CTAs of the Hartigan kernel (0: one per SM)
+    std::function<void()> before_hartigan;  // restart lanes: wait for the others' seeding/Lloyd
+
+    struct HartGeom {
+        int G = 1, cpb = 1, B = 1, R = 1;
+        bool cache = true;
+        size_t smem = 0;
+    };
+    // shared memory of the Hartigan kernel (hartigan.cuh carve-up)
+    size_t hart_smem(int cpb, bool cache, int B, int R) const {
+        return (cache ? (size_t)cpb * d * sizeof(T) + 16 : 0) + sizeof(double) * 2 * (size_t)cpb * c +
+               sizeof(double) * (3 * (size_t)c + HART_RED) + HART_NST * sizeof(double) * (size_t)R * (B + c) +
+               sizeof(int) * 4 * (size_t)c + 2048;
+    }
+    HartGeom hart_geometry() const {
+        int dev = 0, nsm = 148, optin = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+        optin -= 4096;  // the kernel's static shared memory + headroom
+        const int avail = std::min(HART_MAXG, hart_ctas > 0 ? std::min(hart_ctas, nsm) : nsm);
+        for (int pass = 0; pass < 2; ++pass) {
+            const bool cache = pass == 0;  // owned columns cached in shared memory, else streamed
+            for (int cpb = cache ? 8 : 4; cpb >= 1; --cpb) {
+                HartGeom g;
+                g.cache = cache;
+                g.cpb = cpb;
+                g.G = std::max(1, std::min(avail, ceil_div(n, cpb)));
+                g.B = g.G * cpb;
+                const size_t base = hart_smem(cpb, cache, g.B, 0);
+                if (base >= (size_t)optin) continue;
+                const size_t per_row = HART_NST * sizeof(double) * (size_t)(g.B + c);  // cp.async stages
+                const int64_t R = (int64_t)(((size_t)optin - base) / per_row);
+                if (R < 4 && !(R >= 1 && d <= R)) continue;
+                g.R = (int)std::min<int64_t>(R, 32);
+                g.smem = hart_smem(cpb, cache, g.B, g.R);
+                return g;
+            }
+        }
+        throw InvalidArg("hartigan: c too large for the device's shared memory");
+    }
+    void hart_reserve() {
+        const HartGeom g = hart_geometry();
+        const size_t nc = (size_t)n * c;
+        hA.ensure(nc);
+        hE.ensure(nc);
+        hxx.ensure(n);
+        hC2.ensure((size_t)2 * d * c);
+        hver.ensure(c);
+        hebuf.ensure(ceil_div(n, g.B));
+        hpart.ensure((size_t)g.G * g.B * c);
+        hglob.ensure(1);
+        scratch.ensure(std::max(c, 64));
+        hst.ensure<HartGlobal>(1);
+    }
 
     void hartigan(double* C, int* labels) {
         if (c <= 1) return;  // no candidate target: never moves
@@ -348,108 +408,77 @@ struct KMeansEngine {
         groups.build(h_labels.data(), n, c);
         CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
                            cudaMemcpyHostToDevice, st));
-        const size_t nc = (size_t)n * c;
-        hA.ensure(nc);
-        hE.ensure(nc);
-        hxx.ensure(n);
-        hC2.ensure((size_t)2 * d * c);
-        hver.ensure(c);
-        hglob.ensure(1);
-        hccpart.ensure(2 * 1024);
-        scratch.ensure(std::max(c, 64));
+        hart_reserve();
+        const HartGeom hgm = hart_geometry();
         CK(cudaMemcpyAsync(hC2.p, C, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemsetAsync(hver.p, 0, sizeof(int) * c, st));
+        CK(cudaMemsetAsync(hebuf.p, 0, sizeof(int) * ceil_div(n, hgm.B), st));
         CK(cudaMemsetAsync(hglob.p, 0, sizeof(HartGlobal), st));
-        HartArrays h{};
-        h.A = hA.p;
-        h.E = hE.p;
-        h.xx = hxx.p;
-        h.labels = labels;
-        h.counts = counts.p;
-        h.C = hC2.p;
-        h.ver = hver.p;
-        h.scratch = scratch.p;
-        h.kappa_d = kappa_screen();
-        // geometry: one CTA per SM, owned columns cached in shared memory when they fit
-        int dev = 0, nsm = 148, smem_optin = 0;
-        CK(cudaGetDevice(&dev));
-        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        CK(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-        const size_t fixed = sizeof(double) * (2 * c + 32 * 16) + sizeof(int) * 2 * c + 1024;
-        auto need = [&](int cpb, bool cache) {
-            return (cache ? (size_t)cpb * d * sizeof(T) + 16 : 0) +
-                   sizeof(double) * 2 * (size_t)cpb * c + fixed;
-        };
-        int cpb = 8;
-        bool cache = true;
-        while (cpb > 1 && need(cpb, true) > (size_t)smem_optin) --cpb;
-        if (need(cpb, true) > (size_t)smem_optin) {  // a column does not fit: stream it
-            cache = false;
-            cpb = 4;
-            while (cpb > 1 && need(cpb, false) > (size_t)smem_optin) --cpb;
-        }
-        const int G = std::max(1, std::min(nsm, ceil_div(n, cpb)));
-        const int B = G * cpb;
-        const size_t smem = need(cpb, cache);
-        auto kf = cpb <= 2 ? k_hart_block<T, 2> : (cpb <= 4 ? k_hart_block<T, 4> : k_hart_block<T, 8>);
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        HartGlobal* hh = hst.ensure<HartGlobal>(1);
-        const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
-        int pass = 0;
         k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
-        ln.add();
-        for (; pass < 50; ++pass) {
-            for (int b0 = 0; b0 < n; b0 += B) {
-                const int nb = std::min(B, n - b0);
-                // screen the block against the CURRENT centroid slots
-                screen_cols(M + (int64_t)b0 * d, nb, hC2.p, hver.p);
-                const int gb = std::min(G, ceil_div(nb, cpb));
-                const T* Mp = M;
-                HartGlobal* hgp = hglob.p;
-                int* lp = labels;
-                int* cp_ = counts.p;
-                double* csp = hC2.p;
-                int* vp = hver.p;
-                Screen scr = screen_view();
-                double* sp = scratch.p;
-                double* ccp = hccpart.p;
-                int64_t dd = d;
-                int cc_ = c, b0_ = b0, be = b0 + nb, cpb_ = cpb, cache_ = cache ? 1 : 0;
-                double kd = h.kappa_d;
-                static const int dbgv = [] {
-                    const char* e = std::getenv("RESPCA_HART_DBG");
-                    return e ? std::atoi(e) : 0;
-                }();
-                int dbg = dbgv;
-                void* args[] = {&Mp, &hgp, &lp, &cp_, &csp, &vp, &scr, &sp, &ccp,
-                                &dd, &cc_, &b0_, &be, &cpb_, &cache_, &kd, &dbg};
-                CK(cudaLaunchCooperativeKernel((const void*)kf, dim3(gb), dim3(512), args, smem, st));
-                ln.add(1);
-            }
+        // start intervals: one screen of every column against the start centroids
+        screen_cols(M, n, hC2.p, nullptr);
+        k_hart_fill<<<ceil_div((int64_t)n * c, 256), 256, 0, st>>>(screen_view(), hA.p, hE.p, hxx.p, n, c);
+        ln.add(2);
+        const int G = hgm.G, cpb = hgm.cpb;
+        const bool cache = hgm.cache;
+        const size_t smem = hgm.smem;
+        auto kf = cpb <= 2 ? k_hart_all<T, 2> : (cpb <= 4 ? k_hart_all<T, 4> : k_hart_all<T, 8>);
+        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        HartArgs a{};
+        a.g = hglob.p;
+        a.labels = labels;
+        a.counts = counts.p;
+        a.Cs = hC2.p;
+        a.ver = hver.p;
+        a.A = hA.p;
+        a.E = hE.p;
+        a.ebuf = hebuf.p;
+        a.part = hpart.p;
+        a.stage_rows = hgm.R;
+        a.xx = hxx.p;
+        a.cc0 = cc.p;
+        a.scratch = scratch.p;
+        a.d = d;
+        a.n = n;
+        a.c = c;
+        a.cpb = cpb;
+        a.cache_cols = cache ? 1 : 0;
+        a.max_pass = 50;  // kmeans.cpp:101
+        // + the reciprocal-multiply update used for ‖c′‖² and the dots (≤ 7.5u(‖x‖+‖c‖)²)
+        a.kappa_d = kappa_screen() + 16.0 * kU;
+        const T* Mp = M;
+        void* args[] = {&Mp, &a};
+        CK(cudaLaunchCooperativeKernel((const void*)kf, dim3(G), dim3(512), args, smem, st));
+        ln.add(1);
+        const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
+        k_hart_consolidate<<<cg, 256, 0, st>>>(hC2.p, hver.p, d, c);
+        CK(cudaMemcpyAsync(C, hC2.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        ln.add(1);
+        if (stats) {
+            HartGlobal* hh = hst.ensure<HartGlobal>(1);
             CK(cudaMemcpyAsync(hh, hglob.p, sizeof(HartGlobal), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            if (!hh->improved) break;
-            k_hart_improved_reset<<<1, 1, 0, st>>>(hglob.p);
-        }
-        k_hart_consolidate<<<cg, 256, 0, st>>>(h, d, c);
-        k_hart_ver_reset<<<1, 256, 0, st>>>(h, c);
-        CK(cudaMemcpyAsync(C, hC2.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
-        ln.add(2);
-        if (stats) {
             stats->hartigan_moves += hh->moves;
             stats->exact_fallbacks += hh->exact_fallbacks;
-            stats->hartigan_passes += (uint64_t)std::min(pass + 1, 50);
+            stats->hartigan_passes += hh->passes;
             stats->hartigan_rounds += hh->rounds;
+            stats->hartigan_refreshes += hh->refreshed;
             stats->t_hart_kernel += 1e-9 * (double)hh->t_kernel;
             if (trace_on())
-                std::fprintf(stderr, "[respca] hartigan: %llu rounds, kernels %.3fs (phase1 %.3fs, max-CTA phase1/block %.1fus, decide %.3fs, rest = barrier+settle)\n",
-                             (unsigned long long)hh->rounds, 1e-9 * hh->t_kernel,
-                             1e-9 * hh->t_phase1, 1e-3 * hh->t_phase1_max, 1e-9 * hh->t_phase2);
+                std::fprintf(stderr,
+                             "[respca] hartigan: G=%d cpb=%d R=%d %llu passes %llu blocks %llu rounds %llu moves "
+                             "%llu refreshed, kernel %.3fs (block entries %.3fs; CTA0 stale/entry %.2f, heavy %llu)\n",
+                             G, cpb, hgm.R, (unsigned long long)hh->passes, (unsigned long long)hh->blocks,
+                             (unsigned long long)hh->rounds, (unsigned long long)hh->moves,
+                             (unsigned long long)hh->refreshed, 1e-9 * hh->t_kernel, 1e-9 * hh->t_load,
+                             (double)hh->stale_sum / (double)std::max<uint64_t>(1, hh->blocks),
+                             (unsigned long long)hh->heavy_blocks);
             if (trace_on())
-                std::fprintf(stderr, "[respca] hartigan per-round CTA-mean us: 1a %.2f barA %.2f 1b(+1a+barA) %.2f decide %.2f barB %.2f settle %.2f\n",
-                             1e-3 * hh->tmax[0] / (double)hh->rounds / G, 1e-3 * hh->tmax[1] / (double)hh->rounds / G,
-                             1e-3 * hh->tmax[2] / (double)hh->rounds / G, 1e-3 * hh->tmax[3] / (double)hh->rounds / G,
-                             1e-3 * hh->tmax[4] / (double)hh->rounds / G, 1e-3 * hh->tmax[5] / (double)hh->rounds / G);
+                std::fprintf(stderr,
+                             "[respca] hartigan CTA0 phases (s): update %.3f entry-tiles %.3f entry-barrier %.3f "
+                             "entry-reduce+wait %.3f decide %.3f barrier %.3f settle %.3f\n",
+                             1e-9 * hh->tm[0], 1e-9 * hh->tm[1], 1e-9 * hh->tm[2], 1e-9 * hh->tm[3],
+                             1e-9 * hh->tm[4], 1e-9 * hh->tm[5], 1e-9 * hh->tm[7]);
         }
     }
 
@@ -535,54 +564,256 @@ struct KMeansEngine {
         ln.add();
     }
 
+    // full-screen split of screen_cols(M, n, …) (same formula)
+    void reserve_full_screen() {
+        const int tiles = ceil_div(n, tile_j()) * ceil_div(c, tile_k());
+        const int chunks = ceil_div(d, 32);
+        int ns = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
+        ns = std::min(ns, 64);
+        part.ensure((size_t)ns * n * c);
+        xxp.ensure((size_t)ns * n);
+    }
+
+    // number of restarts run side by side (one lane = engine + stream + host
+    // thread each); RESPCA_KM_LANES overrides (tests)
+    int lanes_for(uint64_t n_restarts) const {
+        if (const char* e = std::getenv("RESPCA_KM_LANES")) {
+            const int v = std::atoi(e);
+            if (v >= 1) return (int)std::min<uint64_t>((uint64_t)v, std::max<uint64_t>(n_restarts, 1));
+        }
+        if (n_restarts < 2 || (double)d * (double)n < 4e6) return 1;  // launch-bound: in order
+        return (int)std::min<uint64_t>(n_restarts, 8);
+    }
+
     // kmeans (kmeans.cpp:237-250).  labels/C device outputs.
     void kmeans(uint64_t max_iters, uint64_t n_restarts, uint64_t seed, double tol, int* labels,
                 double* C, double* inertia_out, uint64_t* iters_out) {
         if (c == 0) throw InvalidArg("kmeans: c must be >= 1");
         if ((int64_t)c > n) throw InvalidArg("kmeans: c exceeds column count");
-        std::mt19937_64 rng(seed);
-        double best = std::numeric_limits<double>::infinity();
-        DBuf<int> lab;
-        DBuf<double> cen;
-        lab.ensure(n);
-        cen.ensure((size_t)d * c);
-        bool have = false;
-        for (uint64_t r = 0; r < n_restarts; ++r) {
-            const auto tp = HClock::now();
-            const std::vector<int> chosen = pp_init(rng);
-            gather(chosen, cen.p);
-            if (stats) stats->t_pp += since(tp);
-            const uint64_t it = lloyd_run(cen.p, lab.p, max_iters, tol);
-            const auto ti = HClock::now();
-            const double in = inertia(cen.p, lab.p);
-            if (stats) stats->t_inertia += since(ti);
-            if (in < best) {
-                best = in;
-                have = true;
-                CK(cudaMemcpyAsync(labels, lab.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
-                CK(cudaMemcpyAsync(C, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
-                if (inertia_out) *inertia_out = in;
-                if (iters_out) *iters_out = it;
+        const int L = lanes_for(n_restarts);
+        if (L > 1) {
+            kmeans_lanes(L, max_iters, n_restarts, seed, tol, labels, C, inertia_out, iters_out);
+        } else {
+            std::mt19937_64 rng(seed);
+            double best = std::numeric_limits<double>::infinity();
+            DBuf<int> lab;
+            DBuf<double> cen;
+            lab.ensure(n);
+            cen.ensure((size_t)d * c);
+            bool have = false;
+            for (uint64_t r = 0; r < n_restarts; ++r) {
+                const auto tp = HClock::now();
+                const std::vector<int> chosen = pp_init(rng);
+                gather(chosen, cen.p);
+                if (stats) stats->t_pp += since(tp);
+                const uint64_t it = lloyd_run(cen.p, lab.p, max_iters, tol);
+                const auto ti = HClock::now();
+                const double in = inertia(cen.p, lab.p);
+                if (stats) stats->t_inertia += since(ti);
+                if (in < best) {  // kmeans.cpp:246
+                    best = in;
+                    have = true;
+                    CK(cudaMemcpyAsync(labels, lab.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+                    CK(cudaMemcpyAsync(C, cen.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+                    if (inertia_out) *inertia_out = in;
+                    if (iters_out) *iters_out = it;
+                }
+            }
+            CK(cudaStreamSynchronize(st));
+            if (!have && n_restarts > 0) {
+                // every restart had a NaN inertia: the reference returns the
+                // default-constructed result; mirror that as an error
+                throw RuntimeErr("kmeans: no restart produced a finite inertia");
             }
         }
-        CK(cudaStreamSynchronize(st));
         if (stats && trace_on())
             std::fprintf(stderr,
-                         "[respca] kmeans(X): pp %.3fs lloyd %.3fs (%llu steps) hartigan %.3fs "
+                         "[respca] kmeans(X): %d lane(s); pp %.3fs lloyd %.3fs (%llu steps) hartigan %.3fs "
                          "(%llu rounds, %llu moves, %llu passes, %llu refreshes, round kernels %.3fs) inertia %.3fs "
                          "fallbacks %llu\n",
-                         stats->t_pp, stats->t_lloyd, (unsigned long long)stats->lloyd_steps,
+                         L, stats->t_pp, stats->t_lloyd, (unsigned long long)stats->lloyd_steps,
                          stats->t_hart, (unsigned long long)stats->hartigan_rounds,
                          (unsigned long long)stats->hartigan_moves,
                          (unsigned long long)stats->hartigan_passes,
                          (unsigned long long)stats->hartigan_refreshes, stats->t_hart_kernel,
                          stats->t_inertia,
                          (unsigned long long)stats->exact_fallbacks);
-        if (!have && n_restarts > 0) {
-            // every restart had a NaN inertia: the reference returns the
-            // default-constructed result; mirror that as an error
-            throw RuntimeErr("kmeans: no restart produced a finite inertia");
+    }
+
+    // The restarts of kmeans() side by side.  Restart r's k-means++ draws
+    // must follow restart r−1's (one libstdc++ engine, kmeans.cpp:240), so the
+    // seeding steps take turns; Lloyd, Hartigan and inertia of different
+    // restarts then overlap on their own streams, each Hartigan kernel on
+    // 1/L of the SMs (so every lane's cooperative grid can be resident at
+    // once).  The winner is the reference's: the first restart with the
+    // smallest inertia (strict <, kmeans.cpp:246); the first restart that
+    // throws decides the exception.
+    void kmeans_lanes(int L, uint64_t max_iters, uint64_t n_restarts, uint64_t seed, double tol,
+                      int* labels, double* C, double* inertia_out, uint64_t* iters_out) {
+        int dev = 0, nsm = 148;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        struct Lane {
+            KMeansEngine<T> e;
+            uint64_t launches = 0;
+            Stats st;
+            DBuf<int> wl, bl;
+            DBuf<double> wc, bc;
+            int best_r = -1;
+            double best_in = std::numeric_limits<double>::infinity();
+            uint64_t best_it = 0;
+            ~Lane() {
+                if (e.st) cudaStreamDestroy(e.st);
+            }
+        };
+        std::vector<std::unique_ptr<Lane>> lanes;
+        cudaEvent_t ready;
+        CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+        CK(cudaEventRecord(ready, st));  // M is complete on the caller's stream
+        for (int l = 0; l < L; ++l) {
+            lanes.emplace_back(new Lane());
+            Lane& ln_ = *lanes.back();
+            CK(cudaStreamCreateWithFlags(&ln_.e.st, cudaStreamNonBlocking));
+            CK(cudaStreamWaitEvent(ln_.e.st, ready, 0));
+            ln_.e.ln = Launch{&ln_.launches};
+            ln_.e.stats = stats ? &ln_.st : nullptr;
+            ln_.e.hart_ctas = std::max(1, nsm / L);
+            ln_.e.bind(M, d, n, c);
+            // every buffer a lane touches is allocated before the lanes run
+            // (cudaFree would synchronise the device under them)
+            ln_.e.reserve_full_screen();
+            ln_.e.hart_reserve();
+            ln_.e.d2.ensure(n);
+            ln_.e.gidx.ensure(c);
+            ln_.wl.ensure(n);
+            ln_.bl.ensure(n);
+            ln_.wc.ensure((size_t)d * c);
+            ln_.bc.ensure((size_t)d * c);
         }
+        CK(cudaEventDestroy(ready));
+        std::mt19937_64 rng(seed);
+        std::mutex mu;
+        std::condition_variable cv;
+        uint64_t turn = 0;                 // restart whose seeding may draw next
+        uint64_t abort_at = UINT64_MAX;    // restarts after a failed one are skipped
+        std::vector<std::exception_ptr> errs(n_restarts);
+        // a persistent Hartigan grid holds its SMs until it ends: no lane
+        // starts one before every lane is past its seeding and Lloyd steps
+        // (they need the whole GPU); lanes that stop early count as arrived
+        std::vector<char> arrived(L, 0);
+        int n_arrived = 0;
+        auto arrive = [&](int l) {  // caller holds mu
+            if (!arrived[l]) {
+                arrived[l] = 1;
+                ++n_arrived;
+                cv.notify_all();
+            }
+        };
+        for (int l = 0; l < L; ++l)
+            lanes[l]->e.before_hartigan = [&, l] {
+                std::unique_lock<std::mutex> lk(mu);
+                arrive(l);
+                cv.wait(lk, [&] { return n_arrived == L; });
+            };
+        auto body = [&](int l) {
+            Lane& ln_ = *lanes[l];
+            KMeansEngine<T>& e = ln_.e;
+            struct Done {  // every exit path counts as arrived
+                std::mutex& m;
+                std::function<void()> f;
+                ~Done() {
+                    std::lock_guard<std::mutex> g(m);
+                    f();
+                }
+            } done{mu, [&, l] { arrive(l); }};
+            try {
+                CK(cudaSetDevice(dev));
+            } catch (...) {
+                std::lock_guard<std::mutex> g(mu);
+                errs[l] = std::current_exception();
+                abort_at = std::min<uint64_t>(abort_at, (uint64_t)l);
+                cv.notify_all();
+                return;
+            }
+            for (uint64_t r = (uint64_t)l; r < n_restarts; r += (uint64_t)L) {
+                bool holds_turn = false;
+                try {
+                    {
+                        std::unique_lock<std::mutex> lk(mu);
+                        cv.wait(lk, [&] { return turn == r || r > abort_at; });
+                        if (r > abort_at) return;
+                    }
+                    holds_turn = true;
+                    const auto tp = HClock::now();
+                    const std::vector<int> chosen = e.pp_init(rng);
+                    {
+                        std::lock_guard<std::mutex> g(mu);
+                        turn = r + 1;
+                    }
+                    cv.notify_all();
+                    holds_turn = false;
+                    e.gather(chosen, ln_.wc.p);
+                    if (e.stats) e.stats->t_pp += since(tp);
+                    const uint64_t it = e.lloyd_run(ln_.wc.p, ln_.wl.p, max_iters, tol);
+                    const auto ti = HClock::now();
+                    const double in = e.inertia(ln_.wc.p, ln_.wl.p);
+                    if (e.stats) e.stats->t_inertia += since(ti);
+                    if (in < ln_.best_in) {
+                        ln_.best_in = in;
+                        ln_.best_r = (int)r;
+                        ln_.best_it = it;
+                        CK(cudaMemcpyAsync(ln_.bl.p, ln_.wl.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, e.st));
+                        CK(cudaMemcpyAsync(ln_.bc.p, ln_.wc.p, sizeof(double) * d * c,
+                                           cudaMemcpyDeviceToDevice, e.st));
+                    }
+                    CK(cudaStreamSynchronize(e.st));
+                } catch (...) {
+                    std::lock_guard<std::mutex> g(mu);
+                    errs[r] = std::current_exception();
+                    abort_at = std::min(abort_at, r);
+                    if (holds_turn) turn = r + 1;
+                    cv.notify_all();
+                    return;
+                }
+            }
+        };
+        std::vector<std::thread> threads;
+        for (int l = 0; l < L; ++l) threads.emplace_back(body, l);
+        for (auto& t : threads) t.join();
+        for (auto& lp : lanes) {
+            *ln.counter += lp->launches;
+            if (stats) {
+                const Stats& s2 = lp->st;
+                stats->hartigan_moves += s2.hartigan_moves;
+                stats->exact_fallbacks += s2.exact_fallbacks;
+                stats->lloyd_steps += s2.lloyd_steps;
+                stats->hartigan_passes += s2.hartigan_passes;
+                stats->hartigan_rounds += s2.hartigan_rounds;
+                stats->hartigan_refreshes += s2.hartigan_refreshes;
+                stats->t_pp += s2.t_pp;
+                stats->t_lloyd += s2.t_lloyd;
+                stats->t_hart += s2.t_hart;
+                stats->t_inertia += s2.t_inertia;
+                stats->t_hart_kernel += s2.t_hart_kernel;
+            }
+        }
+        for (uint64_t r = 0; r < n_restarts; ++r)
+            if (errs[r]) std::rethrow_exception(errs[r]);
+        int bl = -1;
+        for (int l = 0; l < L; ++l) {
+            const Lane& x = *lanes[l];
+            if (x.best_r < 0) continue;
+            if (bl < 0 || x.best_in < lanes[bl]->best_in ||
+                (x.best_in == lanes[bl]->best_in && x.best_r < lanes[bl]->best_r))
+                bl = l;
+        }
+        if (bl < 0) throw RuntimeErr("kmeans: no restart produced a finite inertia");
+        const Lane& w = *lanes[bl];
+        CK(cudaMemcpyAsync(labels, w.bl.p, sizeof(int) * n, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(C, w.bc.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
+        CK(cudaStreamSynchronize(st));
+        if (inertia_out) *inertia_out = w.best_in;
+        if (iters_out) *iters_out = w.best_it;
     }
 };
 

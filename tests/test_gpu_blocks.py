@@ -159,6 +159,25 @@ def test_kmeans_bitwise(ctx, orc, R):
         R.kmeans(rand(rng, 2, 5), KMeansConfig(c=0), ctx=ctx)
 
 
+@pytest.mark.parametrize("lanes", ["2", "3", "5"])
+def test_kmeans_restart_lanes_bitwise(ctx, orc, R, monkeypatch, lanes):
+    """Restarts run side by side (one stream + host thread per lane, seeding
+    in turn): same winner, labels, centroids, inertia as the reference's
+    sequential loop (kmeans.cpp:237-250)."""
+    from paper_1904_07497_b200.respca import KMeansConfig
+
+    monkeypatch.setenv("RESPCA_KM_LANES", lanes)
+    rng = np.random.default_rng(24)
+    for d, n, c, seed, restarts in ((4, 24, 2, 3, 5), (20, 200, 6, 7, 5), (64, 300, 12, 2, 7),
+                                    (2, 10, 2, 9, 4)):
+        m = rand(rng, d, n)
+        a = R.kmeans(m, KMeansConfig(c=c, seed=seed, n_restarts=restarts), ctx=ctx)
+        lab, cen, inertia, it = orc.kmeans(m, c, 100, restarts, seed, 1e-6)
+        assert (a.assignment == lab).all()
+        assert bitwise(a.centroids, cen)
+        assert a.inertia == inertia and a.iters_run == it
+
+
 def test_kmeans_warm_bitwise(ctx, orc, R):
     from paper_1904_07497_b200.respca import KMeansConfig
 

@@ -36,6 +36,16 @@ def test_c1_bitwise(ctx, name):
     assert int(np.count_nonzero(res.S)) == case["ref"]["S_nnz"]
 
 
+@pytest.mark.parametrize("lanes", ["1", "5"])
+def test_c1_bitwise_restart_lanes(ctx, monkeypatch, lanes):
+    """solve()'s kmeans(X) with its 5 restarts forced in order (1 lane) or
+    side by side (5 lanes): identical to the reference either way."""
+    monkeypatch.setenv("RESPCA_KM_LANES", lanes)
+    case = load("solve_C1.json")
+    res = _solve(ctx, make_x(case), cfg_from(case["config"]))
+    assert_matches_golden(res, case)
+
+
 def test_solve_against_oracle_random(ctx, orc):
     """Fresh seeded inputs, no fixture: GPU vs the C restatement, bitwise."""
     from paper_1904_07497_b200 import synth
