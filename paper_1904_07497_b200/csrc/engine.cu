@@ -182,7 +182,16 @@ struct Alm : AlmBase {
 
     // initial grouping: kmeans(X) with >= 5 restarts (solver.cpp:143-150)
     void init_labels() {
+        const auto ti0 = Clock::now();
+        auto tr = [&](const char* what) {
+            if (trace_on()) {
+                CK(cudaStreamSynchronize(st));
+                std::fprintf(stderr, "[respca] init: %s at %.3fs\n", what,
+                             std::chrono::duration<double>(Clock::now() - ti0).count());
+            }
+        };
         km.bind(X.p, d, n, c);
+        tr("bind");
         if (c == 1) {
             CK(cudaMemsetAsync(labels.p, 0, sizeof(int) * n, st));
             km.h_labels.assign(n, 0);
@@ -190,11 +199,13 @@ struct Alm : AlmBase {
             const uint64_t restarts = std::max<uint64_t>(cfg.km_n_restarts, 5);
             km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, nullptr,
                       nullptr);
+            tr("kmeans");
             km.fetch_labels(labels.p);
         }
         km.bind(L.p, d, n, c);  // from here on the p-update clusters L
         km.groups.build(km.h_labels.data(), n, c);
         km.upload_groups();
+        tr("groups");
     }
 
     void launch_group_D() {  // G_t = Σ_{j∈g} ((x − s) + θ/ρ) into G[parity]

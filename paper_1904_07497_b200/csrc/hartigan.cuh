@@ -124,6 +124,8 @@ struct HartGlobal {
     alignas(128) unsigned long long moves, exact_fallbacks, rounds, passes, blocks, refreshed;
     unsigned long long t_kernel, t_load, t_cols;  // globaltimer (CTA 0): whole kernel, block loads, column fills
     unsigned long long stale_sum, heavy_blocks;   // CTA 0: stale centroids over all block entries, entries with > 8
+    unsigned long long tsub1, tsub2;
+    unsigned long long hist[9];  // diagnostics: no-move margins below 1e-1..1e-8, total
     unsigned long long tm[8];  // CTA 0 phase sums: 1, entry tiles, entry barrier, entry reduce, decide, barrier, settle
 };
 
@@ -185,14 +187,12 @@ struct HartArgs {
     const double* cc0;    // [c]   ‖c_k‖² of the start centroids (screen)
     double* scratch;      // [c]   exact distances of one column (near-tie)
     int64_t d;
-    int n, c, cpb, cache_cols, max_pass, stage_rows;
+    int n, c, cpb, cache_cols, max_pass, stage_rows, stages, diag;
     double kappa_d;       // screen bound factor (km.cuh) + the reciprocal-update term
 };
 
 constexpr int HART_RED = 32 * 24;  // block_sum scratch (≤ 24 sums)
 constexpr int HART_MAXG = 160;     // max CTAs of the Hartigan kernel (partials per entry)
-
-constexpr int HART_NST = 4;  // cp.async stages of the block refresh
 
 RESPCA_DEV void cp_wait_dyn(int pending) {
     switch (pending) {
@@ -203,87 +203,112 @@ RESPCA_DEV void cp_wait_dyn(int pending) {
     }
 }
 
-// Block refresh partials of one CTA: its row slice [s0, s1) of
-// x_jb · c_stale[t] for every block column jb < nb and stale centroid t, as
-// TQ×TK register tiles (a tile's columns / centroids strided by ntq / ntk so
-// that a warp reads consecutive shared words).  Row chunks of R rows stream
-// through HART_NST cp.async stages.  Output: part[(jb·c + t)·G + CTA].
-template <typename T, int TQ, int TK>
-RESPCA_DEV void hart_entry_tiles(const T* __restrict__ M, const HartArgs& a, const int* vs,
-                                 const int* stale, int nstale, int b0, int nb, int B, int64_t s0,
-                                 int64_t s1, int R, T* stc, double* sce) {
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int c = a.c, G = gridDim.x;
+// Block refresh partials of one CTA on the FP64 tensor cores (DMMA m8n8k4):
+// its row slice [s0, s1) of x_jb · c_stale[t] for every block column jb < nb
+// and stale centroid t.  Operands are staged i-contiguous ([col][row], row
+// stride R + 4: conflict-free fragment loads, as in km.cuh), in chunks of R
+// rows (a power of two ≥ 8) through a.stages cp.async stages, zero-padded to
+// whole 16×16 warp tiles (2×2 DMMA tiles: each fragment feeds two MMAs).
+// A warp owns up to TPW warp tiles per round.  Output: part[(jb·c + t)·G + CTA].
+template <typename T, int TPW>
+RESPCA_DEV void hart_entry_dmma(const T* __restrict__ M, const HartArgs& a, const int* vs,
+                                const int* stale, int nstale, int b0, int nb, int64_t s0, int64_t s1,
+                                int R, T* stc, double* sce, unsigned long long* tacc) {
+    const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
+    const int nwarps = nt >> 5;
+    const int c = a.c, G = gridDim.x, NS = a.stages;
     const int64_t d = a.d;
-    const int ntq = (nb + TQ - 1) / TQ, ntk = (nstale + TK - 1) / TK, ntiles = ntq * ntk;
+    const double* __restrict__ Cs = a.Cs;
+    const int MP = (nb + 15) & ~15, NP = (nstale + 15) & ~15, RS = R + 4;
+    const int wtn = NP >> 4, nwt = (MP >> 4) * wtn;  // 16×16 warp tiles
+    const int lgR = 31 - __clz(R);
+    const size_t sstc = (size_t)MP * RS, ssce = (size_t)NP * RS;
     const int nch = s1 > s0 ? (int)((s1 - s0 + R - 1) / R) : 0;
+    const int g = lane >> 2, t4 = lane & 3;
+    unsigned long long tq0 = tid == 0 ? (unsigned long long)clock64() : 0;
+    auto lapt = [&](int slot) {
+        if (tid == 0) {
+            const unsigned long long t = (unsigned long long)clock64();
+            tacc[slot] += t - tq0;
+            tq0 = t;
+        }
+    };
     auto issue = [&](int ch) {
         const int64_t c0 = s0 + (int64_t)ch * R;
         const int rows = (int)(s1 - c0 < R ? s1 - c0 : R);
-        T* sb = stc + (size_t)(ch % HART_NST) * R * B;
-        double* cb = sce + (size_t)(ch % HART_NST) * R * c;
-        for (int e = tid; e < nb * rows; e += nt) {
-            const int jb = e / rows, rr = e - (e / rows) * rows;
-            const T* src = M + (int64_t)(b0 + jb) * d + c0 + rr;
-            if (sizeof(T) == 8) cp_async8(sb + rr * B + jb, src, true);
-            else cp_async4(sb + rr * B + jb, src, true);
+        T* sb = stc + (size_t)(ch % NS) * sstc;
+        double* cb = sce + (size_t)(ch % NS) * ssce;
+        for (int e = tid; e < (MP << lgR); e += nt) {
+            const int jb = e >> lgR, rr = e & (R - 1);
+            const bool ok = jb < nb && rr < rows;
+            const T* src = M + (int64_t)(b0 + (ok ? jb : 0)) * d + c0 + (ok ? rr : 0);
+            if (sizeof(T) == 8) cp_async8(sb + jb * RS + rr, src, ok);
+            else cp_async4(sb + jb * RS + rr, src, ok);
         }
-        for (int e = tid; e < nstale * rows; e += nt) {
-            const int t = e / rows, rr = e - (e / rows) * rows;
-            const int k = stale[t];
-            cp_async8(cb + rr * c + t, a.Cs + ((int64_t)vs[k] * c + k) * d + c0 + rr, true);
+        for (int e = tid; e < (NP << lgR); e += nt) {
+            const int t = e >> lgR, rr = e & (R - 1);
+            const bool ok = t < nstale && rr < rows;
+            const int k = stale[t < nstale ? t : 0];
+            cp_async8(cb + t * RS + rr, Cs + ((int64_t)vs[k] * c + k) * d + c0 + (ok ? rr : 0), ok);
         }
         cp_commit();
     };
-    for (int tr0 = 0; tr0 < ntiles; tr0 += nt) {
-        const int tile = tr0 + tid;
-        const bool act = tile < ntiles;
-        const int tq = act ? tile / ntk : 0, tk = act ? tile - (tile / ntk) * ntk : 0;
-        double acc[TQ * TK];
+    for (int tr0 = 0; tr0 < nwt; tr0 += nwarps * TPW) {
+        double acc[TPW][2][2][2];  // [warp tile][m half][n half][fragment]
+        int wm[TPW], wn[TPW];
 #pragma unroll
-        for (int e = 0; e < TQ * TK; ++e) acc[e] = 0.0;
+        for (int i = 0; i < TPW; ++i) {
+            const int wt = tr0 + warp + i * nwarps;
+            wm[i] = wt < nwt ? wt / wtn : -1;
+            wn[i] = wt < nwt ? wt - (wt / wtn) * wtn : 0;
+#pragma unroll
+            for (int x = 0; x < 2; ++x)
+#pragma unroll
+                for (int y = 0; y < 2; ++y) acc[i][x][y][0] = acc[i][x][y][1] = 0.0;
+        }
         __syncthreads();  // stage buffers free
         int issued = 0;
-        for (; issued < nch && issued < HART_NST - 1; ++issued) issue(issued);
+        for (; issued < nch && issued < NS - 1; ++issued) issue(issued);
         for (int ch = 0; ch < nch; ++ch) {
+            lapt(2);
             if (issued < nch) issue(issued++);  // refills the stage chunk ch−1 used
+            lapt(0);
             cp_wait_dyn(issued - ch - 1);
             __syncthreads();
-            if (act) {
-                const int64_t c0 = s0 + (int64_t)ch * R;
-                const int rows = (int)(s1 - c0 < R ? s1 - c0 : R);
-                const T* sb = stc + (size_t)(ch % HART_NST) * R * B;
-                const double* cb = sce + (size_t)(ch % HART_NST) * R * c;
-                for (int rr = 0; rr < rows; ++rr) {
-                    double xq[TQ], ck[TK];
+            lapt(1);
+            const T* sb = stc + (size_t)(ch % NS) * sstc;
+            const double* cb = sce + (size_t)(ch % NS) * ssce;
 #pragma unroll
-                    for (int u = 0; u < TQ; ++u) {
-                        const int jb = tq + u * ntq;
-                        xq[u] = jb < nb ? (double)sb[rr * B + jb] : 0.0;
-                    }
-#pragma unroll
-                    for (int w = 0; w < TK; ++w) {
-                        const int t = tk + w * ntk;
-                        ck[w] = t < nstale ? cb[rr * c + t] : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < TQ; ++u)
-#pragma unroll
-                        for (int w = 0; w < TK; ++w) acc[u * TK + w] = __fma_rn(xq[u], ck[w], acc[u * TK + w]);
+            for (int i = 0; i < TPW; ++i) {
+                if (wm[i] < 0) continue;
+                const T* ap = sb + (wm[i] * 16 + g) * RS + t4;
+                const double* bp = cb + (wn[i] * 16 + g) * RS + t4;
+                for (int k0 = 0; k0 < R; k0 += 4) {
+                    const double a0 = (double)ap[k0], a1 = (double)ap[8 * RS + k0];
+                    const double bv0 = bp[k0], bv1 = bp[8 * RS + k0];
+                    dmma884(acc[i][0][0][0], acc[i][0][0][1], a0, bv0);
+                    dmma884(acc[i][0][1][0], acc[i][0][1][1], a0, bv1);
+                    dmma884(acc[i][1][0][0], acc[i][1][0][1], a1, bv0);
+                    dmma884(acc[i][1][1][0], acc[i][1][1][1], a1, bv1);
                 }
             }
             __syncthreads();  // chunk consumed before its stage is refilled
         }
-        if (act) {
 #pragma unroll
-            for (int u = 0; u < TQ; ++u)
+        for (int i = 0; i < TPW; ++i)
+            if (wm[i] >= 0)
 #pragma unroll
-                for (int w = 0; w < TK; ++w) {
-                    const int jb = tq + u * ntq, t = tk + w * ntk;
-                    if (jb < nb && t < nstale)
-                        __stcg(a.part + ((size_t)jb * c + t) * G + blockIdx.x, acc[u * TK + w]);
+                for (int x = 0; x < 2; ++x) {
+                    const int jb = wm[i] * 16 + x * 8 + g;
+#pragma unroll
+                    for (int y = 0; y < 2; ++y)
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int t = wn[i] * 16 + y * 8 + 2 * t4 + h;
+                            if (jb < nb && t < nstale)
+                                __stcg(a.part + ((size_t)jb * c + t) * G + blockIdx.x, acc[i][x][y][h]);
+                        }
                 }
-        }
     }
 }
 
@@ -312,10 +337,10 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     off += sizeof(double) * c;
     double* red = reinterpret_cast<double*>(sm + off);
     off += sizeof(double) * HART_RED;
-    T* stc = reinterpret_cast<T*>(sm + off);  // [HART_NST][R][B] block-column row chunks
-    off += HART_NST * sizeof(double) * (size_t)R * B;
-    double* sce = reinterpret_cast<double*>(sm + off);  // [HART_NST][R][c] stale-centroid row chunks
-    off += HART_NST * sizeof(double) * (size_t)R * c;
+    T* stc = reinterpret_cast<T*>(sm + off);  // [stages][B↑16][R+4] block-column row chunks
+    off += (size_t)a.stages * sizeof(double) * (size_t)(R + 4) * ((B + 15) & ~15);
+    double* sce = reinterpret_cast<double*>(sm + off);  // [stages][c↑16][R+4] stale-centroid row chunks
+    off += (size_t)a.stages * sizeof(double) * (size_t)(R + 4) * ((c + 15) & ~15);
     int* stale = reinterpret_cast<int*>(sm + off);
     off += sizeof(int) * c;
     int* cnt = reinterpret_cast<int*>(sm + off);
@@ -327,6 +352,7 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     __shared__ int s_lab[MAXQ];
     __shared__ int s_nstale;
     __shared__ __align__(8) uint64_t s_bar;  // column fills (bulk copies)
+
 
     const uint32_t col_bytes = (uint32_t)(d * (int64_t)sizeof(T));
     const bool bulk = cache_cols && (col_bytes % 16 == 0) && ((uintptr_t)M % 16 == 0);
@@ -362,10 +388,11 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     unsigned long long rounds = 0, blocks = 0, refreshed = 0, t_load = 0, t_cols = 0;
     unsigned long long stale_sum = 0, heavy = 0;
     unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    unsigned long long tmark = gtimer();
+    unsigned long long tsub[3] = {0, 0, 0};  // entry tiles: issue, wait, compute+sync
+    unsigned long long tmark = (unsigned long long)clock64();  // SM cycles
     auto lap = [&](int slot) {
         if (tid == 0) {
-            const unsigned long long t = gtimer();
+            const unsigned long long t = (unsigned long long)clock64();
             tm[slot] += t - tmark;
             tmark = t;
         }
@@ -566,15 +593,13 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                 // ---- block refresh, split over rows: this CTA's row slice of
                 //      (every block column) · (every stale centroid) → HBM
                 //      partials; then each owned column sums its G partials
-                const int nb2 = (nb + 1) >> 1, nb4 = (nb + 3) >> 2;
-                const int ns2 = (nstale + 1) >> 1;
-                const int nt = (int)blockDim.x;
-                if (nb2 * ns2 <= nt)
-                    hart_entry_tiles<T, 2, 2>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
-                else if (nb4 * ns2 <= nt)
-                    hart_entry_tiles<T, 4, 2>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
-                else  // 4×4 tiles, several tile rounds when the block is large
-                    hart_entry_tiles<T, 4, 4>(M, a, vs, stale, nstale, b0, nb, B, s0, s1, R, stc, sce);
+                {
+                    const int nwt = ((nb + 15) >> 4) * ((nstale + 15) >> 4), nw = (int)(blockDim.x >> 5);
+                    if (nwt <= nw)
+                        hart_entry_dmma<T, 1>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub);
+                    else
+                        hart_entry_dmma<T, 2>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub);
+                }
                 lap(1);
                 grid_barrier(hg);
                 lap(2);
@@ -638,6 +663,21 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                 };
                 const int st = hart_decide_warp_w(from, c, cnt, wa, wb, iv, to);
                 if (st != 0 && lane == 0) atomicMin(&hg->first[r % 3][0], pack4(j, st, from, to));
+                if (a.diag && st == 0 && cnt[from] > 1) {
+                    // diagnostics: relative margin of a "no move" decision
+                    double mn = INFINITY;
+                    for (int k = lane; k < c; k += 32)
+                        if (k != from) mn = fmin(mn, wb[k] * As[warp * c + k]);
+                    for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+                    if (lane == 0) {
+                        const double sc = sqrt(fabs(s_xx[warp])) + sqrt(fabs(ccs[from]));
+                        const double m = (mn - wa[from] * As[warp * c + from]) / (sc * sc);
+                        double th = 1e-1;
+                        for (int b = 0; b < 8; ++b, th *= 0.1)
+                            if (m < th) atomicAdd(&hg->hist[b], 1ULL);
+                        atomicAdd(&hg->hist[8], 1ULL);
+                    }
+                }
             }
         }
         // slot (r+1)%3 is next written after this barrier and last read before
@@ -738,6 +778,7 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
             hg->stale_sum = stale_sum;
             hg->heavy_blocks = heavy;
             for (int q = 0; q < 8; ++q) hg->tm[q] = tm[q];
+            hg->tm[6] = tsub[0]; hg->tsub1 = tsub[1]; hg->tsub2 = tsub[2];
         }
     }
     if (lane == 0 && refreshed) atomicAdd(&hg->refreshed, refreshed);

@@ -349,16 +349,22 @@ struct KMeansEngine {
     int hart_ctas = 0;  // CTAs of the Hartigan kernel (0: one per SM)
     std::function<void()> before_hartigan;  // restart lanes: wait for the others' seeding/Lloyd
 
+    static int env_int(const char* name, int dflt) {
+        const char* e = std::getenv(name);
+        return e ? std::atoi(e) : dflt;
+    }
     struct HartGeom {
-        int G = 1, cpb = 1, B = 1, R = 1;
+        int G = 1, cpb = 1, B = 1, R = 8, stages = 2;
         bool cache = true;
         size_t smem = 0;
     };
     // shared memory of the Hartigan kernel (hartigan.cuh carve-up)
-    size_t hart_smem(int cpb, bool cache, int B, int R) const {
+    size_t hart_smem(int cpb, bool cache, int B, int R, int stages) const {
+        const size_t stage = R > 0 ? (size_t)stages * sizeof(double) * (size_t)(R + 4) *
+                                         (size_t)(((B + 15) & ~15) + ((c + 15) & ~15))
+                                   : 0;
         return (cache ? (size_t)cpb * d * sizeof(T) + 16 : 0) + sizeof(double) * 2 * (size_t)cpb * c +
-               sizeof(double) * (3 * (size_t)c + HART_RED) + HART_NST * sizeof(double) * (size_t)R * (B + c) +
-               sizeof(int) * 4 * (size_t)c + 2048;
+               sizeof(double) * (3 * (size_t)c + HART_RED) + stage + sizeof(int) * 4 * (size_t)c + 2048;
     }
     HartGeom hart_geometry() const {
         int dev = 0, nsm = 148, optin = 0;
@@ -375,14 +381,17 @@ struct KMeansEngine {
                 g.cpb = cpb;
                 g.G = std::max(1, std::min(avail, ceil_div(n, cpb)));
                 g.B = g.G * cpb;
-                const size_t base = hart_smem(cpb, cache, g.B, 0);
-                if (base >= (size_t)optin) continue;
-                const size_t per_row = HART_NST * sizeof(double) * (size_t)(g.B + c);  // cp.async stages
-                const int64_t R = (int64_t)(((size_t)optin - base) / per_row);
-                if (R < 4 && !(R >= 1 && d <= R)) continue;
-                g.R = (int)std::min<int64_t>(R, 32);
-                g.smem = hart_smem(cpb, cache, g.B, g.R);
-                return g;
+                // refresh chunks: the most rows (32/16/8), then the most stages (3/2)
+                for (int R : {32, 16, 8})
+                    for (int stages : {3, 2}) {
+                        if (R > 8 && (int64_t)R / 2 >= (d + g.G - 1) / g.G) continue;  // slice shorter
+                        const size_t sm = hart_smem(cpb, cache, g.B, R, stages);
+                        if (sm > (size_t)optin) continue;
+                        g.R = R;
+                        g.stages = stages;
+                        g.smem = sm;
+                        return g;
+                    }
             }
         }
         throw InvalidArg("hartigan: c too large for the device's shared memory");
@@ -435,6 +444,8 @@ struct KMeansEngine {
         a.ebuf = hebuf.p;
         a.part = hpart.p;
         a.stage_rows = hgm.R;
+        a.stages = hgm.stages;
+        a.diag = env_int("RESPCA_HART_DIAG", 0);
         a.xx = hxx.p;
         a.cc0 = cc.p;
         a.scratch = scratch.p;
@@ -475,10 +486,16 @@ struct KMeansEngine {
                              (unsigned long long)hh->heavy_blocks);
             if (trace_on())
                 std::fprintf(stderr,
-                             "[respca] hartigan CTA0 phases (s): update %.3f entry-tiles %.3f entry-barrier %.3f "
-                             "entry-reduce+wait %.3f decide %.3f barrier %.3f settle %.3f\n",
-                             1e-9 * hh->tm[0], 1e-9 * hh->tm[1], 1e-9 * hh->tm[2], 1e-9 * hh->tm[3],
-                             1e-9 * hh->tm[4], 1e-9 * hh->tm[5], 1e-9 * hh->tm[7]);
+                             "[respca] hartigan CTA0 phases (s at 1.965 GHz): update %.3f entry-tiles %.3f entry-barrier %.3f "
+                             "entry-reduce+wait %.3f decide %.3f barrier %.3f settle %.3f | tiles: issue %.3f wait %.3f compute %.3f\n",
+                             hh->tm[0] / 1.965e9, hh->tm[1] / 1.965e9, hh->tm[2] / 1.965e9, hh->tm[3] / 1.965e9,
+                             hh->tm[4] / 1.965e9, hh->tm[5] / 1.965e9, hh->tm[7] / 1.965e9, hh->tm[6] / 1.965e9,
+                             hh->tsub1 / 1.965e9, hh->tsub2 / 1.965e9);
+            if (trace_on() && env_int("RESPCA_HART_DIAG", 0))
+                std::fprintf(stderr,
+                             "[respca] hartigan no-move margins / (|x|+|c|)^2 below 1e-1..1e-8: %llu %llu %llu %llu %llu %llu %llu %llu of %llu\n",
+                             hh->hist[0], hh->hist[1], hh->hist[2], hh->hist[3], hh->hist[4], hh->hist[5], hh->hist[6],
+                             hh->hist[7], hh->hist[8]);
         }
     }
 
@@ -666,6 +683,7 @@ struct KMeansEngine {
                 if (e.st) cudaStreamDestroy(e.st);
             }
         };
+        const auto t_k0 = HClock::now();
         std::vector<std::unique_ptr<Lane>> lanes;
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
@@ -691,6 +709,7 @@ struct KMeansEngine {
             ln_.bc.ensure((size_t)d * c);
         }
         CK(cudaEventDestroy(ready));
+        if (trace_on()) std::fprintf(stderr, "[respca] lanes: %d set up in %.3fs\n", L, since(t_k0));
         std::mt19937_64 rng(seed);
         std::mutex mu;
         std::condition_variable cv;
@@ -754,10 +773,14 @@ struct KMeansEngine {
                     holds_turn = false;
                     e.gather(chosen, ln_.wc.p);
                     if (e.stats) e.stats->t_pp += since(tp);
+                    const double t_pp_end = since(t_k0);
                     const uint64_t it = e.lloyd_run(ln_.wc.p, ln_.wl.p, max_iters, tol);
                     const auto ti = HClock::now();
                     const double in = e.inertia(ln_.wc.p, ln_.wl.p);
                     if (e.stats) e.stats->t_inertia += since(ti);
+                    if (trace_on())
+                        std::fprintf(stderr, "[respca] lane %d restart %llu: seeded at %.3fs, done at %.3fs\n", l,
+                                     (unsigned long long)r, t_pp_end, since(t_k0));
                     if (in < ln_.best_in) {
                         ln_.best_in = in;
                         ln_.best_r = (int)r;
@@ -780,6 +803,7 @@ struct KMeansEngine {
         std::vector<std::thread> threads;
         for (int l = 0; l < L; ++l) threads.emplace_back(body, l);
         for (auto& t : threads) t.join();
+        if (trace_on()) std::fprintf(stderr, "[respca] lanes joined at %.3fs\n", since(t_k0));
         for (auto& lp : lanes) {
             *ln.counter += lp->launches;
             if (stats) {
