@@ -52,7 +52,7 @@ struct Groups {
 
 struct Stats {
     uint64_t hartigan_moves = 0, exact_fallbacks = 0, lloyd_steps = 0, hartigan_passes = 0;
-    uint64_t hartigan_rounds = 0, hartigan_refreshes = 0;
+    uint64_t hartigan_rounds = 0, hartigan_refreshes = 0, pp_respeculated = 0;
     double t_pp = 0, t_lloyd = 0, t_hart = 0, t_inertia = 0;  // seconds (host clock, synced)
     double t_hart_kernel = 0;  // device span of the Hartigan round kernels
 };
@@ -710,10 +710,30 @@ struct KMeansEngine {
         }
         CK(cudaEventDestroy(ready));
         if (trace_on()) std::fprintf(stderr, "[respca] lanes: %d set up in %.3fs\n", L, since(t_k0));
-        std::mt19937_64 rng(seed);
+        // Restart r's seeding draws continue restart r−1's (one libstdc++
+        // engine, kmeans.cpp:240): 1 uniform_int, then 1 uniform_real per pick
+        // whose d² total is positive (kmeans.cpp:196-211) — c−1 of them unless
+        // the data degenerate.  Seedings therefore start from SPECULATED engine
+        // states (that count assumed) and are checked against the true state
+        // once restart r−1's seeding is known; a mismatch redoes the seeding.
+        std::vector<std::mt19937_64> spec(n_restarts), truth(n_restarts + 1);
+        std::vector<char> truth_known(n_restarts + 1, 0);
+        {
+            std::mt19937_64 sim(seed);
+            for (uint64_t r = 0; r < n_restarts; ++r) {
+                spec[r] = sim;
+                std::uniform_int_distribution<std::size_t> first(0, (std::size_t)n - 1);
+                (void)first(sim);
+                for (int p = 1; p < c; ++p) {
+                    std::uniform_real_distribution<double> u(0.0, 1.0);
+                    (void)u(sim);
+                }
+            }
+            truth[0] = std::mt19937_64(seed);
+            truth_known[0] = 1;
+        }
         std::mutex mu;
         std::condition_variable cv;
-        uint64_t turn = 0;                 // restart whose seeding may draw next
         uint64_t abort_at = UINT64_MAX;    // restarts after a failed one are skipped
         std::vector<std::exception_ptr> errs(n_restarts);
         // a persistent Hartigan grid holds its SMs until it ends: no lane
@@ -755,22 +775,30 @@ struct KMeansEngine {
                 return;
             }
             for (uint64_t r = (uint64_t)l; r < n_restarts; r += (uint64_t)L) {
-                bool holds_turn = false;
                 try {
+                    // seeding from the speculated engine state, then confirmed
+                    // against the true one (redone from it on a mismatch)
+                    const auto tp = HClock::now();
+                    std::mt19937_64 eng = spec[r];
+                    std::vector<int> chosen = e.pp_init(eng);
+                    std::mt19937_64 start;
                     {
                         std::unique_lock<std::mutex> lk(mu);
-                        cv.wait(lk, [&] { return turn == r || r > abort_at; });
+                        cv.wait(lk, [&] { return truth_known[r] || r > abort_at; });
                         if (r > abort_at) return;
+                        start = truth[r];
                     }
-                    holds_turn = true;
-                    const auto tp = HClock::now();
-                    const std::vector<int> chosen = e.pp_init(rng);
+                    if (!(start == spec[r])) {
+                        eng = start;
+                        chosen = e.pp_init(eng);
+                        if (e.stats) e.stats->pp_respeculated += 1;
+                    }
                     {
                         std::lock_guard<std::mutex> g(mu);
-                        turn = r + 1;
+                        truth[r + 1] = eng;
+                        truth_known[r + 1] = 1;
                     }
                     cv.notify_all();
-                    holds_turn = false;
                     e.gather(chosen, ln_.wc.p);
                     if (e.stats) e.stats->t_pp += since(tp);
                     const double t_pp_end = since(t_k0);
@@ -794,7 +822,6 @@ struct KMeansEngine {
                     std::lock_guard<std::mutex> g(mu);
                     errs[r] = std::current_exception();
                     abort_at = std::min(abort_at, r);
-                    if (holds_turn) turn = r + 1;
                     cv.notify_all();
                     return;
                 }
@@ -814,6 +841,7 @@ struct KMeansEngine {
                 stats->hartigan_passes += s2.hartigan_passes;
                 stats->hartigan_rounds += s2.hartigan_rounds;
                 stats->hartigan_refreshes += s2.hartigan_refreshes;
+                stats->pp_respeculated += s2.pp_respeculated;
                 stats->t_pp += s2.t_pp;
                 stats->t_lloyd += s2.t_lloyd;
                 stats->t_hart += s2.t_hart;

@@ -176,6 +176,16 @@ def test_kmeans_restart_lanes_bitwise(ctx, orc, R, monkeypatch, lanes):
         assert (a.assignment == lab).all()
         assert bitwise(a.centroids, cen)
         assert a.inertia == inertia and a.iters_run == it
+    # duplicate columns: a seeding runs out of positive d² mass and skips its
+    # draws, so the next restarts' speculated engine states are wrong and are
+    # redone from the true ones
+    base = np.random.default_rng(3).uniform(-1, 1, (6, 3))
+    m = np.asfortranarray(np.array([base[:, i % 3] for i in range(30)]).T)
+    m[:, 5] += 1e-3
+    a = R.kmeans(m, KMeansConfig(c=5, seed=11, n_restarts=5), ctx=ctx)
+    lab, cen, inertia, it = orc.kmeans(m, 5, 100, 5, 11, 1e-6)
+    assert (a.assignment == lab).all() and bitwise(a.centroids, cen)
+    assert a.inertia == inertia and a.iters_run == it
 
 
 def test_kmeans_warm_bitwise(ctx, orc, R):
