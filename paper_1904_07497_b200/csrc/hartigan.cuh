@@ -87,9 +87,17 @@ RESPCA_DEV int hart_decide_warp_w(int from, int c, const int* cnt, const double*
     return 1;
 }
 
+// Hartigan intervals [mid − e, mid + e] contain BOTH the reference's computed
+// sq_dist (sequential chain) and the real ‖x − c‖² to the stored centroid:
+// |ref − real| ≤ γ·real for a chain of d positive rounded squares, γ = (d+3)u·1.02.
+// The real value is what the exact move identities below transform.
+RESPCA_DEV double hart_widen(double mid, double e, double gam) {
+    return __dadd_ru(e, __dmul_ru(gam, __dadd_ru(fabs(mid), e)));
+}
+
 // intervals of every (column, centroid) pair from a full screen (start state)
 __global__ void k_hart_fill(Screen sc, double* __restrict__ A, double* __restrict__ E,
-                            double* __restrict__ xx, int n, int c) {
+                            double* __restrict__ xx, int n, int c, double gam) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (int64_t)n * c) return;
     const int j = (int)(e / c), k = (int)(e % c);
@@ -97,7 +105,7 @@ __global__ void k_hart_fill(Screen sc, double* __restrict__ A, double* __restric
     double lo, hi, mid;
     sc.get(j, k, xxj, sqrt(fabs(xxj)), lo, hi, mid);
     A[e] = mid;
-    E[e] = isfinite(hi - mid) ? hi - mid : INFINITY;
+    E[e] = isfinite(hi - mid) ? hart_widen(mid, hi - mid, gam) : INFINITY;
     if (k == 0) xx[j] = xxj;
 }
 
@@ -124,7 +132,7 @@ struct HartGlobal {
     alignas(128) unsigned long long moves, exact_fallbacks, rounds, passes, blocks, refreshed;
     unsigned long long t_kernel, t_load, t_cols;  // globaltimer (CTA 0): whole kernel, block loads, column fills
     unsigned long long stale_sum, heavy_blocks;   // CTA 0: stale centroids over all block entries, entries with > 8
-    unsigned long long tsub1, tsub2;
+    unsigned long long tsub1, tsub2, redos, act_cycles, act_rounds, dq_cycles;
     unsigned long long hist[9];  // diagnostics: no-move margins below 1e-1..1e-8, total
     unsigned long long tm[8];  // CTA 0 phase sums: 1, entry tiles, entry barrier, entry reduce, decide, barrier, settle
 };
@@ -186,9 +194,12 @@ struct HartArgs {
     const double* xx;     // [n]   ‖x_j‖² (screen)
     const double* cc0;    // [c]   ‖c_k‖² of the start centroids (screen)
     double* scratch;      // [c]   exact distances of one column (near-tie)
+    double* cand;         // [n][4] a candidate column's (mid, e) to its from / to centroid
+    double* ccp;          // [c][G] row-slice partials of ‖c‖² (block refresh)
     int64_t d;
     int n, c, cpb, cache_cols, max_pass, stage_rows, stages, diag;
     double kappa_d;       // screen bound factor (km.cuh) + the reciprocal-update term
+    double gam;           // (d+3)u·1.02: reference chain vs real distance (hart_widen)
 };
 
 constexpr int HART_RED = 32 * 24;  // block_sum scratch (≤ 24 sums)
@@ -213,7 +224,7 @@ RESPCA_DEV void cp_wait_dyn(int pending) {
 template <typename T, int TPW>
 RESPCA_DEV void hart_entry_dmma(const T* __restrict__ M, const HartArgs& a, const int* vs,
                                 const int* stale, int nstale, int b0, int nb, int64_t s0, int64_t s1,
-                                int R, T* stc, double* sce, unsigned long long* tacc) {
+                                int R, T* stc, double* sce, unsigned long long* tacc, double* ccacc) {
     const int tid = threadIdx.x, nt = blockDim.x, warp = tid >> 5, lane = tid & 31;
     const int nwarps = nt >> 5;
     const int c = a.c, G = gridDim.x, NS = a.stages;
@@ -266,6 +277,9 @@ RESPCA_DEV void hart_entry_dmma(const T* __restrict__ M, const HartArgs& a, cons
 #pragma unroll
                 for (int y = 0; y < 2; ++y) acc[i][x][y][0] = acc[i][x][y][1] = 0.0;
         }
+        const bool norms = tr0 == 0;  // ‖c‖² slice partials, once
+        if (norms)
+            for (int t = tid; t < nstale; t += nt) ccacc[t] = 0.0;
         __syncthreads();  // stage buffers free
         int issued = 0;
         for (; issued < nch && issued < NS - 1; ++issued) issue(issued);
@@ -278,6 +292,15 @@ RESPCA_DEV void hart_entry_dmma(const T* __restrict__ M, const HartArgs& a, cons
             lapt(1);
             const T* sb = stc + (size_t)(ch % NS) * sstc;
             const double* cb = sce + (size_t)(ch % NS) * ssce;
+            if (norms) {  // thread per stale centroid, on the warps without tiles if any
+                const int w0 = nwt < nwarps ? nwt : 0, nw0 = nwarps - w0;
+                if (warp >= w0)
+                    for (int t = (warp - w0) * 32 + lane; t < nstale; t += nw0 * 32) {
+                        double v = ccacc[t];
+                        for (int rr = 0; rr < R; ++rr) v = __fma_rn(cb[t * RS + rr], cb[t * RS + rr], v);
+                        ccacc[t] = v;
+                    }
+            }
 #pragma unroll
             for (int i = 0; i < TPW; ++i) {
                 if (wm[i] < 0) continue;
@@ -310,6 +333,8 @@ RESPCA_DEV void hart_entry_dmma(const T* __restrict__ M, const HartArgs& a, cons
                         }
                 }
     }
+    __syncthreads();
+    for (int t = tid; t < nstale; t += nt) __stcg(a.ccp + (size_t)t * G + blockIdx.x, ccacc[t]);
 }
 
 template <typename T, int MAXQ>
@@ -341,6 +366,8 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     off += (size_t)a.stages * sizeof(double) * (size_t)(R + 4) * ((B + 15) & ~15);
     double* sce = reinterpret_cast<double*>(sm + off);  // [stages][c↑16][R+4] stale-centroid row chunks
     off += (size_t)a.stages * sizeof(double) * (size_t)(R + 4) * ((c + 15) & ~15);
+    double* ccacc = reinterpret_cast<double*>(sm + off);  // [c] ‖c‖² slice partials
+    off += sizeof(double) * c;
     int* stale = reinterpret_cast<int*>(sm + off);
     off += sizeof(int) * c;
     int* cnt = reinterpret_cast<int*>(sm + off);
@@ -386,7 +413,7 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     const int64_t s0 = (int64_t)blockIdx.x * slice < d ? (int64_t)blockIdx.x * slice : d;
     const int64_t s1 = s0 + slice < d ? s0 + slice : d;
     unsigned long long rounds = 0, blocks = 0, refreshed = 0, t_load = 0, t_cols = 0;
-    unsigned long long stale_sum = 0, heavy = 0;
+    unsigned long long stale_sum = 0, heavy = 0, redos = 0, act_cycles = 0, act_rounds = 0, dq_cycles = 0;
     unsigned long long tm[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tsub[3] = {0, 0, 0};  // entry tiles: issue, wait, compute+sync
     unsigned long long tmark = (unsigned long long)clock64();  // SM cycles
@@ -401,12 +428,19 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
 
     for (int r = 0;; ++r) {
         lap(7);
-        // ---- phase 1: the pending move (kmeans.cpp:126-131).  Every CTA runs
-        //      the update over all rows: its own row slice with the reference's
-        //      exact formula (stored to the other slot), every row with a
-        //      reciprocal multiply for ‖c′‖² and the dots of its owned columns
-        //      still to visit (within the bound, kappa_d).  No grid barrier: a
-        //      slot's slices are read by other CTAs only after the next one.
+        // ---- phase 1: the pending move (kmeans.cpp:126-131).
+        //  (a) this CTA's row slice of both updated centroids, with the
+        //      reference's exact formula, to the other slot (other CTAs read a
+        //      slot's slices only after the next grid barrier);
+        //  (b) the owned columns still to visit get their from/to intervals by
+        //      the exact move identities (real distances; e = exact update)
+        //        ‖x−e_f‖² = (n·D_xf − D_xm)/(n−1) + n·D_fm/(n−1)²
+        //        ‖x−e_t‖² = (n·D_xt + D_xm)/(n+1) − n·D_tm/(n+1)²
+        //      evaluated in directed rounding from the old intervals, the
+        //      moved column's own (broadcast by its owner) and D_xm = ‖x − x_m‖²
+        //      (one pass over x_m), plus the stored-vs-exact centroid rounding
+        //      and the chain-vs-real slack; when that interval has grown too
+        //      wide the CTA recomputes its entries from the new centroid values.
         if (pf >= 0) {
             const double* of = a.Cs + ((int64_t)vs[pf] * c + pf) * d;
             const double* ot = a.Cs + ((int64_t)vs[pt] * c + pt) * d;
@@ -415,91 +449,174 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
             const T* xm = M + (int64_t)pm * d;
             const double dcf = (double)pnf, dct = (double)pnt;
             const double na1 = (double)(pnf - 1), nb1 = (double)(pnt + 1);
-            const double rf = 1.0 / na1, rt = 1.0 / nb1;
+            for (int64_t i = s0 + tid; i < s1; i += blockDim.x) {
+                const double x = (double)__ldg(xm + i);
+                __stcg(nfp + i, (__ldcg(of + i) * dcf - x) / na1);  // kmeans.cpp:128-129 operation order
+                __stcg(ntp + i, (__ldcg(ot + i) * dct + x) / nb1);
+            }
             int nact = 0;
             for (int q = 0; q < nown; ++q) nact += (jown + q >= cursor);
             const int q0 = nown - nact;  // active owned columns: the suffix q0..nown-1
-            double acc[2 + 2 * MAXQ];
+            const double mf = __ldcg(a.cand + 4 * (int64_t)pm), ef = __ldcg(a.cand + 4 * (int64_t)pm + 1);
+            const double mt = __ldcg(a.cand + 4 * (int64_t)pm + 2), et = __ldcg(a.cand + 4 * (int64_t)pm + 3);
+            const double xxm = __ldcg(a.xx + pm);
+            bool redo = false;
+            double nmid = 0.0, ne = INFINITY;
+            const unsigned long long ta0 = clock64();
+            if (nact) {  // block-uniform
+                double dq[MAXQ];
 #pragma unroll
-            for (int e = 0; e < 2 + 2 * MAXQ; ++e) acc[e] = 0.0;
-            auto row = [&](int64_t i, double x, double ofv, double otv) {
-                const double uf = ofv * dcf - x;  // kmeans.cpp:128-129 operation order
-                const double ut = otv * dct + x;
-                if (i >= s0 && i < s1) {
-                    __stcg(nfp + i, uf / na1);
-                    __stcg(ntp + i, ut / nb1);
+                for (int q = 0; q < MAXQ; ++q) dq[q] = 0.0;
+                auto rowq = [&](int64_t i, double x) {
+#pragma unroll
+                    for (int q = 0; q < MAXQ; ++q)
+                        if (q < nact) {
+                            const double t = colv(jown, q0 + q, i) - x;
+                            dq[q] = __fma_rn(t, t, dq[q]);
+                        }
+                };
+                const int64_t step = blockDim.x;
+                if (sizeof(T) == 8 && (d & 1) == 0) {
+                    const double2* x2 = reinterpret_cast<const double2*>(xm);
+                    const int64_t dh = d >> 1;
+                    int64_t i = tid;
+                    for (; i + 7 * step < dh; i += 8 * step) {
+                        double2 xv[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) xv[u] = __ldg(x2 + i + u * step);
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            rowq(2 * (i + u * step), xv[u].x);
+                            rowq(2 * (i + u * step) + 1, xv[u].y);
+                        }
+                    }
+                    if (i + 3 * step < dh) {
+                        double2 xv[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) xv[u] = __ldg(x2 + i + u * step);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            rowq(2 * (i + u * step), xv[u].x);
+                            rowq(2 * (i + u * step) + 1, xv[u].y);
+                        }
+                        i += 4 * step;
+                    }
+                    for (; i < dh; i += step) {
+                        const double2 xv = __ldg(x2 + i);
+                        rowq(2 * i, xv.x);
+                        rowq(2 * i + 1, xv.y);
+                    }
+                } else {
+                    for (int64_t i = tid; i < d; i += step) rowq(i, (double)__ldg(xm + i));
                 }
-                const double cf = uf * rf, ct = ut * rt;
-                acc[0] = __fma_rn(cf, cf, acc[0]);
-                acc[1] = __fma_rn(ct, ct, acc[1]);
+                block_sum<MAXQ>(dq, red);
+                if (tid == 0) dq_cycles += clock64() - ta0;
+                bool wide = false;
+                if (tid < 2 * nact) {
+                    const int qa = tid >> 1, which = tid & 1, q = q0 + qa;
+                    const int k = which ? pt : pf;
+                    double dqm = 0.0;
 #pragma unroll
-                for (int q = 0; q < MAXQ; ++q)
-                    if (q < nact) {
-                        const double xq = colv(jown, q0 + q, i);
-                        acc[2 + 2 * q] = __fma_rn(xq, cf, acc[2 + 2 * q]);
-                        acc[3 + 2 * q] = __fma_rn(xq, ct, acc[3 + 2 * q]);
+                    for (int e = 0; e < MAXQ; ++e)
+                        if (e == qa) dqm = dq[e];
+                    // D_xm interval (positive-term chain): [dqm(1−γ), dqm(1+2γ)]
+                    const double dlo = dqm * (1.0 - 1.01 * a.gam), dhi = dqm * (1.0 + 2.02 * a.gam);
+                    const double om = As[q * c + k], oe = Es[q * c + k];
+                    const double lo = fmax(om - oe, 0.0), hi = om + oe;
+                    // identities in round-to-nearest with reciprocal multiplies;
+                    // every term is ≥ 0, so 16u of their magnitude sum covers the
+                    // roundings (≤ 8 operations per chain)
+                    double flo, fhi, nn, dn;
+                    if (!which) {  // from: n = pnf, n−1 = na1
+                        nn = dcf;
+                        dn = na1;
+                        const double r1 = 1.0 / dn, r2 = r1 * r1;
+                        const double m1 = fmax(mf - ef, 0.0), m2 = mf + ef;
+                        flo = (nn * lo - dhi) * r1 + nn * m1 * r2;
+                        fhi = (nn * hi - dlo) * r1 + nn * m2 * r2;
+                        const double sl = 16.0 * kU * ((nn * hi + dhi) * r1 + nn * m2 * r2);
+                        flo -= sl;
+                        fhi += sl;
+                    } else {  // to: n = pnt, n+1 = nb1
+                        nn = dct;
+                        dn = nb1;
+                        const double r1 = 1.0 / dn, r2 = r1 * r1;
+                        const double m1 = fmax(mt - et, 0.0), m2 = mt + et;
+                        flo = (nn * lo + dlo) * r1 - nn * m2 * r2;
+                        fhi = (nn * hi + dhi) * r1 - nn * m1 * r2;
+                        const double sl = 16.0 * kU * ((nn * hi + dhi) * r1 + nn * m2 * r2);
+                        flo -= sl;
+                        fhi += sl;
                     }
-            };
-            const int64_t step = blockDim.x;
-            if (sizeof(T) == 8 && (d & 1) == 0) {
-                // 16-byte loads, 4 in flight per array per thread
-                const double2* x2 = reinterpret_cast<const double2*>(xm);
-                const double2* f2 = reinterpret_cast<const double2*>(of);
-                const double2* t2 = reinterpret_cast<const double2*>(ot);
-                const int64_t dh = d >> 1;
-                int64_t i = tid;
-                for (; i + 3 * step < dh; i += 4 * step) {
-                    double2 xv[4], fv[4], tv[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        xv[u] = __ldg(x2 + i + u * step);
-                        fv[u] = __ldcg(f2 + i + u * step);
-                        tv[u] = __ldcg(t2 + i + u * step);
-                    }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        row(2 * (i + u * step), xv[u].x, fv[u].x, tv[u].x);
-                        row(2 * (i + u * step) + 1, xv[u].y, fv[u].y, tv[u].y);
-                    }
+                    flo = fmax(flo, 0.0);
+                    // stored centroid vs the exact update: |δ_i| ≤ 3u(n|c_i| + |x_i|)/dn
+                    const double del = 3.03 * kU * (nn * sqrt(fabs(ccs[k])) + sqrt(fabs(xxm))) / dn;
+                    const double sh = sqrt(fmax(fhi, 0.0));
+                    const double rlo = fmax(flo - 2.0 * sh * del * 1.01, 0.0);
+                    const double rhi = fhi + (2.0 * sh * del + del * del) * 1.01;
+                    // union with the reference's chain value
+                    const double ulo = rlo * (1.0 - 1.01 * a.gam), uhi = rhi * (1.0 + 1.01 * a.gam);
+                    nmid = 0.5 * (ulo + uhi);
+                    ne = (0.5 * (uhi - ulo)) * (1.0 + 8.0 * kU) + 4.0 * kU * uhi;
+                    const double fresh = screen_err(a.kappa_d, sqrt(fabs(s_xx[q])), sqrt(fabs(ccs[k])), nmid);
+                    wide = !(isfinite(nmid) && isfinite(ne) && ne <= 64.0 * fresh);
                 }
-                for (; i < dh; i += step) {
-                    const double2 xv = __ldg(x2 + i), fv = __ldcg(f2 + i), tv = __ldcg(t2 + i);
-                    row(2 * i, xv.x, fv.x, tv.x);
-                    row(2 * i + 1, xv.y, fv.y, tv.y);
+                redo = __syncthreads_or(wide) != 0;
+                if (tid == 0) {
+                    act_cycles += clock64() - ta0;
+                    ++act_rounds;
+                }
+            }
+            if (!redo) {
+                if (tid < 2 * nact) {
+                    const int qa = tid >> 1, which = tid & 1, q = q0 + qa;
+                    const int k = which ? pt : pf;
+                    As[q * c + k] = nmid;
+                    Es[q * c + k] = ne;
                 }
             } else {
-                int64_t i = tid;
-                for (; i + 3 * step < d; i += 4 * step) {
-                    double xv[4], fv[4], tv[4];
+                // recompute from the new values over all rows (reciprocal multiply
+                // inside the bound, kappa_d)
+                const double rf = 1.0 / na1, rt = 1.0 / nb1;
+                double acc[2 + 2 * MAXQ];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        xv[u] = (double)__ldg(xm + i + u * step);
-                        fv[u] = __ldcg(of + i + u * step);
-                        tv[u] = __ldcg(ot + i + u * step);
-                    }
+                for (int e = 0; e < 2 + 2 * MAXQ; ++e) acc[e] = 0.0;
+                for (int64_t i = tid; i < d; i += blockDim.x) {
+                    const double x = (double)__ldg(xm + i);
+                    const double cf = (__ldcg(of + i) * dcf - x) * rf, ct = (__ldcg(ot + i) * dct + x) * rt;
+                    acc[0] = __fma_rn(cf, cf, acc[0]);
+                    acc[1] = __fma_rn(ct, ct, acc[1]);
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) row(i + u * step, xv[u], fv[u], tv[u]);
+                    for (int q = 0; q < MAXQ; ++q)
+                        if (q < nact) {
+                            const double xq = colv(jown, q0 + q, i);
+                            acc[2 + 2 * q] = __fma_rn(xq, cf, acc[2 + 2 * q]);
+                            acc[3 + 2 * q] = __fma_rn(xq, ct, acc[3 + 2 * q]);
+                        }
                 }
-                for (; i < d; i += step) row(i, (double)__ldg(xm + i), __ldcg(of + i), __ldcg(ot + i));
-            }
-            block_sum<2 + 2 * MAXQ>(acc, red);
-            if (tid < 2 * nact) {
-                const int qa = tid >> 1, which = tid & 1, q = q0 + qa;
-                double dot = 0.0;
+                block_sum<2 + 2 * MAXQ>(acc, red);
+                if (tid < 2 * nact) {
+                    const int qa = tid >> 1, which = tid & 1, q = q0 + qa;
+                    double dot = 0.0;
 #pragma unroll
-                for (int e = 0; e < 2 * MAXQ; ++e)
-                    if (e == tid) dot = acc[2 + e];
-                const double cck = which ? acc[1] : acc[0];
-                const double xxj = s_xx[q];
-                const double mid = (xxj + cck) - 2.0 * dot;
-                const double e = screen_err(a.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
-                const int k = which ? pt : pf;
-                As[q * c + k] = mid;
-                Es[q * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+                    for (int e = 0; e < 2 * MAXQ; ++e)
+                        if (e == tid) dot = acc[2 + e];
+                    const double cck = which ? acc[1] : acc[0];
+                    const double xxj = s_xx[q];
+                    const double mid = (xxj + cck) - 2.0 * dot;
+                    const double e = screen_err(a.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
+                    const int k = which ? pt : pf;
+                    As[q * c + k] = mid;
+                    Es[q * c + k] = isfinite(mid) && isfinite(e) ? hart_widen(mid, e, a.gam) : INFINITY;
+                }
+                if (tid == 0) ++redos;
             }
+            __syncthreads();
             if (tid == 0) {
-                ccs[pf] = acc[0];
-                ccs[pt] = acc[1];
+                // ‖c′‖² by the same identities (only the bound's scale uses it
+                // between block entries, which recompute it from the slices)
+                ccs[pf] = fmax((dcf * ccs[pf] - xxm) / na1 + dcf * mf / (na1 * na1), 0.0);
+                ccs[pt] = fmax((dct * ccs[pt] + xxm) / nb1 - dct * mt / (nb1 * nb1), 0.0);
                 vs[pf] ^= 1;  // this CTA's slices of the new values are stored
                 vs[pt] ^= 1;
             }
@@ -596,13 +713,21 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                 {
                     const int nwt = ((nb + 15) >> 4) * ((nstale + 15) >> 4), nw = (int)(blockDim.x >> 5);
                     if (nwt <= nw)
-                        hart_entry_dmma<T, 1>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub);
+                        hart_entry_dmma<T, 1>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub, ccacc);
                     else
-                        hart_entry_dmma<T, 2>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub);
+                        hart_entry_dmma<T, 2>(M, a, vs, stale, nstale, b0, nb, s0, s1, R, stc, sce, tsub, ccacc);
                 }
                 lap(1);
                 grid_barrier(hg);
                 lap(2);
+                // ---- ‖c‖² of the stale centroids (slice partials, fixed order)
+                for (int t = warp; t < nstale; t += nwarps) {
+                    double v = 0.0;
+                    for (int g2 = lane; g2 < G; g2 += 32) v += __ldcg(a.ccp + (size_t)t * G + g2);
+                    v = warp_sum(v);
+                    if (lane == 0) ccs[stale[t]] = v;
+                }
+                __syncthreads();
                 // ---- owned columns: the G slice partials (contiguous) in fixed
                 //      order; two pairs per warp in flight
                 const int npairs = nown * nstale;
@@ -615,8 +740,8 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                         const double* base = a.part + ((size_t)(jown - b0 + q) * c + t) * G;
 #pragma unroll
                         for (int u = 0; u < HART_MAXG / 32; ++u) {
-                            const int g = lane + 32 * u;
-                            v[m][u] = (p < npairs && g < G) ? __ldcg(base + g) : 0.0;
+                            const int g2 = lane + 32 * u;
+                            v[m][u] = (p < npairs && g2 < G) ? __ldcg(base + g2) : 0.0;
                         }
                     }
 #pragma unroll
@@ -633,7 +758,7 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                             const double mid = (xxj + cck) - 2.0 * sdot;
                             const double e = screen_err(a.kappa_d, sqrt(fabs(xxj)), sqrt(fabs(cck)), mid);
                             As[q * c + k] = mid;
-                            Es[q * c + k] = isfinite(mid) && isfinite(e) ? e : INFINITY;
+                            Es[q * c + k] = isfinite(mid) && isfinite(e) ? hart_widen(mid, e, a.gam) : INFINITY;
                             ++refreshed;
                         }
                     }
@@ -662,7 +787,17 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                     hi = mid + e;
                 };
                 const int st = hart_decide_warp_w(from, c, cnt, wa, wb, iv, to);
-                if (st != 0 && lane == 0) atomicMin(&hg->first[r % 3][0], pack4(j, st, from, to));
+                if (st != 0 && lane == 0) {
+                    // this column's intervals to its from / to centroid, for the
+                    // identities of phase 1 should it be the elected move
+                    double* cd = a.cand + 4 * (int64_t)j;
+                    __stcg(cd, As[warp * c + from]);
+                    __stcg(cd + 1, Es[warp * c + from]);
+                    __stcg(cd + 2, to >= 0 ? As[warp * c + to] : 0.0);
+                    __stcg(cd + 3, to >= 0 ? Es[warp * c + to] : INFINITY);
+                    __threadfence();
+                    atomicMin(&hg->first[r % 3][0], pack4(j, st, from, to));
+                }
                 if (a.diag && st == 0 && cnt[from] > 1) {
                     // diagnostics: relative margin of a "no move" decision
                     double mn = INFINITY;
@@ -721,6 +856,14 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                         };
                         const int s2 = hart_decide_warp_w(from, c, cnt, wa, wb, iv, t2);
                         if (lane == 0) {
+                            if (s2 == 1) {  // the reference's own values (chain): ± γ covers the real ones
+                                const double vf = __ldcg(a.scratch + from), vt = __ldcg(a.scratch + t2);
+                                double* cd = a.cand + 4 * (int64_t)j;
+                                __stcg(cd, vf);
+                                __stcg(cd + 1, hart_widen(vf, 0.0, a.gam));
+                                __stcg(cd + 2, vt);
+                                __stcg(cd + 3, hart_widen(vt, 0.0, a.gam));
+                            }
                             hg->xres = pack4(j, s2, from, t2);
                             hg->exact_fallbacks += 1;
                         }
@@ -777,6 +920,10 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
             hg->t_cols = t_cols;
             hg->stale_sum = stale_sum;
             hg->heavy_blocks = heavy;
+            hg->redos = redos;
+            hg->act_cycles = act_cycles;
+            hg->act_rounds = act_rounds;
+            hg->dq_cycles = dq_cycles;
             for (int q = 0; q < 8; ++q) hg->tm[q] = tm[q];
             hg->tm[6] = tsub[0]; hg->tsub1 = tsub[1]; hg->tsub2 = tsub[2];
         }

@@ -343,7 +343,7 @@ struct KMeansEngine {
     // (hartigan.cuh): ONE persistent cooperative launch for every pass; the
     // start intervals come from one full screen, later ones from the kernel's
     // lazy per-entry refresh.
-    DBuf<double> hA, hE, hxx, hC2, hpart;
+    DBuf<double> hA, hE, hxx, hC2, hpart, hcand, hccp;
     DBuf<int> hver, hebuf;
     DBuf<HartGlobal> hglob;
     int hart_ctas = 0;  // CTAs of the Hartigan kernel (0: one per SM)
@@ -364,7 +364,7 @@ struct KMeansEngine {
                                          (size_t)(((B + 15) & ~15) + ((c + 15) & ~15))
                                    : 0;
         return (cache ? (size_t)cpb * d * sizeof(T) + 16 : 0) + sizeof(double) * 2 * (size_t)cpb * c +
-               sizeof(double) * (3 * (size_t)c + HART_RED) + stage + sizeof(int) * 4 * (size_t)c + 2048;
+               sizeof(double) * (4 * (size_t)c + HART_RED) + stage + sizeof(int) * 4 * (size_t)c + 2048;
     }
     HartGeom hart_geometry() const {
         int dev = 0, nsm = 148, optin = 0;
@@ -406,6 +406,8 @@ struct KMeansEngine {
         hver.ensure(c);
         hebuf.ensure(ceil_div(n, g.B));
         hpart.ensure((size_t)g.G * g.B * c);
+        hcand.ensure((size_t)4 * n);
+        hccp.ensure((size_t)g.G * c);
         hglob.ensure(1);
         scratch.ensure(std::max(c, 64));
         hst.ensure<HartGlobal>(1);
@@ -426,7 +428,8 @@ struct KMeansEngine {
         k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
         // start intervals: one screen of every column against the start centroids
         screen_cols(M, n, hC2.p, nullptr);
-        k_hart_fill<<<ceil_div((int64_t)n * c, 256), 256, 0, st>>>(screen_view(), hA.p, hE.p, hxx.p, n, c);
+        const double gam = ((double)d + 3.0) * kU * 1.02;
+        k_hart_fill<<<ceil_div((int64_t)n * c, 256), 256, 0, st>>>(screen_view(), hA.p, hE.p, hxx.p, n, c, gam);
         ln.add(2);
         const int G = hgm.G, cpb = hgm.cpb;
         const bool cache = hgm.cache;
@@ -449,6 +452,9 @@ struct KMeansEngine {
         a.xx = hxx.p;
         a.cc0 = cc.p;
         a.scratch = scratch.p;
+        a.cand = hcand.p;
+        a.ccp = hccp.p;
+        a.gam = gam;
         a.d = d;
         a.n = n;
         a.c = c;
@@ -478,12 +484,12 @@ struct KMeansEngine {
             if (trace_on())
                 std::fprintf(stderr,
                              "[respca] hartigan: G=%d cpb=%d R=%d %llu passes %llu blocks %llu rounds %llu moves "
-                             "%llu refreshed, kernel %.3fs (block entries %.3fs; CTA0 stale/entry %.2f, heavy %llu)\n",
+                             "%llu refreshed, kernel %.3fs (block entries %.3fs; CTA0 stale/entry %.2f, heavy %llu, redo rounds %llu)\n",
                              G, cpb, hgm.R, (unsigned long long)hh->passes, (unsigned long long)hh->blocks,
                              (unsigned long long)hh->rounds, (unsigned long long)hh->moves,
                              (unsigned long long)hh->refreshed, 1e-9 * hh->t_kernel, 1e-9 * hh->t_load,
                              (double)hh->stale_sum / (double)std::max<uint64_t>(1, hh->blocks),
-                             (unsigned long long)hh->heavy_blocks);
+                             (unsigned long long)hh->heavy_blocks, (unsigned long long)hh->redos);
             if (trace_on())
                 std::fprintf(stderr,
                              "[respca] hartigan CTA0 phases (s at 1.965 GHz): update %.3f entry-tiles %.3f entry-barrier %.3f "
@@ -491,6 +497,11 @@ struct KMeansEngine {
                              hh->tm[0] / 1.965e9, hh->tm[1] / 1.965e9, hh->tm[2] / 1.965e9, hh->tm[3] / 1.965e9,
                              hh->tm[4] / 1.965e9, hh->tm[5] / 1.965e9, hh->tm[7] / 1.965e9, hh->tm[6] / 1.965e9,
                              hh->tsub1 / 1.965e9, hh->tsub2 / 1.965e9);
+            if (trace_on())
+                std::fprintf(stderr, "[respca] hartigan CTA0 active rounds %llu: phase-1 %.2f us (x_m pass + sum %.2f us)\n",
+                             (unsigned long long)hh->act_rounds,
+                             hh->act_cycles / 1965.0 / std::max<double>(1.0, (double)hh->act_rounds),
+                             hh->dq_cycles / 1965.0 / std::max<double>(1.0, (double)hh->act_rounds));
             if (trace_on() && env_int("RESPCA_HART_DIAG", 0))
                 std::fprintf(stderr,
                              "[respca] hartigan no-move margins / (|x|+|c|)^2 below 1e-1..1e-8: %llu %llu %llu %llu %llu %llu %llu %llu of %llu\n",
