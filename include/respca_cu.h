@@ -31,7 +31,8 @@ enum {
     RESPCA_ERUNTIME = 2,  /* std::runtime_error ("kmeans: cannot repair empty cluster", kmeans.cpp:58) */
     RESPCA_ENOMEM = 3,    /* device allocation failed */
     RESPCA_ECUDA = 4,     /* CUDA runtime / driver error, or no usable sm_100 device */
-    RESPCA_ENONFINITE = 5 /* a non-finite value appeared inside the loop (device flag) */
+    RESPCA_ENONFINITE = 5,/* a non-finite value appeared inside the loop (device flag) */
+    RESPCA_EIO = 6        /* respca::io::IoError family (io.hpp:13-33): open / magic / truncation */
 };
 
 enum { RESPCA_F64 = 0, RESPCA_F32 = 1 };    /* storage type of X, L, S, Θ */
@@ -171,6 +172,31 @@ int respca_cu_bench_prepare(respca_cu_ctx* ctx, const void* x, uint64_t d, uint6
  * number of slow-path iterations through *slow. */
 int respca_cu_bench_steps(respca_cu_ctx* ctx, uint64_t iters, double* ms, double* pass_f_ms,
                           double* pass_a_ms, uint64_t* slow);
+
+/* ---- file I/O straight to / from HBM, outlier scores ------- */
+
+/* RESPCA1 binary header (io.hpp:66-69: magic "RESPCA1\0", u64le rows, u64le
+ * cols, then rows*cols f64le column-major).  Host only (no GPU needed);
+ * RESPCA_EIO with the reference's message on a missing file, bad magic, short
+ * header or a payload shorter than rows*cols doubles (io.cpp:138-153). */
+int respca_cu_binary_info(const char* path, uint64_t* rows, uint64_t* cols, char* err,
+                          size_t err_len);
+
+/* solve() on a RESPCA1 file: the payload streams from disk into HBM through
+ * two pinned chunks (the read of chunk k+1 overlaps the copy of chunk k; fp32
+ * mode converts on the device), and L / S stream back out as RESPCA1 files
+ * (device→host copy of chunk k+1 overlaps the write of chunk k).  l_path /
+ * s_path may be NULL (not written).  d, n are taken from the file. */
+int respca_cu_solve_file(respca_cu_ctx* ctx, const char* x_path, int dtype,
+                         const respca_cu_config* cfg, const char* l_path, const char* s_path,
+                         uint64_t* labels_out, uint64_t labels_cap, respca_cu_report* rep);
+
+/* io::outlier_scores (io.cpp:296-306): scores[j] = ‖S_j‖₂ (column_l2_norms
+ * order, matrix.cpp:117-125), flagged = ascending j with scores[j] >= threshold
+ * (*n_flagged entries of `flagged`, capacity n).  threshold < 0 → EINVAL. */
+int respca_cu_outlier_scores(respca_cu_ctx* ctx, const double* s, uint64_t d, uint64_t n,
+                             double threshold, double* scores, uint64_t* flagged,
+                             uint64_t* n_flagged);
 
 #ifdef __cplusplus
 }

@@ -292,5 +292,66 @@ def reference() -> Checker:
     return _cache["ref"]
 
 
+class RefIO:
+    """The unmodified reference's RESPCA1 reader/writer and outlier scores
+    (io.cpp:138-164, 296-306) through oracle/ref_io_shim.cpp."""
+
+    def __init__(self, path: Path):
+        self.lib = C.CDLL(str(path))
+        vp, cp = C.c_void_p, C.c_char_p
+        self.lib.ref_write_binary.argtypes = [cp, vp, u64, u64, cp, C.c_size_t]
+        self.lib.ref_read_binary.argtypes = [cp, vp, u64, C.POINTER(u64), C.POINTER(u64), cp,
+                                             C.c_size_t]
+        self.lib.ref_outlier_scores.argtypes = [vp, u64, u64, C.c_double, vp, vp, C.POINTER(u64),
+                                                cp, C.c_size_t]
+
+    @staticmethod
+    def _raise(rc, err):
+        msg = err.value.decode()
+        if rc == 1:
+            raise OSError(msg)  # io::IoError
+        raise ValueError(msg)
+
+    def write_binary(self, path, m):
+        a = np.asfortranarray(np.asarray(m, dtype=np.float64))
+        err = C.create_string_buffer(512)
+        rc = self.lib.ref_write_binary(str(path).encode(), a.ctypes.data, a.shape[0], a.shape[1],
+                                       err, 512)
+        if rc:
+            self._raise(rc, err)
+
+    def read_binary(self, path, cap: int = 1 << 26):
+        out = np.empty(cap)
+        r, c = u64(), u64()
+        err = C.create_string_buffer(512)
+        rc = self.lib.ref_read_binary(str(path).encode(), out.ctypes.data, cap, C.byref(r),
+                                      C.byref(c), err, 512)
+        if rc:
+            self._raise(rc, err)
+        n = r.value * c.value
+        return np.asfortranarray(out[:n].reshape((r.value, c.value), order="F"))
+
+    def outlier_scores(self, s, threshold):
+        a = np.asfortranarray(np.asarray(s, dtype=np.float64))
+        d, n = a.shape
+        sc, fl, nf = np.empty(n), np.empty(n, dtype=np.uint64), u64()
+        err = C.create_string_buffer(512)
+        rc = self.lib.ref_outlier_scores(a.ctypes.data, d, n, C.c_double(threshold), sc.ctypes.data,
+                                         fl.ctypes.data, C.byref(nf), err, 512)
+        if rc:
+            self._raise(rc, err)
+        return sc, fl[: nf.value].copy()
+
+
+def reference_io_available() -> bool:
+    return (HERE / "_ref" / "librespca_ref_io.so").exists()
+
+
+def reference_io() -> RefIO:
+    if "refio" not in _cache:
+        _cache["refio"] = RefIO(HERE / "_ref" / "librespca_ref_io.so")
+    return _cache["refio"]
+
+
 def lambda_default(d: int, n: int) -> float:
     return math.sqrt(float(max(d, n)))

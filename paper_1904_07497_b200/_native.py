@@ -12,7 +12,7 @@ from pathlib import Path
 
 LIB_DIR = Path(__file__).resolve().parent / "lib"
 
-RESPCA_OK, RESPCA_EINVAL, RESPCA_ERUNTIME, RESPCA_ENOMEM, RESPCA_ECUDA, RESPCA_ENONFINITE = range(6)
+RESPCA_OK, RESPCA_EINVAL, RESPCA_ERUNTIME, RESPCA_ENOMEM, RESPCA_ECUDA, RESPCA_ENONFINITE, RESPCA_EIO = range(7)
 F64, F32 = 0, 1
 L1, L21 = 0, 1
 
@@ -58,7 +58,8 @@ EXPORTS = [
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
     "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
-    "respca_cu_debug_screen_tc",
+    "respca_cu_debug_screen_tc", "respca_cu_binary_info", "respca_cu_solve_file",
+    "respca_cu_outlier_scores",
 ]
 
 
@@ -109,6 +110,11 @@ def lib() -> C.CDLL:
             L.respca_cu_bench_steps.argtypes = [vp, u64, dptr, dptr, dptr, u64ptr]
             L.respca_cu_debug_screen.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             L.respca_cu_debug_screen_tc.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
+            L.respca_cu_binary_info.argtypes = [C.c_char_p, u64ptr, u64ptr, C.c_char_p, C.c_size_t]
+            L.respca_cu_solve_file.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(CConfig),
+                                               C.c_char_p, C.c_char_p, u64ptr, u64, C.POINTER(CReport)]
+            L.respca_cu_outlier_scores.argtypes = [vp, dptr, u64, u64, C.c_double, dptr, u64ptr,
+                                                   u64ptr]
             _lib = L
         return _lib
 
@@ -170,4 +176,10 @@ def check(ctx: Context, rc: int) -> None:
         raise MemoryError(msg)
     if rc == RESPCA_ENONFINITE:
         raise FloatingPointError(msg)
+    if rc == RESPCA_EIO:
+        raise IoError(msg)  # respca::io::IoError
     raise RuntimeError(f"CUDA error: {msg}")
+
+
+class IoError(OSError):
+    """respca::io::IoError family (io.hpp:13-33): open, magic, truncation."""

@@ -18,6 +18,7 @@
 
 #include "alm.cuh"
 #include "engine.cuh"
+#include "binio.cuh"
 #include "kmeans_engine.cuh"
 #include "km.cuh"
 
@@ -34,6 +35,7 @@ struct respca_cu_ctx {
     std::string err;
     uint64_t launches = 0;
     std::unique_ptr<AlmBase> resident;  // bench-resident solver state
+    StreamBufs io;                       // pinned chunks for file streaming
 };
 
 namespace {
@@ -118,6 +120,13 @@ struct Alm : AlmBase {
 
     // upload + device-side validation (finite, ‖X‖ ≠ 0)  (solver.cpp:128-132)
     void upload(const T* x, uint64_t dd, uint64_t nn, const respca_cu_config& c_) {
+        upload_with(dd, nn, c_, [&](T* dst) {
+            CK(cudaMemcpyAsync(dst, x, sizeof(T) * (size_t)(dd * nn), cudaMemcpyHostToDevice, st));
+        });
+    }
+    // fill(X) writes the d×n input into device memory on `st`
+    template <class Fill>
+    void upload_with(uint64_t dd, uint64_t nn, const respca_cu_config& c_, Fill&& fill) {
         cfg = c_;
         validate_cfg(cfg);
         if (cfg.c > nn) throw InvalidArg("solve: c exceeds column count");
@@ -129,7 +138,7 @@ struct Alm : AlmBase {
         L.ensure(N);
         S.ensure(N);
         Th.ensure(N);
-        CK(cudaMemcpyAsync(X.p, x, sizeof(T) * N, cudaMemcpyHostToDevice, st));
+        fill(X.p);
         const int blocks = std::min<int64_t>(2048, ceil_div(N, 256));
         nrm.ensure(3 * 2048 + 8);
         k_norms<T><<<blocks, 256, 0, st>>>(X.p, N, nrm.p);
@@ -368,6 +377,15 @@ struct Alm : AlmBase {
     }
 
     void download(T* Lo, T* So, uint64_t* lab, respca_cu_report* rep_out) {
+        const int64_t N = d * n;
+        download_with(
+            [&](const T* Ld) { CK(cudaMemcpyAsync(Lo, Ld, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); },
+            [&](const T* Sd) { CK(cudaMemcpyAsync(So, Sd, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); },
+            lab, rep_out);
+    }
+    // sinkL / sinkS read the device L / S (stream-ordered on `st`)
+    template <class SinkL, class SinkS>
+    void download_with(SinkL&& sinkL, SinkS&& sinkS, uint64_t* lab, respca_cu_report* rep_out) {
         const Ctl h = read_ctl();
         if (trace_on())
             std::fprintf(stderr,
@@ -376,9 +394,8 @@ struct Alm : AlmBase {
                          h.iter, h.margin_hist[0], h.margin_hist[1], h.margin_hist[2],
                          h.margin_hist[3], h.margin_hist[4], h.margin_hist[5],
                          (long long)h.iter * n);
-        const int64_t N = d * n;
-        CK(cudaMemcpyAsync(Lo, L.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
-        CK(cudaMemcpyAsync(So, S.p, sizeof(T) * N, cudaMemcpyDeviceToHost, st));
+        sinkL(L.p);
+        sinkS(S.p);
         std::vector<int> hl(n);
         CK(cudaMemcpyAsync(hl.data(), labels.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
         std::vector<double> hr((size_t)h.iter * 4 + 4);
@@ -473,10 +490,11 @@ struct Alm : AlmBase {
     }
 };
 
-template <typename T>
-void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
-                const respca_cu_config& cfg, T* Lo, T* So, uint64_t* lab,
-                respca_cu_report* rep) {
+// solve() with the input coming from `fill(X)` and the outputs going to
+// `sinkL(L)`, `sinkS(S)` (host buffers or streamed files)
+template <typename T, class Fill, class SinkL, class SinkS>
+void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_config& cfg, Fill&& fill,
+                SinkL&& sinkL, SinkS&& sinkS, uint64_t* lab, respca_cu_report* rep) {
     check_dims(d, n);
     validate_cfg(cfg);
     if (cfg.c > n) throw InvalidArg("solve: c exceeds column count");
@@ -484,7 +502,7 @@ void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
     Alm<T> a(ctx);
     Events ev;
     CK(cudaEventRecord(ev.a, ctx->st));
-    a.upload(x, d, n, cfg);
+    a.upload_with(d, n, cfg, fill);
     CK(cudaEventRecord(ev.b, ctx->st));
     CK(cudaEventSynchronize(ev.b));
     const double h2d = ev.ms();
@@ -505,7 +523,7 @@ void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
     const double loop_ms = e3.ms();
     Events e4;
     CK(cudaEventRecord(e4.a, ctx->st));
-    a.download(Lo, So, lab, rep);
+    a.download_with(sinkL, sinkS, lab, rep);
     CK(cudaEventRecord(e4.b, ctx->st));
     CK(cudaEventSynchronize(e4.b));
     if (rep) {
@@ -515,6 +533,39 @@ void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
         rep->d2h_ms = e4.ms();
         rep->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
     }
+}
+
+template <typename T>
+void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
+                const respca_cu_config& cfg, T* Lo, T* So, uint64_t* lab,
+                respca_cu_report* rep) {
+    const size_t N = (size_t)(d * n);
+    cudaStream_t st = ctx->st;
+    solve_core<T>(
+        ctx, d, n, cfg,
+        [&](T* X) { CK(cudaMemcpyAsync(X, x, sizeof(T) * N, cudaMemcpyHostToDevice, st)); },
+        [&](const T* L) { CK(cudaMemcpyAsync(Lo, L, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); },
+        [&](const T* S) { CK(cudaMemcpyAsync(So, S, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); }, lab, rep);
+}
+
+// solve() between RESPCA1 files
+template <typename T>
+void solve_file_impl(respca_cu_ctx* ctx, const char* xp, const respca_cu_config& cfg, const char* lp,
+                     const char* sp, uint64_t* lab, uint64_t lab_cap, respca_cu_report* rep) {
+    BinReader r(xp);
+    const uint64_t d = r.rows, n = r.cols;
+    check_dims(d, n);
+    if (lab_cap < n) throw InvalidArg("respca_cu_solve_file: labels capacity smaller than the column count");
+    cudaStream_t st = ctx->st;
+    solve_core<T>(
+        ctx, d, n, cfg, [&](T* X) { r.to_device<T>(X, (int64_t)(d * n), st, ctx->io, &ctx->launches); },
+        [&](const T* L) {
+            if (lp) write_binary_from_device<T>(lp, L, d, n, st, ctx->io, &ctx->launches);
+        },
+        [&](const T* S) {
+            if (sp) write_binary_from_device<T>(sp, S, d, n, st, ctx->io, &ctx->launches);
+        },
+        lab, rep);
 }
 
 template <class F>
@@ -537,6 +588,9 @@ int guarded(respca_cu_ctx* ctx, F&& f) {
     } catch (const NonFinite& e) {
         ctx->err = e.what();
         return RESPCA_ENONFINITE;
+    } catch (const IoErr& e) {
+        ctx->err = e.what();
+        return RESPCA_EIO;
     } catch (const std::exception& e) {
         ctx->err = e.what();
         return RESPCA_ECUDA;
@@ -1114,6 +1168,64 @@ int respca_cu_column_mean(respca_cu_ctx* ctx, const double* m, uint64_t d, uint6
         km.launch_group_mean(o.p);
         CK(cudaMemcpyAsync(out, o.p, sizeof(double) * d, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+int respca_cu_binary_info(const char* path, uint64_t* rows, uint64_t* cols, char* err, size_t err_len) {
+    try {
+        if (!path || !rows || !cols) throw InvalidArg("respca_cu_binary_info: null pointer");
+        BinReader r(path);
+        *rows = r.rows;
+        *cols = r.cols;
+        if (err && err_len) err[0] = 0;
+        return RESPCA_OK;
+    } catch (const std::exception& e) {
+        if (err && err_len) {
+            std::strncpy(err, e.what(), err_len - 1);
+            err[err_len - 1] = 0;
+        }
+        return dynamic_cast<const IoErr*>(&e) ? RESPCA_EIO : RESPCA_EINVAL;
+    }
+}
+
+int respca_cu_solve_file(respca_cu_ctx* ctx, const char* x_path, int dtype, const respca_cu_config* cfg,
+                         const char* l_path, const char* s_path, uint64_t* labels_out, uint64_t labels_cap,
+                         respca_cu_report* rep) {
+    return guarded(ctx, [&] {
+        if (!x_path || !cfg || !labels_out) throw InvalidArg("respca_cu_solve_file: null pointer");
+        if (cfg->sparse_norm != RESPCA_L1 && cfg->sparse_norm != RESPCA_L21)
+            throw InvalidArg("respca_cu_solve_file: unknown sparse_norm");
+        if (dtype == RESPCA_F64)
+            solve_file_impl<double>(ctx, x_path, *cfg, l_path, s_path, labels_out, labels_cap, rep);
+        else if (dtype == RESPCA_F32)
+            solve_file_impl<float>(ctx, x_path, *cfg, l_path, s_path, labels_out, labels_cap, rep);
+        else
+            throw InvalidArg("respca_cu_solve_file: unknown dtype");
+    });
+}
+
+int respca_cu_outlier_scores(respca_cu_ctx* ctx, const double* s, uint64_t d, uint64_t n, double threshold,
+                             double* scores, uint64_t* flagged, uint64_t* n_flagged) {
+    return guarded(ctx, [&] {  // io.cpp:296-306
+        if (!s || !scores) throw InvalidArg("respca_cu_outlier_scores: null pointer");
+        if (threshold < 0.0) throw InvalidArg("outlier_scores: negative threshold");
+        check_dims(d, n);
+        cudaStream_t st = ctx->st;
+        Dev64 dm;
+        const double* p = dm.up(st, s, d * n);
+        DBuf<double> nr;
+        nr.ensure(n);
+        k_col_sumsq<double, 0><<<ceil_div(n, 128), 128, 0, st>>>(p, nullptr, nullptr, 1.0, d, n, nr.p);
+        ctx->launches++;
+        CK(cudaMemcpyAsync(scores, nr.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        uint64_t m = 0;
+        for (uint64_t j = 0; j < n; ++j)
+            if (scores[j] >= threshold) {
+                if (flagged) flagged[m] = j;
+                ++m;
+            }
+        if (n_flagged) *n_flagged = m;
     });
 }
 

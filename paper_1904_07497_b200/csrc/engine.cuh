@@ -27,6 +27,10 @@ struct NoMem : std::runtime_error {
 struct NonFinite : std::runtime_error {
     using std::runtime_error::runtime_error;
 };
+// io::IoError and its subclasses (io.hpp:13-33): file open/format/size errors
+struct IoErr : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
 
 inline void ck(cudaError_t e, const char* what) {
     if (e == cudaSuccess) return;

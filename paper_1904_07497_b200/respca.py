@@ -178,6 +178,93 @@ def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
                                int(rep.exact_fallbacks))
 
 
+def _result(L, S, lab, arrs, rep) -> DecompositionResult:
+    it = int(rep.iters)
+    report = ConvergenceReport(arrs[0][:it].copy(), arrs[1][:it].copy(), arrs[2][:it].copy(),
+                               arrs[3][:it].copy(), bool(rep.converged), it)
+    return DecompositionResult(L, S, lab, report, float(rep.wall_time), float(rep.lambda_),
+                               float(rep.init_ms), float(rep.loop_ms), float(rep.h2d_ms),
+                               float(rep.d2h_ms), int(rep.slow_iters), int(rep.hartigan_moves),
+                               int(rep.exact_fallbacks))
+
+
+def binary_info(path) -> tuple[int, int]:
+    """Rows and columns of a RESPCA1 file (io.hpp:66-69), validated like
+    read_binary_matrix (io.cpp:138-153).  No GPU needed."""
+    r, c = C.c_uint64(), C.c_uint64()
+    err = C.create_string_buffer(512)
+    rc = N.lib().respca_cu_binary_info(str(path).encode(), C.byref(r), C.byref(c), err, 512)
+    if rc == N.RESPCA_EIO:
+        raise N.IoError(err.value.decode())
+    if rc != N.RESPCA_OK:
+        raise ValueError(err.value.decode())
+    return int(r.value), int(c.value)
+
+
+def solve_file(x_path, cfg: Optional[SolverConfig] = None, l_path=None, s_path=None,
+               precision: str = "f64", ctx: Optional[N.Context] = None) -> DecompositionResult:
+    """solve() between RESPCA1 files, streamed disk → HBM → disk in pinned
+    chunks.  The result carries no L/S arrays (None):
+    they are in `l_path` / `s_path` when given."""
+    cfg = cfg or SolverConfig()
+    ctx = _ctx(ctx)
+    d, n = binary_info(x_path)
+    budget = cfg.fixed_iters if cfg.fixed_iters is not None else cfg.max_iter
+    budget = max(int(budget), 1)
+    lab = np.empty(n, dtype=np.uint64)
+    arrs = [np.zeros(budget) for _ in range(4)]
+    rep = N.CReport()
+    rep.feas, rep.delta_l, rep.delta_s, rep.objective = (_dp(a) for a in arrs)
+    cc = cfg.to_c()
+    enc = (lambda p: None if p is None else str(p).encode())
+    rc = N.lib().respca_cu_solve_file(ctx.handle, str(x_path).encode(),
+                                      N.F32 if precision == "f32" else N.F64, C.byref(cc),
+                                      enc(l_path), enc(s_path), _up(lab), n, C.byref(rep))
+    N.check(ctx, rc)
+    return _result(None, None, lab, arrs, rep)
+
+
+class OutlierScores:
+    """io::OutlierScores (io.hpp:100-103)."""
+
+    def __init__(self, scores: np.ndarray, flagged: np.ndarray):
+        self.scores = scores
+        self.flagged = flagged
+
+
+def outlier_scores(s, threshold: float, ctx=None) -> OutlierScores:
+    """io::outlier_scores (io.cpp:296-306): column ℓ2 norms of S (the
+    reference's sequential order) and the columns at or above `threshold`."""
+    ctx = _ctx(ctx)
+    sm = _mat(s)
+    d, n = sm.shape
+    sc = np.empty(n)
+    fl = np.empty(n, dtype=np.uint64)
+    nf = C.c_uint64()
+    N.check(ctx, N.lib().respca_cu_outlier_scores(ctx.handle, _dp(sm), d, n, float(threshold),
+                                                 _dp(sc), _up(fl), C.byref(nf)))
+    return OutlierScores(sc, fl[: nf.value].copy())
+
+
+def write_binary_matrix(path, m) -> None:
+    """RESPCA1 writer (io.cpp:156-164): magic, u64le rows, u64le cols, f64le
+    column-major payload.  Host-side helper (tests, tools)."""
+    a = np.asfortranarray(np.asarray(m, dtype=np.float64))
+    with open(path, "wb") as f:
+        f.write(b"RESPCA1\0")
+        f.write(np.array(a.shape, dtype="<u8").tobytes())
+        f.write(a.astype("<f8").tobytes(order="F"))
+
+
+def read_binary_matrix(path) -> np.ndarray:
+    """RESPCA1 reader with the reference's checks (io.cpp:138-153)."""
+    d, n = binary_info(path)
+    with open(path, "rb") as f:
+        f.seek(24)
+        a = np.fromfile(f, dtype="<f8", count=d * n)
+    return np.asfortranarray(a.reshape((d, n), order="F"))
+
+
 def l_update(D, labels, c: int, lambda_: float, rho: float, ctx=None) -> np.ndarray:
     ctx = _ctx(ctx)
     Dm = _mat(D)
