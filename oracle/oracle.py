@@ -331,6 +331,20 @@ class RefIO:
         n = r.value * c.value
         return np.asfortranarray(out[:n].reshape((r.value, c.value), order="F"))
 
+    def synth(self, d, n, c, sparsity=0.05, magnitude=1.0, sigma=0.0, seed=0):
+        """io::synth_generate → (x, l0, s0, labels)."""
+        f = self.lib.ref_synth
+        f.argtypes = [u64, u64, u64, C.c_double, C.c_double, C.c_double, u64, C.c_void_p,
+                      C.c_void_p, C.c_void_p, C.c_void_p, C.c_char_p, C.c_size_t]
+        x, l0, s0 = (np.empty((d, n), order="F") for _ in range(3))
+        lab = np.empty(n, dtype=np.uint64)
+        err = C.create_string_buffer(512)
+        rc = f(d, n, c, sparsity, magnitude, sigma, seed, x.ctypes.data, l0.ctypes.data,
+               s0.ctypes.data, lab.ctypes.data, err, 512)
+        if rc:
+            self._raise(rc, err)
+        return x, l0, s0, lab
+
     def outlier_scores(self, s, threshold):
         a = np.asfortranarray(np.asarray(s, dtype=np.float64))
         d, n = a.shape

@@ -72,4 +72,27 @@ int ref_outlier_scores(const double* s, uint64_t d, uint64_t n, double threshold
     }
 }
 
+int ref_synth(uint64_t d, uint64_t n, uint64_t c, double sparsity, double magnitude, double sigma,
+              uint64_t seed, double* x, double* l0, double* s0, uint64_t* labels, char* err, size_t len) {
+    try {  // io::synth_generate (io.cpp:232-294)
+        respca::io::SynthSpec spec;
+        spec.d = d;
+        spec.n = n;
+        spec.c = c;
+        spec.sparsity = sparsity;
+        spec.magnitude = magnitude;
+        spec.noise_sigma = sigma;
+        spec.seed = seed;
+        const auto data = respca::io::synth_generate(spec);
+        std::memcpy(x, data.x.data().data(), sizeof(double) * d * n);
+        std::memcpy(l0, data.l0.data().data(), sizeof(double) * d * n);
+        std::memcpy(s0, data.s0.data().data(), sizeof(double) * d * n);
+        for (uint64_t j = 0; j < n; ++j) labels[j] = data.assignment.label(j);
+        return 0;
+    } catch (const std::exception& e) {
+        put_err(err, len, e.what());
+        return 2;
+    }
+}
+
 }  // extern "C"

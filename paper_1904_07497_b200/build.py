@@ -80,6 +80,19 @@ def build_dropin(force: bool = False) -> Path:
     return out
 
 
+def build_cli(force: bool = False) -> Path:
+    """respca_b200: the reference command-line tool on the C-ABI."""
+    LIB.mkdir(exist_ok=True)
+    out = LIB / "respca_b200"
+    src = ROOT / "paper_1904_07497_b200" / "tools" / "respca_cli.cpp"
+    deps = [src, INC / "respca_cu.h", LIB / "librespca_cu.so"]
+    if force or _stale(out, deps):
+        cxx = os.environ.get("CXX", "g++")
+        _run([cxx, "-std=gnu++20", "-O2", f"-I{INC}", str(src), "-o", str(out), f"-L{LIB}",
+              "-lrespca_cu", "-Wl,-rpath,$ORIGIN"])
+    return out
+
+
 def build_oracle() -> None:
     """CPU checkers (test infrastructure): oracle/liboracle.so always; the
     reference library oracle/_ref/ only where /root/reference exists."""
@@ -92,6 +105,7 @@ def build_all(force: bool = False) -> None:
     build_synth(force)
     build_cuda(force)
     build_dropin(force)
+    build_cli(force)
     build_oracle()
 
 
