@@ -16,6 +16,8 @@
 // R=2 doubles).
 #pragma once
 
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 
 namespace respca_dev {
@@ -119,7 +121,10 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
     // buf[parity], G_{t+1} written to buf[1 - parity] (never the same one)
     const double* G0, const double* G1, double* Gn0, double* Gn1, double* __restrict__ Cw,
     const double* __restrict__ mean_w, const Ctl* __restrict__ ctl,
-    double* __restrict__ partials, int64_t d, int rowblocks) {
+    double* __restrict__ partials, int64_t d, int rowblocks,
+    // optional BF16 copy of L′ in the K-major [n][dpad] layout the tcgen05
+    // screen loads by TMA (nullptr: not written)
+    __nv_bfloat16* __restrict__ Lb, int64_t dpad) {
     __shared__ double red[32 * 5];
     if (ctl->done) return;  // loop already finished (bench launches ahead)
     const int g = blockIdx.x / rowblocks;
@@ -148,7 +153,7 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
         }
 
         auto body = [&](const Vec<T, R>& xv, const Vec<T, R>& sv, const Vec<T, R>& tv,
-                        const Vec<T, R>& lv, int64_t off) {
+                        const Vec<T, R>& lv, int64_t off, int col) {
             double lo[R], so[R], to[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -179,14 +184,29 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
             Vec<T, R>::store(L + off, lo);
             Vec<T, R>::store(S + off, so);
             Vec<T, R>::store(Th + off, to);
+            if (Lb) {
+                __nv_bfloat16* lb = Lb + (int64_t)col * dpad + i0;
+                if (R == 2) {
+                    __nv_bfloat162 b2;
+                    b2.x = __double2bfloat16(lo[0]);
+                    b2.y = __double2bfloat16(lo[R - 1]);
+                    *reinterpret_cast<__nv_bfloat162*>(lb) = b2;
+                } else {
+                    lb[0] = __double2bfloat16(lo[0]);
+                }
+            }
         };
 
         int t = beg;
         for (; t + U <= end; t += U) {
             Vec<T, R> xv[U], sv[U], tv[U], lv[U];
             int64_t off[U];
+            int mj[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) off[u] = (int64_t)__ldg(members + t + u) * d + i0;
+            for (int u = 0; u < U; ++u) {
+                mj[u] = __ldg(members + t + u);
+                off[u] = (int64_t)mj[u] * d + i0;
+            }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 xv[u].load(X + off[u]);
@@ -195,16 +215,17 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
                 lv[u].load_cs(L + off[u]);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) body(xv[u], sv[u], tv[u], lv[u], off[u]);
+            for (int u = 0; u < U; ++u) body(xv[u], sv[u], tv[u], lv[u], off[u], mj[u]);
         }
         for (; t < end; ++t) {
             Vec<T, R> xv, sv, tv, lv;
-            const int64_t off = (int64_t)__ldg(members + t) * d + i0;
+            const int col = __ldg(members + t);
+            const int64_t off = (int64_t)col * d + i0;
             xv.load(X + off);
             sv.load_cs(S + off);
             tv.load_cs(Th + off);
             lv.load_cs(L + off);
-            body(xv, sv, tv, lv, off);
+            body(xv, sv, tv, lv, off, col);
         }
         const double inv = 1.0 / ng;  // means_of: sum * (1.0 / count), kmeans.cpp:78-79
 #pragma unroll

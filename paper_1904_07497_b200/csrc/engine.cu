@@ -36,6 +36,9 @@ struct respca_cu_ctx {
     uint64_t launches = 0;
     std::unique_ptr<AlmBase> resident;  // bench-resident solver state
     StreamBufs io;                       // pinned chunks for file streaming
+    Arena arena;                         // N-sized solve state reused across solves
+    std::unique_ptr<PoolBase> lanes[2];  // k-means restart lanes (fp64, fp32 storage)
+    std::unique_ptr<PoolBase> engines[2];  // solve()'s k-means engine (fp64, fp32 storage)
 };
 
 namespace {
@@ -93,7 +96,8 @@ struct Alm : AlmBase {
     bool l21 = false;
     DBuf<int> labels, labels_new;
     DBuf<Ctl> ctl;
-    KMeansEngine<T> km;
+    KMeansEngine<T> own_km;  // bench-resident state keeps its own engine
+    KMeansEngine<T>& km;     // solve(): the context's engine (buffers reused)
     WhileGraph wg;
     PlainGraph rest;
     double init_ms = 0.0, xnorm = 0.0;
@@ -101,11 +105,31 @@ struct Alm : AlmBase {
         const char* e = std::getenv("RESPCA_TC_SCREEN");
         return !(e && e[0] == '0');
     }();
+    // Pass F → BF16 L′ → TMA-fed screen (RESPCA_TC_SCREEN=1 keeps the
+    // converting producers, =0 the FP64 DMMA screen)
+    bool use_tma = [] {
+        const char* e = std::getenv("RESPCA_TC_SCREEN");
+        return !(e && (e[0] == '0' || e[0] == '1'));
+    }();
+    bool lb_on = false;
+    int64_t dpad = 0;
+    DBuf<__nv_bfloat16> Lb;
 
-    explicit Alm(respca_cu_ctx* cx) : ctx(cx), st(cx->st), ln{&cx->launches} {
+    bool use_arena = false;  // solve(): borrow the context's arena for X, L, S, Θ, Lb
+
+    static KMeansEngine<T>& shared_engine(respca_cu_ctx* cx) {
+        auto& h = cx->engines[sizeof(T) == 8 ? 0 : 1];
+        if (!h) h.reset(new EngineHolder<T>());
+        return static_cast<EngineHolder<T>*>(h.get())->e;
+    }
+    explicit Alm(respca_cu_ctx* cx, bool shared = false)
+        : ctx(cx), st(cx->st), ln{&cx->launches}, km(shared ? shared_engine(cx) : own_km) {
         km.st = st;
         km.ln = ln;
         km.stats = &stats;
+        auto& pool = ctx->lanes[sizeof(T) == 8 ? 0 : 1];
+        if (!pool) pool.reset(new LanePool<T>());
+        km.lane_pool = static_cast<LanePool<T>*>(pool.get());
     }
 
     Ctl read_ctl() {
@@ -134,10 +158,17 @@ struct Alm : AlmBase {
         n = (int)nn;
         c = (int)cfg.c;
         const int64_t N = d * n;
-        X.ensure(N);
-        L.ensure(N);
-        S.ensure(N);
-        Th.ensure(N);
+        if (use_arena) {
+            X.borrow(ctx->arena.get("X", sizeof(T) * N), N);
+            L.borrow(ctx->arena.get("L", sizeof(T) * N), N);
+            S.borrow(ctx->arena.get("S", sizeof(T) * N), N);
+            Th.borrow(ctx->arena.get("Th", sizeof(T) * N), N);
+        } else {
+            X.ensure(N);
+            L.ensure(N);
+            S.ensure(N);
+            Th.ensure(N);
+        }
         fill(X.p);
         const int blocks = std::min<int64_t>(2048, ceil_div(N, 256));
         nrm.ensure(3 * 2048 + 8);
@@ -169,6 +200,13 @@ struct Alm : AlmBase {
         ctl.ensure(1);
         R = (d % 2 == 0) ? 2 : 1;
         rowblocks = ceil_div(d, 256 * R);
+        dpad = ((d + TC_KB - 1) / TC_KB) * TC_KB;
+        lb_on = use_tc && use_tma && c > 1 && c <= TC_N && cfg.sparse_norm != RESPCA_L21;
+        if (lb_on) {
+            if (use_arena) Lb.borrow(ctx->arena.get("Lb", sizeof(__nv_bfloat16) * (size_t)n * dpad), (size_t)n * dpad);
+            else Lb.ensure((size_t)n * dpad);
+            CK(cudaMemsetAsync(Lb.p, 0, sizeof(__nv_bfloat16) * (size_t)n * dpad, st));  // K padding stays 0
+        }
         nbF = rowblocks * c;
         partials.ensure((size_t)nbF * 5);
         Ctl h{};
@@ -247,16 +285,19 @@ struct Alm : AlmBase {
     // Pass F variants (RESPCA_PASSF, tuning only): members per batch U / min
     // blocks per SM.  Default 4 = U 8, 1 block/SM: 89% of measured HBM peak at C3
     // (U 4: 79%, U 2 with 2 blocks/SM: 87%, U 12/16 spill).
-    int passf_variant = [] {
+    // With the BF16 L′ side output (lb_on) U 2 / 2 blocks per SM is best (876 vs
+    // 826 iterations/s for U 8 / 1 block, which then spills).
+    int passf_variant_env = [] {
         const char* e = std::getenv("RESPCA_PASSF");
-        return e ? std::atoi(e) : 4;
+        return e ? std::atoi(e) : -1;
     }();
     template <int RR, int U, int MB>
     void launch_pf() {
         double* G1 = G.p + (size_t)d * c;
         k_pass_f<T, RR, U, MB><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
                                                     G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
-                                                    partials.p, d, rowblocks);
+                                                    partials.p, d, rowblocks, lb_on ? Lb.p : nullptr,
+                                                    dpad);
     }
     void launch_pass_f() {
         if (l21) {  // ℓ2,1: F1 only (the S/Θ half runs after the column norms)
@@ -273,6 +314,7 @@ struct Alm : AlmBase {
             return;
         }
         if (R == 2) {
+            const int passf_variant = passf_variant_env >= 0 ? passf_variant_env : (lb_on ? 2 : 4);
             switch (passf_variant) {
                 case 1: launch_pf<2, 4, 2>(); break;
                 case 2: launch_pf<2, 2, 2>(); break;
@@ -290,8 +332,9 @@ struct Alm : AlmBase {
     }
     void launch_pass_a() {
         if (c <= 1) return;
-        if (use_tc && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05 BF16 screen
-        else km.screen(Cw.p);                           // FP64 DMMA screen
+        if (lb_on) km.screen_tma(Lb.p, dpad, Cw.p);         // tcgen05, operands by TMA from Pass F's BF16 L′
+        else if (use_tc && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05, fp64 → bf16 producers
+        else km.screen(Cw.p);                               // FP64 DMMA screen
         km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);
         k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
         ln.add();
@@ -499,7 +542,8 @@ void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_conf
     validate_cfg(cfg);
     if (cfg.c > n) throw InvalidArg("solve: c exceeds column count");
     const auto t0 = Clock::now();
-    Alm<T> a(ctx);
+    Alm<T> a(ctx, /*shared=*/true);
+    a.use_arena = true;
     Events ev;
     CK(cudaEventRecord(ev.a, ctx->st));
     a.upload_with(d, n, cfg, fill);
@@ -533,6 +577,9 @@ void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_conf
         rep->d2h_ms = e4.ms();
         rep->wall_time = std::chrono::duration<double>(Clock::now() - t0).count();
     }
+    if (trace_on())
+        std::fprintf(stderr, "[respca] solve: h2d %.1f ms, init %.1f ms, loop %.1f ms, d2h %.1f ms, host wall %.1f ms\n",
+                     h2d, init_ms, loop_ms, e4.ms(), 1e3 * std::chrono::duration<double>(Clock::now() - t0).count());
 }
 
 template <typename T>
@@ -683,6 +730,7 @@ int respca_cu_solve(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, i
         if (!x || !cfg || !L_out || !S_out || !labels_out) throw InvalidArg("respca_cu_solve: null pointer");
         if (cfg->sparse_norm != RESPCA_L1 && cfg->sparse_norm != RESPCA_L21)
             throw InvalidArg("respca_cu_solve: unknown sparse_norm");
+        const auto tw0 = Clock::now();
         if (dtype == RESPCA_F64)
             solve_impl<double>(ctx, (const double*)x, d, n, *cfg, (double*)L_out, (double*)S_out,
                                labels_out, rep);
@@ -691,6 +739,9 @@ int respca_cu_solve(respca_cu_ctx* ctx, const void* x, uint64_t d, uint64_t n, i
                               labels_out, rep);
         else
             throw InvalidArg("respca_cu_solve: unknown dtype");
+        if (trace_on())
+            std::fprintf(stderr, "[respca] respca_cu_solve total %.1f ms (incl. teardown)\n",
+                         1e3 * std::chrono::duration<double>(Clock::now() - tw0).count());
     });
 }
 

@@ -46,28 +46,74 @@ template <class U>
 struct DBuf {
     U* p = nullptr;
     size_t cap = 0;
+    bool owned = true;  // false: memory lent by a context Arena
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() {
-        if (p) cudaFree(p);
+        if (p && owned) cudaFree(p);
     }
     U* ensure(size_t count) {
         if (count == 0) count = 1;
         if (count > cap) {
-            if (p) cudaFree(p);
+            if (p && owned) cudaFree(p);
             p = nullptr;
             cap = 0;
+            owned = true;
             CK(cudaMalloc(&p, count * sizeof(U)));
             cap = count;
         }
         return p;
     }
+    void borrow(void* q, size_t count) {  // arena memory, never freed here
+        if (p && owned) cudaFree(p);
+        p = static_cast<U*>(q);
+        cap = count;
+        owned = false;
+    }
     void release() {
-        if (p) cudaFree(p);
+        if (p && owned) cudaFree(p);
         p = nullptr;
         cap = 0;
     }
+};
+
+// Device memory a context keeps across solves (named slots that only grow):
+// repeated solves skip cudaMalloc/cudaFree of the N-sized state, whose cost
+// (and cudaFree's implicit device synchronisation) is erratic at GB sizes.
+struct Arena {
+    struct Slot {
+        void* p = nullptr;
+        size_t bytes = 0;
+    };
+    std::vector<std::pair<std::string, Slot>> slots;
+    void* get(const std::string& name, size_t bytes) {
+        for (auto& kv : slots)
+            if (kv.first == name) {
+                if (kv.second.bytes < bytes) {
+                    cudaFree(kv.second.p);
+                    kv.second.p = nullptr;
+                    kv.second.bytes = 0;
+                    CK(cudaMalloc(&kv.second.p, bytes));
+                    kv.second.bytes = bytes;
+                }
+                return kv.second.p;
+            }
+        Slot sl;
+        CK(cudaMalloc(&sl.p, bytes));
+        sl.bytes = bytes;
+        slots.emplace_back(name, sl);
+        return sl.p;
+    }
+    ~Arena() {
+        for (auto& kv : slots)
+            if (kv.second.p) cudaFree(kv.second.p);
+    }
+};
+
+// type-erased holder for per-context pools (k-means restart lanes)
+struct PoolBase {
+    virtual ~PoolBase() = default;
 };
 
 // pinned host staging buffer

@@ -70,8 +70,19 @@ inline double since(HClock::time_point t) {
 }
 
 template <typename T>
+struct KmLane;
+// restart lanes kept by a context across solves (streams + buffers)
+template <typename T>
+struct LanePool : PoolBase {
+    std::vector<std::unique_ptr<KmLane<T>>> lanes;
+};
+
+template <typename T>
 struct KMeansEngine {
     cudaStream_t st = nullptr;
+    LanePool<T>* lane_pool = nullptr;  // context-owned lanes (nullptr: per call)
+    // the tcgen05 B operand copy lives with the engine; a tensor map keyed on
+    // (pointer, n, dpad) is rebuilt when any of them changes
     Launch ln{nullptr};
     Stats* stats = nullptr;
     const T* M = nullptr;
@@ -152,6 +163,7 @@ struct KMeansEngine {
         scr_n = nn;
         scr_split = ns;
         tc_mode = false;
+        tma_mode = false;
     }
     void screen(const double* C) { screen_cols(M, n, C); }
     // bound factor of the screen (see km.cuh): γ-bounds of the length-d
@@ -168,6 +180,7 @@ struct KMeansEngine {
         const int64_t d_pad = ((d + TC_KB - 1) / TC_KB) * TC_KB;
         tcCb.ensure((size_t)TC_N * d_pad);
         tcerr.ensure(1);
+        CK(cudaMemsetAsync(tcerr.p, 0, sizeof(int), st));
         k_tc_prep_centroids<<<TC_N, 256, 0, st>>>(C, d, c, d_pad, tcCb.p, cc.p);
         const int tiles = ceil_div(n, TC_M);
         const int64_t total_kb = d_pad / TC_KB;
@@ -185,6 +198,63 @@ struct KMeansEngine {
         scr_n = n;
         scr_split = ns;
         tc_mode = true;
+        tma_mode = false;
+    }
+    // ---- the loop's screen with TMA-fed operands (tc_screen.cuh) -------------
+    bool tma_mode = false;
+    const void* tma_key_a = nullptr;
+    int64_t tma_key_n = -1, tma_key_dpad = -1;
+    CUtensorMap mapA{}, mapB{};
+    static CUtensorMap make_map(const void* base, uint64_t inner, uint64_t outer, uint32_t box_outer) {
+        using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+        static Encode enc = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+            if (!fn || q != cudaDriverEntryPointSuccess) throw CudaErr("cuTensorMapEncodeTiled unavailable");
+            return reinterpret_cast<Encode>(fn);
+        }();
+        CUtensorMap m;
+        const cuuint64_t dims[2] = {inner, outer};
+        const cuuint64_t strides[1] = {inner * 2};
+        const cuuint32_t box[2] = {(cuuint32_t)TC_KB, box_outer};
+        const cuuint32_t es[2] = {1, 1};
+        const CUresult r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box,
+                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) throw CudaErr("cuTensorMapEncodeTiled failed");
+        return m;
+    }
+    // Lb: BF16 columns [n][dpad] written by Pass F; C: FP64 centroids
+    void screen_tma(const __nv_bfloat16* Lbp, int64_t dpad, const double* C) {
+        tcCb.ensure((size_t)TC_N * dpad);
+        tcerr.ensure(1);
+        CK(cudaMemsetAsync(tcerr.p, 0, sizeof(int), st));
+        k_tc_prep_centroids<<<TC_N, 256, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p);
+        if (tma_key_a != (const void*)Lbp || tma_key_n != n || tma_key_dpad != dpad) {
+            mapA = make_map(Lbp, (uint64_t)dpad, (uint64_t)n, TC_M);
+            mapB = make_map(tcCb.p, (uint64_t)dpad, (uint64_t)TC_N, TC_N);
+            tma_key_a = Lbp;
+            tma_key_n = n;
+            tma_key_dpad = dpad;
+        }
+        const int tiles = ceil_div(n, TC_M);
+        const int64_t total_kb = dpad / TC_KB;
+        int ns = (int)std::max<int64_t>(1, std::min<int64_t>(total_kb / 4, (2 * 148) / tiles));
+        ns = std::max(1, std::min(ns, 16));
+        const int kbps = (int)((total_kb + ns - 1) / ns);
+        part.ensure((size_t)ns * n * c);
+        xxp.ensure((size_t)ns * n);
+        CK(cudaFuncSetAttribute(k_screen_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+        k_screen_tma<<<dim3(tiles, ns), TM_THREADS, TC_SMEM, st>>>(mapA, mapB, d, n, c, kbps, part.p, xxp.p,
+                                                                   tcerr.p);
+        ln.add(2);
+        scr_n = n;
+        scr_split = ns;
+        tc_mode = true;
+        tma_mode = true;
     }
     Screen screen_view() const {
         Screen s;
@@ -195,6 +265,7 @@ struct KMeansEngine {
         s.n = scr_n;
         s.c = c;
         s.kappa_d = tc_mode ? tc_bf16_kappa((double)d) + kappa_screen() : kappa_screen();
+        if (tma_mode) s.kappa_d = (s.kappa_d + tma_xx_kappa((double)d)) * 1.01;  // ‖x‖² from BF16 values
         return s;
     }
 
@@ -681,28 +752,20 @@ struct KMeansEngine {
         int dev = 0, nsm = 148;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-        struct Lane {
-            KMeansEngine<T> e;
-            uint64_t launches = 0;
-            Stats st;
-            DBuf<int> wl, bl;
-            DBuf<double> wc, bc;
-            int best_r = -1;
-            double best_in = std::numeric_limits<double>::infinity();
-            uint64_t best_it = 0;
-            ~Lane() {
-                if (e.st) cudaStreamDestroy(e.st);
-            }
-        };
+        using Lane = KmLane<T>;
         const auto t_k0 = HClock::now();
-        std::vector<std::unique_ptr<Lane>> lanes;
+        LanePool<T> local;
+        std::vector<std::unique_ptr<Lane>>& lanes = (lane_pool ? *lane_pool : local).lanes;
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, st));  // M is complete on the caller's stream
-        for (int l = 0; l < L; ++l) {
+        while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
-            Lane& ln_ = *lanes.back();
-            CK(cudaStreamCreateWithFlags(&ln_.e.st, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&lanes.back()->e.st, cudaStreamNonBlocking));
+        }
+        for (int l = 0; l < L; ++l) {
+            Lane& ln_ = *lanes[l];
+            ln_.reset();
             CK(cudaStreamWaitEvent(ln_.e.st, ready, 0));
             ln_.e.ln = Launch{&ln_.launches};
             ln_.e.stats = stats ? &ln_.st : nullptr;
@@ -842,7 +905,8 @@ struct KMeansEngine {
         for (int l = 0; l < L; ++l) threads.emplace_back(body, l);
         for (auto& t : threads) t.join();
         if (trace_on()) std::fprintf(stderr, "[respca] lanes joined at %.3fs\n", since(t_k0));
-        for (auto& lp : lanes) {
+        for (int l = 0; l < L; ++l) {
+            auto& lp = lanes[l];
             *ln.counter += lp->launches;
             if (stats) {
                 const Stats& s2 = lp->st;
@@ -877,6 +941,34 @@ struct KMeansEngine {
         CK(cudaStreamSynchronize(st));
         if (inertia_out) *inertia_out = w.best_in;
         if (iters_out) *iters_out = w.best_it;
+    }
+};
+
+// a context's k-means engine for solve() (buffers reused across solves)
+template <typename T>
+struct EngineHolder : PoolBase {
+    KMeansEngine<T> e;
+};
+
+template <typename T>
+struct KmLane {
+    KMeansEngine<T> e;
+    uint64_t launches = 0;
+    Stats st;
+    DBuf<int> wl, bl;
+    DBuf<double> wc, bc;
+    int best_r = -1;
+    double best_in = std::numeric_limits<double>::infinity();
+    uint64_t best_it = 0;
+    void reset() {
+        launches = 0;
+        st = Stats{};
+        best_r = -1;
+        best_in = std::numeric_limits<double>::infinity();
+        best_it = 0;
+    }
+    ~KmLane() {
+        if (e.st) cudaStreamDestroy(e.st);
     }
 };
 

@@ -21,6 +21,7 @@
 // mbarriers; warps 0-3 drain the TMEM accumulator (tcgen05.ld 32x32b).
 #pragma once
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "km.cuh"
@@ -68,6 +69,11 @@ RESPCA_DEV bool mbar_wait(uint64_t* bar, uint32_t parity) {
             else if (t - t0 > 2000000000ULL) return false;
         }
     }
+}
+
+RESPCA_DEV void mbar_expect_tx_cta(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
 }
 
 RESPCA_DEV uint64_t tc_desc_sw128(uint32_t saddr) {
@@ -303,6 +309,188 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_screen_tc(
     if (warp == TC_PRODUCERS)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
                      "r"(TC_N));
+}
+
+// ---------------------------------------------------------------------------
+// TMA-fed variant for the ALM loop.  Pass F also writes L′ as BF16 in the
+// K-major layout [n][d_pad] (Lb), so the screen no longer converts: one thread
+// issues cp.async.bulk.tensor loads of the A tile (128 columns × 64 K, 16 KB)
+// and the B tile (64 centroids × 64 K, 8 KB) straight into the SWIZZLE_128B
+// layout the MMA descriptors expect; one thread issues tcgen05.mma; four warps
+// accumulate ‖x_j‖² from the BF16 A tiles while the MMAs run (FP64
+// accumulation of bf16 squares: |Σ bf16(x)² − ‖x‖²| ≤ (2⁻⁸ + 2⁻¹⁷)‖x‖²,
+// covered by tma_xx_kappa) and then drain TMEM.
+//   warp 0: TMA producer   warp 1: MMA issuer   warps 2-5: ‖x‖² + epilogue
+// ---------------------------------------------------------------------------
+constexpr int TM_THREADS = 6 * 32;
+
+__host__ __device__ inline double tma_xx_kappa(double d) {
+    return 0.00390625 + 7.62939453125e-06 + d * 1.2212453270876722e-16;
+}
+
+RESPCA_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+        "[%4];\n" ::"r"(dst),
+        "l"((uint64_t)map), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
+    const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t d,
+    int n, int c, int kblocks_per_split, double* __restrict__ part, double* __restrict__ xxp,
+    int* __restrict__ err) {
+    extern __shared__ __align__(1024) unsigned char tsm_raw[];
+    unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
+    unsigned char* stage_base = tsm;
+    uint64_t* full_bar = reinterpret_cast<uint64_t*>(tsm + (size_t)TC_STAGES * TC_STAGE_BYTES);
+    uint64_t* empty_bar = full_bar + TC_STAGES;
+    uint64_t* done_bar = empty_bar + TC_STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done_bar + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j0 = blockIdx.x * TC_M, split = blockIdx.y;
+    const int64_t kb0 = (int64_t)split * kblocks_per_split;
+    const int64_t total_kb = (d + TC_KB - 1) / TC_KB;
+    int64_t kb1 = kb0 + kblocks_per_split;
+    if (kb1 > total_kb) kb1 = total_kb;
+    const int nkb = kb1 > kb0 ? (int)(kb1 - kb0) : 0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < TC_STAGES; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1 + 4);  // MMA commit + the four ‖x‖² warps
+        }
+        mbar_init(done_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&mapA) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"((uint64_t)&mapB) : "memory");
+    }
+    if (warp == 1) {  // the MMA warp owns the TMEM allocation
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n");
+    const uint32_t tmem = *tmem_slot;
+
+    double xx = 0.0;                        // warps 2-5: ‖x_row‖² of this split
+    const int quarter = warp & 3;           // TMEM lanes a warp may access: 32·(warp % 4)
+    const int row = quarter * 32 + lane;
+    if (warp == 0) {
+        if (lane == 0) {  // ---------------- TMA producer ----------------
+            for (int it = 0; it < nkb; ++it) {
+                const int s = it % TC_STAGES;
+                if (it >= TC_STAGES && !mbar_wait(&empty_bar[s], ((it / TC_STAGES) - 1) & 1)) {
+                    atomicExch(err, 1);
+                    break;
+                }
+                const uint32_t a = smem_u32(stage_base + (size_t)s * TC_STAGE_BYTES);
+                mbar_expect_tx_cta(&full_bar[s], TC_A_BYTES + TC_B_BYTES);
+                const int kx = (int)((kb0 + it) * TC_KB);
+                tma_load_2d(a, &mapA, kx, j0, &full_bar[s]);
+                tma_load_2d(a + TC_A_BYTES, &mapB, kx, 0, &full_bar[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---------------- MMA issuer ----------------
+            bool ok = true;
+            for (int it = 0; it < nkb; ++it) {
+                const int s = it % TC_STAGES;
+                if (!mbar_wait(&full_bar[s], (it / TC_STAGES) & 1)) {
+                    atomicExch(err, 2);
+                    ok = false;
+                    break;
+                }
+                asm volatile("tcgen05.fence::after_thread_sync;\n");
+                const uint32_t a0 = smem_u32(stage_base + (size_t)s * TC_STAGE_BYTES);
+                const uint32_t b0 = a0 + TC_A_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < TC_KB / 16; ++kk) {
+                    const uint64_t ad = tc_desc_sw128(a0 + kk * 32);
+                    const uint64_t bd = tc_desc_sw128(b0 + kk * 32);
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(ad), "l"(bd), "r"(TC_IDESC), "r"(acc));
+                }
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(&empty_bar[s]))
+                    : "memory");
+            }
+            if (ok)
+                asm volatile(
+                    "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(done_bar))
+                    : "memory");
+            else
+                mbar_arrive(done_bar);
+        }
+    } else {  // ---------------- ‖x‖² from the landed A tiles ----------------
+        for (int it = 0; it < nkb; ++it) {
+            const int s = it % TC_STAGES;
+            if (!mbar_wait(&full_bar[s], (it / TC_STAGES) & 1)) {
+                if (lane == 0) atomicExch(err, 4);
+                break;
+            }
+            const unsigned char* A = stage_base + (size_t)s * TC_STAGE_BYTES;
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+                const uint4 q = *reinterpret_cast<const uint4*>(A + sw128(row, ch));
+                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+                for (int h = 0; h < 4; ++h) {
+                    const double lo = (double)__uint_as_float(w[h] << 16);
+                    const double hi = (double)__uint_as_float(w[h] & 0xffff0000u);
+                    xx = __fma_rn(lo, lo, xx);
+                    xx = __fma_rn(hi, hi, xx);
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);
+        }
+    }
+    __syncthreads();  // every stage issued
+    if (warp >= 2) {  // ---------------- epilogue: TMEM → partials ----------------
+        bool ok = nkb == 0 || mbar_wait(done_bar, 0);
+        if (!ok && lane == 0) atomicExch(err, 3);
+        asm volatile("tcgen05.fence::after_thread_sync;\n");
+        const int j = j0 + row;
+        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            uint32_t r[32];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+                "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]),
+                  "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]),
+                  "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                  "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]),
+                  "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr + half * 32));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (j < n && ok) {
+                double* dst = part + ((int64_t)split * n + j) * c;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const int k = half * 32 + q;
+                    if (k < c) dst[k] = nkb ? (double)__uint_as_float(r[q]) : 0.0;
+                }
+            }
+        }
+        if (j < n) xxp[(int64_t)split * n + j] = nkb ? xx : 0.0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n");
+    __syncthreads();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
 }
 
 }  // namespace respca_dev
