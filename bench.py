@@ -278,7 +278,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
     L = N.lib()
     dt = np.float32 if w.dtype == "f32" else np.float64
     Xp = pinned(w.d, w.n, np.float64)
-    w.make(out=Xp)
+    w.make_device(out=Xp, ctx=ctx)  # respca-synth-1, O(d·n) part assembled on the GPU
     Xh = Xp if dt == np.float64 else np.asfortranarray(Xp.astype(np.float32))
     cfg = w.solver_config()
     cc = cfg.to_c()

@@ -198,6 +198,14 @@ int respca_cu_outlier_scores(respca_cu_ctx* ctx, const double* s, uint64_t d, ui
                              double threshold, double* scores, uint64_t* flagged,
                              uint64_t* n_flagged);
 
+/* The "respca-synth-1" rpca workload generator (paper_1904_07497_b200/csrc/
+ * synth.c) with its O(d·n) assembly on the device: X = U·Vᵀ + S0, U (d×r),
+ * V (n×r) i.i.d. N(0, sigma²), S0 Bernoulli(p) support with U[lo, hi] values.
+ * Byte-identical to the host generator; X_out (host, d×n column-major, F64 or
+ * F32 per dtype) receives the result. */
+int respca_cu_synth_rpca(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t r, double sigma, double p,
+                         double lo, double hi, uint64_t seed, int dtype, void* X_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,10 +47,13 @@ def _stale(out: Path, deps: list[Path]) -> bool:
 def build_cuda(force: bool = False) -> Path:
     LIB.mkdir(exist_ok=True)
     out = LIB / "librespca_cu.so"
-    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [INC / "respca_cu.h"]
+    deps = (list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [INC / "respca_cu.h", CSRC / "synth.c",
+            CSRC / "synth.h"])
     if force or _stale(out, deps):
+        # synth.c rides along for the device generator's host factors (U, V)
         _run([NVCC, *ARCH, *NVFLAGS, f"-I{INC}", f"-I{CSRC}", "-shared",
-              str(CSRC / "engine.cu"), "-o", str(out), "-lcudart", "-Xcompiler", "-pthread"],
+              str(CSRC / "engine.cu"), str(CSRC / "synth.c"), "-o", str(out), "-lcudart",
+              "-Xcompiler", "-pthread,-ffp-contract=off"],
              log=LIB / "ptxas_engine.log")
     return out
 

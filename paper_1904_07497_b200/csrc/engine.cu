@@ -19,6 +19,8 @@
 #include "alm.cuh"
 #include "engine.cuh"
 #include "binio.cuh"
+#include "synth.h"
+#include "synth_dev.cuh"
 #include "kmeans_engine.cuh"
 #include "km.cuh"
 
@@ -1277,6 +1279,44 @@ int respca_cu_outlier_scores(respca_cu_ctx* ctx, const double* s, uint64_t d, ui
                 ++m;
             }
         if (n_flagged) *n_flagged = m;
+    });
+}
+
+int respca_cu_synth_rpca(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t r, double sigma, double p,
+                         double lo, double hi, uint64_t seed, int dtype, void* X_out) {
+    return guarded(ctx, [&] {  // csrc/synth.c rpca, assembled on the device
+        check_dims(d, n);
+        if (!X_out) throw InvalidArg("respca_cu_synth_rpca: null pointer");
+        if (r == 0) throw InvalidArg("respca_cu_synth_rpca: r must be >= 1");
+        if (dtype != RESPCA_F64 && dtype != RESPCA_F32) throw InvalidArg("respca_cu_synth_rpca: unknown dtype");
+        if (n > 65535 * 65535ULL) throw InvalidArg("respca_cu_synth_rpca: too many columns");
+        synth_rpca_spec sp{d, n, r, sigma, p, lo, hi, seed};
+        std::vector<double> U(d * r), V(n * r);
+        if (synth_rpca_factors(&sp, U.data(), V.data()) != 0) throw InvalidArg("synth_rpca: bad spec");
+        uint64_t ks = 0, kval = 0;
+        synth_rpca_keys(&sp, &ks, &kval);
+        cudaStream_t st = ctx->st;
+        DBuf<double> du, dv;
+        du.ensure(d * r);
+        dv.ensure(n * r);
+        CK(cudaMemcpyAsync(du.p, U.data(), sizeof(double) * d * r, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(dv.p, V.data(), sizeof(double) * n * r, cudaMemcpyHostToDevice, st));
+        const size_t es = dtype == RESPCA_F64 ? 8 : 4;
+        void* dx = ctx->arena.get("X", es * d * n);  // a later solve overwrites it anyway
+        const dim3 grid(ceil_div(d, 256), 1, 1);
+        for (uint64_t j0 = 0; j0 < n; j0 += 65535) {  // grid.y ≤ 65535 columns per launch
+            const uint64_t nj = std::min<uint64_t>(65535, n - j0);
+            const double* vp = dv.p + j0 * r;
+            if (dtype == RESPCA_F64)
+                k_synth_rpca<double><<<dim3(grid.x, (unsigned)nj), 256, sizeof(double) * r, st>>>(
+                    du.p, vp, (int64_t)d, (int)r, p, lo, hi - lo, ks, kval, (int64_t)j0, (double*)dx + j0 * d);
+            else
+                k_synth_rpca<float><<<dim3(grid.x, (unsigned)nj), 256, sizeof(double) * r, st>>>(
+                    du.p, vp, (int64_t)d, (int)r, p, lo, hi - lo, ks, kval, (int64_t)j0, (float*)dx + j0 * d);
+            ctx->launches++;
+        }
+        CK(cudaMemcpyAsync(X_out, dx, es * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
     });
 }
 

@@ -50,6 +50,25 @@ static inline double normal01(uint64_t key, uint64_t idx) {
 
 const char* synth_version(void) { return "respca-synth-1"; }
 
+/* the factors of synth_rpca alone: U (d×r column-major), V (n×r, row j =
+ * V[j, :]) — the device assembly (respca_cu_synth_rpca) uses these */
+int synth_rpca_factors(const synth_rpca_spec* sp, double* U, double* V) {
+    const uint64_t d = sp->d, n = sp->n, r = sp->r;
+    if (d == 0 || n == 0 || r == 0) return 1;
+    const uint64_t ku = stream_key(sp->seed, 0), kv = stream_key(sp->seed, 1);
+#pragma omp parallel for schedule(static)
+    for (uint64_t e = 0; e < d * r; ++e) U[e] = sp->sigma * normal01(ku, e);
+#pragma omp parallel for schedule(static)
+    for (uint64_t e = 0; e < n * r; ++e) V[e] = sp->sigma * normal01(kv, e);
+    return 0;
+}
+
+/* the S0 stream keys (support, values) of a spec */
+void synth_rpca_keys(const synth_rpca_spec* sp, uint64_t* ks, uint64_t* kval) {
+    *ks = stream_key(sp->seed, 2);
+    *kval = stream_key(sp->seed, 3);
+}
+
 int synth_rpca(const synth_rpca_spec* sp, double* X, double* L0, double* S0) {
     const uint64_t d = sp->d, n = sp->n, r = sp->r;
     if (d == 0 || n == 0 || r == 0) return 1;

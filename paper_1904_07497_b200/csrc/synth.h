@@ -26,6 +26,8 @@ const char* synth_version(void);
 /* X (d·n doubles, column-major) required; L0 / S0 may be NULL.  0 = ok. */
 int synth_rpca(const synth_rpca_spec* spec, double* X, double* L0, double* S0);
 int synth_video(const synth_video_spec* spec, double* X, double* L0, double* S0);
+int synth_rpca_factors(const synth_rpca_spec* spec, double* U, double* V);
+void synth_rpca_keys(const synth_rpca_spec* spec, uint64_t* ks, uint64_t* kval);
 void synth_to_f32(const double* src, float* dst, uint64_t count);
 
 #ifdef __cplusplus

@@ -64,6 +64,26 @@ def rpca(d: int, n: int, r: int, sigma: float, p: float, lo: float = -50.0, hi: 
     return (X, L0, S0) if with_truth else X
 
 
+def rpca_device(d: int, n: int, r: int, sigma: float, p: float, lo: float = -50.0,
+                hi: float = 50.0, seed: int = 42, dtype=np.float64, out: np.ndarray | None = None,
+                ctx=None) -> np.ndarray:
+    """rpca() with the O(d·n) assembly on the GPU (respca_cu_synth_rpca):
+    byte-identical to the host generator, milliseconds instead of seconds at
+    C3/C5 sizes.  `dtype` float32 gives the rounded copy synth_to_f32 makes."""
+    from . import _native as N
+
+    dt = np.dtype(dtype)
+    if out is not None:
+        assert out.shape == (d, n) and out.dtype == dt and out.flags.f_contiguous
+    X = out if out is not None else np.empty((d, n), dtype=dt, order="F")
+    ctx = ctx if ctx is not None else N.default_context()
+    rc = N.lib().respca_cu_synth_rpca(ctx.handle, d, n, r, sigma, p, lo, hi, seed,
+                                      N.F32 if dt == np.float32 else N.F64,
+                                      X.ctypes.data_as(C.c_void_p))
+    N.check(ctx, rc)
+    return X
+
+
 def video(frames: int = 1000, height: int = 240, width: int = 320, block: int = 40,
           blur_sigma: float = 24.0, noise_sigma: float = 0.01, seed: int = 42,
           with_truth: bool = False):
@@ -100,6 +120,14 @@ class Workload:
             return video(frames=self.n, seed=self.seed, with_truth=with_truth)
         return rpca(self.d, self.n, self.r, self.sigma, self.p, seed=self.seed,
                     with_truth=with_truth, out=out)
+
+    def make_device(self, out: np.ndarray | None = None, ctx=None):
+        """make() with the O(d·n) assembly on the GPU when the generator has one
+        (rpca); same bytes."""
+        if self.kind != "rpca":
+            return self.make(out=out)
+        return rpca_device(self.d, self.n, self.r, self.sigma, self.p, seed=self.seed, out=out,
+                           ctx=ctx)
 
     def solver_config(self, **over):
         from .respca import KMeansConfig, SolverConfig
