@@ -330,6 +330,10 @@ def run_ours(args, w, world, rank, local, pg) -> None:
             el = time.perf_counter() - t0
             if rep:
                 runs.append((el, res))
+            if os.environ.get("RESPCA_BENCH_VERBOSE"):
+                print(f"e2e run {rep}: wall {el:.3f}s init {res.init_ms:.0f}ms loop {res.loop_ms:.0f}ms "
+                      f"h2d {res.h2d_ms:.0f}ms d2h {res.d2h_ms:.0f}ms c-abi {res.wall_time:.3f}s",
+                      file=sys.stderr, flush=True)
         el = allmax(pg, max(r[0] for r in runs), local)
         res = runs[-1][1]
         e2e = {"value": world * res.report.iters / el, "unit": "iters/s",
@@ -337,7 +341,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
                "d2h_bytes_per_step": int(2 * N_el * esize + 8 * w.n + 32 * res.report.iters),
                "step": "one complete respca_cu_solve (pinned host X → host L, S, labels)",
                "iters": res.report.iters, "converged": res.report.converged,
-               "wall_s": el}
+               "wall_s": el, "runs_s": [round(r[0], 4) for r in runs]}
         ttc = {"seconds": el, "device_init_ms": res.init_ms, "device_loop_ms": res.loop_ms,
                "h2d_ms": res.h2d_ms, "d2h_ms": res.d2h_ms, "iters": res.report.iters,
                "hartigan_moves": res.hartigan_moves, "exact_fallbacks": res.exact_fallbacks,

@@ -41,6 +41,7 @@ struct respca_cu_ctx {
     Arena arena;                         // N-sized solve state reused across solves
     std::unique_ptr<PoolBase> lanes[2];  // k-means restart lanes (fp64, fp32 storage)
     std::unique_ptr<PoolBase> engines[2];  // solve()'s k-means engine (fp64, fp32 storage)
+    std::unique_ptr<AlmBase> solver[2];    // solve()'s ALM state + captured graphs, reused
 };
 
 namespace {
@@ -119,6 +120,15 @@ struct Alm : AlmBase {
 
     bool use_arena = false;  // solve(): borrow the context's arena for X, L, S, Θ, Lb
 
+    // per-solve counters of a reused solver
+    void begin_solve() {
+        stats = Stats{};
+        slow_iters = 0;
+        init_ms = 0.0;
+        km.st = st;
+        km.ln = ln;
+        km.stats = &stats;
+    }
     static KMeansEngine<T>& shared_engine(respca_cu_ctx* cx) {
         auto& h = cx->engines[sizeof(T) == 8 ? 0 : 1];
         if (!h) h.reset(new EngineHolder<T>());
@@ -363,6 +373,31 @@ struct Alm : AlmBase {
     }
     int kernels_per_iter() const { return 1 + (c > 1 ? 6 : 0) + 1 + (l21 ? 3 : 0); }
 
+    // the captured graphs bake in pointers and shapes: re-capture only when
+    // one of them (or any device allocation) changed since the last capture
+    uint64_t cap_key[12] = {};
+    bool cap_valid = false;
+    void capture_if_needed() {
+        const uint64_t key[12] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
+                                  (uint64_t)use_tc, (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
+                                  (uint64_t)passf_variant_env, (uint64_t)dpad, g_alloc_gen.load()};
+        if (cap_valid && std::equal(key, key + 12, cap_key)) return;
+        cap_valid = false;
+        try {
+            capture();
+        } catch (...) {  // never leave the stream in capture mode
+            cudaStreamCaptureStatus cs;
+            if (cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+                cudaGraph_t g = nullptr;
+                cudaStreamEndCapture(st, &g);
+                if (g) cudaGraphDestroy(g);
+            }
+            cudaGetLastError();
+            throw;
+        }
+        std::copy(key, key + 12, cap_key);
+        cap_valid = true;
+    }
     void capture() {
         const uint64_t saved = *ln.counter;  // captured launches are not executions
         // WHILE graph: the product loop
@@ -415,6 +450,7 @@ struct Alm : AlmBase {
             if (h.slow) {
                 ++slow_iters;
                 slow_path(h);
+                capture_if_needed();  // the exact continuation may have grown a buffer
             }
             if (h.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
             if (h.done) break;
@@ -544,8 +580,14 @@ void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_conf
     validate_cfg(cfg);
     if (cfg.c > n) throw InvalidArg("solve: c exceeds column count");
     const auto t0 = Clock::now();
-    Alm<T> a(ctx, /*shared=*/true);
-    a.use_arena = true;
+    auto& slot = ctx->solver[sizeof(T) == 8 ? 0 : 1];
+    if (!slot) {
+        auto* fresh = new Alm<T>(ctx, /*shared=*/true);
+        fresh->use_arena = true;
+        slot.reset(fresh);
+    }
+    Alm<T>& a = *static_cast<Alm<T>*>(slot.get());
+    a.begin_solve();
     Events ev;
     CK(cudaEventRecord(ev.a, ctx->st));
     a.upload_with(d, n, cfg, fill);
@@ -560,7 +602,7 @@ void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_conf
     CK(cudaEventRecord(e2.b, ctx->st));
     CK(cudaEventSynchronize(e2.b));
     const double init_ms = e2.ms();
-    a.capture();
+    a.capture_if_needed();
     Events e3;
     CK(cudaEventRecord(e3.a, ctx->st));
     a.run_loop();

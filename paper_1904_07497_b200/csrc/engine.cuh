@@ -4,6 +4,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -42,6 +43,11 @@ inline void ck(cudaError_t e, const char* what) {
 }
 #define CK(x) ::respca_host::ck((x), #x)
 
+// bumped whenever device memory behind a DBuf / Arena slot changes address:
+// captured CUDA graphs bake pointers in, so a graph is re-captured when this
+// moved since its capture
+inline std::atomic<uint64_t> g_alloc_gen{0};
+
 template <class U>
 struct DBuf {
     U* p = nullptr;
@@ -62,11 +68,13 @@ struct DBuf {
             owned = true;
             CK(cudaMalloc(&p, count * sizeof(U)));
             cap = count;
+            g_alloc_gen.fetch_add(1);
         }
         return p;
     }
     void borrow(void* q, size_t count) {  // arena memory, never freed here
         if (p && owned) cudaFree(p);
+        if (p != q) g_alloc_gen.fetch_add(1);
         p = static_cast<U*>(q);
         cap = count;
         owned = false;
@@ -96,12 +104,14 @@ struct Arena {
                     kv.second.bytes = 0;
                     CK(cudaMalloc(&kv.second.p, bytes));
                     kv.second.bytes = bytes;
+                    g_alloc_gen.fetch_add(1);
                 }
                 return kv.second.p;
             }
         Slot sl;
         CK(cudaMalloc(&sl.p, bytes));
         sl.bytes = bytes;
+        g_alloc_gen.fetch_add(1);
         slots.emplace_back(name, sl);
         return sl.p;
     }
