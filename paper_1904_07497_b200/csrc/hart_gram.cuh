@@ -1,0 +1,681 @@
+// Exact sequential Hartigan refinement (kmeans.cpp:96-139) on the Gram matrix.
+//
+// hartigan_refine visits columns j = 0..n−1 pass after pass and applies every
+// improving single-point move at once, so each decision sees the centroids
+// and counts left by all earlier moves.  The persistent kernel of
+// hartigan.cuh keeps that order with distance intervals refreshed from the
+// d-long centroid rows (O(d·n·c) per pass).  Here the same decisions are made
+// from quantities that a move changes in O(n) work, independent of d:
+//
+//   G = MᵀM (n×n, FP64 tensor cores, once per kmeans(X), shared by every
+//   restart), and per restart, for every centroid k with members Σ_k:
+//     S_k[j] = x_j·Σ_k          (n values; a move m: f→t subtracts / adds G[:,m])
+//     Q_k    = ‖Σ_k‖²            (O(1) per move)
+//     ‖x_j − μ_k‖² = G_jj − 2·S_k[j]/n_k + Q_k/n_k²     (μ_k = Σ_k/n_k)
+//
+// The reference's centroids are not the exact means μ_k but running values
+// c_k (means_of rounding, then the incremental update of kmeans.cpp:128-129
+// per move), and its distance is the sequential chain of rounded squares.
+// Every source of difference is bounded rigorously and carried per centroid:
+//   |Ŝ_k[j] − x_j·Σ_k| ≤ ‖x_j‖·ES_k       |Q̂_k − ‖Σ_k‖²| ≤ EQ_k
+//   ‖c_k − μ_k‖ ≤ Δ_k                      |Ĝ_jm − x_j·x_m| ≤ γ_G‖x_j‖‖x_m‖
+//   |chain − ‖x − c‖²| ≤ γ_c‖x − c‖²       (γ_c = (d+3)u·1.02, hart_widen)
+// so each (j, k) pair gets an interval that provably holds the reference's
+// sq_dist value; a decision is taken only when it is the same for every value
+// in the intervals (monotone IEEE rounding of the weights, as in
+// hartigan.cuh).  Undecidable columns replay the logged moves onto the
+// centroids with the reference's own formula and decide on the reference's
+// chain.  Labels are therefore bit-identical to the reference's.
+//
+// One CTA per restart: a window of 32 columns is decided by 32 warps (lanes
+// over centroids), the first column that is not provably "no move" is
+// settled, the O(n) update is applied by all threads, and the scan resumes at
+// the next column — no grid barrier per move.
+#pragma once
+
+#include "km.cuh"
+
+namespace respca_dev {
+
+// ---------------------------------------------------------------------------
+// G = MᵀM: lower-triangle 128×128 tiles (mirrored on store), m16n8k8 DMMA,
+// 3-stage cp.async ring over K-chunks of 32 rows.  8 warps, warp tile 64×32.
+// ---------------------------------------------------------------------------
+constexpr int GR_T = 128, GR_KC = 32, GR_AS = GR_KC + 4, GR_ST = 3;
+
+template <typename T>
+size_t gram_smem() {
+    return (size_t)2 * GR_ST * GR_T * GR_AS * sizeof(T);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_t d, int n,
+                                                 double* __restrict__ G) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    T* As = reinterpret_cast<T*>(sm);        // [ST][128][AS]  columns i0.. (rows of A)
+    T* Bs = As + GR_ST * GR_T * GR_AS;       // [ST][128][AS]  columns j0..
+    constexpr int EPV = 16 / sizeof(T);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int wr = warp >> 2, wc = warp & 3;
+    // triangular tile index → (bi ≥ bj)
+    const long long tix = blockIdx.x;
+    int bi = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
+    while ((long long)(bi + 1) * (bi + 2) / 2 <= tix) ++bi;
+    while ((long long)bi * (bi + 1) / 2 > tix) --bi;
+    const int bj = (int)(tix - (long long)bi * (bi + 1) / 2);
+    const int i0 = bi * GR_T, j0 = bj * GR_T;
+    const int nch = (int)((d + GR_KC - 1) / GR_KC);
+    const bool vec = (d % EPV) == 0 && ((uintptr_t)M % 16) == 0;
+
+    auto load = [&](int ch, int buf) {
+        const int64_t k0 = (int64_t)ch * GR_KC;
+        T* ad = As + (size_t)buf * GR_T * GR_AS;
+        T* bd = Bs + (size_t)buf * GR_T * GR_AS;
+        if (vec) {
+            constexpr int VPC = GR_KC / EPV;  // vectors per column chunk
+            for (int e = tid; e < 2 * GR_T * VPC; e += 256) {
+                const int half = e / (GR_T * VPC), r = (e / VPC) % GR_T, v = e % VPC;
+                const int col = (half ? j0 : i0) + r;
+                const int64_t k = k0 + v * EPV;
+                int bytes = 0;
+                if (col < n && k < d) bytes = (int)(sizeof(T) * (d - k < EPV ? d - k : EPV));
+                T* dst = (half ? bd : ad) + r * GR_AS + v * EPV;
+                cp_async16(dst, bytes ? M + (int64_t)col * d + k : M, bytes);
+            }
+        } else {
+            for (int e = tid; e < 2 * GR_T * GR_KC; e += 256) {
+                const int half = e / (GR_T * GR_KC), r = (e / GR_KC) % GR_T, kk = e % GR_KC;
+                const int col = (half ? j0 : i0) + r;
+                const int64_t k = k0 + kk;
+                const bool p = col < n && k < d;
+                T* dst = (half ? bd : ad) + r * GR_AS + kk;
+                if (sizeof(T) == 8) cp_async8(dst, p ? M + (int64_t)col * d + k : M, p);
+                else cp_async4(dst, p ? M + (int64_t)col * d + k : M, p);
+            }
+        }
+        cp_commit();
+    };
+
+    double acc[4][4][4];
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int z = 0; z < 4; ++z) acc[x][y][z] = 0.0;
+
+    for (int s = 0; s < GR_ST - 1; ++s) {
+        if (s < nch) load(s, s);
+        else cp_commit();
+    }
+    for (int ch = 0; ch < nch; ++ch) {
+        cp_wait<GR_ST - 2>();
+        __syncthreads();
+        // refill the stage consumed two chunks ago
+        if (ch + GR_ST - 1 < nch) load(ch + GR_ST - 1, (ch + GR_ST - 1) % GR_ST);
+        else cp_commit();
+        const T* as = As + (size_t)(ch % GR_ST) * GR_T * GR_AS + (wr * 64 + g) * GR_AS + t4;
+        const T* bs = Bs + (size_t)(ch % GR_ST) * GR_T * GR_AS + (wc * 32 + g) * GR_AS + t4;
+#pragma unroll
+        for (int kk = 0; kk < GR_KC; kk += 8) {
+            double a[4][4], b[4][2];
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+                a[x][0] = (double)as[(x * 16) * GR_AS + kk];
+                a[x][1] = (double)as[(x * 16 + 8) * GR_AS + kk];
+                a[x][2] = (double)as[(x * 16) * GR_AS + kk + 4];
+                a[x][3] = (double)as[(x * 16 + 8) * GR_AS + kk + 4];
+            }
+#pragma unroll
+            for (int y = 0; y < 4; ++y) {
+                b[y][0] = (double)bs[(y * 8) * GR_AS + kk];
+                b[y][1] = (double)bs[(y * 8) * GR_AS + kk + 4];
+            }
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+#pragma unroll
+                for (int y = 0; y < 4; ++y)
+                    dmma1688(acc[x][y][0], acc[x][y][1], acc[x][y][2], acc[x][y][3], a[x][0], a[x][1],
+                             a[x][2], a[x][3], b[y][0], b[y][1]);
+        }
+    }
+    cp_wait<0>();
+    // epilogue: (r, q) with r ≥ q stored at G[q·n + r] and G[r·n + q]
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+            for (int z = 0; z < 4; ++z) {
+                const int r = i0 + wr * 64 + x * 16 + g + (z >= 2 ? 8 : 0);
+                const int q = j0 + wc * 32 + y * 8 + 2 * t4 + (z & 1);
+                if (r < n && q < n && r >= q) {
+                    __stcg(G + (int64_t)q * n + r, acc[x][y][z]);
+                    __stcg(G + (int64_t)r * n + q, acc[x][y][z]);
+                }
+            }
+}
+
+// diagonal: xx = Ĝ_jj, xn ≥ ‖x_j‖ ≥ xl (|Ĝ_jj − ‖x_j‖²| ≤ γ_G‖x_j‖²)
+__global__ void k_gram_diag(const double* __restrict__ G, int n, double gamG, double* __restrict__ xx,
+                            double* __restrict__ xn, double* __restrict__ xl) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double v = fmax(G[(int64_t)j * n + j], 0.0);
+    xx[j] = v;
+    xn[j] = __dsqrt_ru(__dmul_ru(v, __dadd_ru(1.0, 2.0 * gamG)));
+    xl[j] = __dsqrt_rd(fmax(__dmul_rd(v, __dsub_rd(1.0, 2.0 * gamG)), 0.0));
+}
+
+// S_k[j] = Σ_{m∈k} Ĝ[m][j] (members in ascending order), thread per (j, k)
+__global__ void k_gram_s0(const double* __restrict__ G, const int* __restrict__ goff,
+                          const int* __restrict__ members, int n, double* __restrict__ S) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
+    if (j >= n) return;
+    const int p0 = __ldg(goff + k), p1 = __ldg(goff + k + 1);
+    double s = 0.0;
+    int p = p0;
+    for (; p + 4 <= p1; p += 4) {
+        const double g0 = __ldcg(G + (int64_t)__ldg(members + p) * n + j);
+        const double g1 = __ldcg(G + (int64_t)__ldg(members + p + 1) * n + j);
+        const double g2 = __ldcg(G + (int64_t)__ldg(members + p + 2) * n + j);
+        const double g3 = __ldcg(G + (int64_t)__ldg(members + p + 3) * n + j);
+        s += g0;
+        s += g1;
+        s += g2;
+        s += g3;
+    }
+    for (; p < p1; ++p) s += __ldcg(G + (int64_t)__ldg(members + p) * n + j);
+    S[(int64_t)k * n + j] = s;
+}
+
+// per-centroid state of the Gram refinement
+struct GramScal {
+    double Q, A, ES, EQ, Dl;  // Q̂_k, Σ‖x_m‖ (upper), S error / ‖x_j‖, Q error, ‖c_k − μ_k‖
+};
+
+RESPCA_DEV double gam_n(double m) {  // γ_m = m·u/(1 − m·u), bounded with slack
+    return m * kU * 1.01;
+}
+
+// initial scalars from S⁰ and the start centroids C = means_of (kmeans.cpp:66-82)
+__global__ void k_gram_scal(const double* __restrict__ S, const double* __restrict__ xn,
+                            const int* __restrict__ goff, const int* __restrict__ members, int n, int c,
+                            double gamG, GramScal* __restrict__ out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= c) return;
+    const int p0 = goff[k], p1 = goff[k + 1];
+    const double nk = (double)(p1 - p0);
+    double A = 0.0, Q = 0.0;
+    for (int p = p0; p < p1; ++p) {
+        const int m = members[p];
+        A = __dadd_ru(A, xn[m]);
+        Q += S[(int64_t)k * n + m];
+    }
+    const double gn = gam_n(nk);
+    GramScal s;
+    s.A = A;
+    s.Q = Q;
+    // Ŝ⁰ = Σ_m Ĝ[m][j]: recursive-sum error γ_nk·Σ|Ĝ| plus the Ĝ errors
+    s.ES = __dmul_ru(__dadd_ru(__dmul_ru(gn, 1.0 + gamG), gamG), __dmul_ru(A, 1.01));
+    // Q̂⁰ = Σ_m Ŝ⁰_k[m]: Σ_m xn_m·ES + γ_nk·Σ_m xn_m (A + ES)
+    s.EQ = __dmul_ru(__dadd_ru(__dmul_ru(A, s.ES), __dmul_ru(gn, __dmul_ru(A, __dadd_ru(A, s.ES)))), 1.01);
+    // start centroid = fl(fl(Σ x_m) · fl(1/n_k)): ‖c − μ‖ ≤ γ_nk·A/n_k·(1+3u) + 2.01u·‖μ‖
+    const double mn = __dsqrt_ru(fmax(__ddiv_ru(__dadd_ru(Q, s.EQ), nk * nk), 0.0));
+    s.Dl = __dmul_ru(__dadd_ru(__dmul_ru(__ddiv_ru(__dmul_ru(gn, A), nk), 1.0 + 4.0 * kU),
+                               __dmul_ru(2.02 * kU, mn)),
+                     1.01);
+    out[k] = s;
+}
+
+struct GramArgs {
+    const double* G;   // [n][n] Ĝ (column m contiguous)
+    const double* xx;  // [n] Ĝ_jj
+    const double* xn;  // [n] ≥ ‖x_j‖
+    const double* xl;  // [n] ≤ ‖x_j‖
+    double* S;         // [c][n] Ŝ_k[j]
+    const GramScal* scal0;  // [c] initial scalars
+    int* labels;       // [n] in/out
+    int* counts;       // [c] in: start counts, out: final counts
+    double* Cs;        // [c][d] stored centroids (in: start centroids; replayed on demand)
+    int* log;          // [max_pass·n][5] moves (m, from, to, n_from, n_to)
+    unsigned long long* stats;  // [8] moves, passes, windows, exact fallbacks, replayed rows·moves
+    const void* M;     // the data (T), for the exact fallback
+    int64_t d;
+    int n, c, max_pass;
+    double gamG, gamc;
+};
+
+// per-centroid decision coefficients (shared memory)
+struct GramCoef {
+    double wa, wb;   // n/(n−1), n/(n+1) as the reference rounds them (kmeans.cpp:107, 114)
+    double a2, bq;   // fl(2/n), fl(Q̂/n²)
+    double E0, E1;   // interval half-width = E0 + E1·‖x_j‖ + γ_G‖x_j‖² + 5.1u(Ĝ_jj + |t| + bq)
+    double mn;       // ≥ ‖μ_k‖
+};
+
+// Bounds below are evaluated in round-to-nearest: every one is a chain of at
+// most a few dozen positive terms, so a final factor (1 + 64u) covers the
+// roundings (each op contributes at most a relative u).
+constexpr double kSlack = 1.0 + 64.0 * kU;
+
+RESPCA_DEV void gram_coef(const GramScal& s, int cnt, GramCoef& o) {
+    const double nk = (double)cnt;
+    o.wa = nk / (nk - 1.0);  // the reference's correctly rounded weights
+    o.wb = nk / (nk + 1.0);
+    const double rn = 1.0 / nk;
+    o.a2 = 2.0 * rn;           // |a2 − 2/n| ≤ u·a2
+    o.bq = (s.Q * rn) * rn;    // |bq − Q̂/n²| ≤ 3.01u·|bq|
+    const double r2 = rn * rn * kSlack;
+    o.mn = sqrt(fmax((s.Q + s.EQ) * r2, 0.0)) * kSlack;
+    // ‖x − c‖² vs ‖x − μ‖²: 2(‖x‖ + ‖μ‖)Δ + Δ²
+    o.E0 = ((s.EQ * r2 + 2.0 * o.mn * s.Dl) + s.Dl * s.Dl) * kSlack;
+    o.E1 = (2.0 * s.ES * rn + 2.0 * s.Dl) * kSlack;
+}
+
+// interval [lo, hi] ∋ the reference's sq_dist(x_j, c_k); mid for the argmin
+struct GramCol {
+    double gjj, xnj, gq;
+};
+RESPCA_DEV void gram_iv(const GramCol& col, const GramCoef& cf, double s, double gamc, double& lo, double& hi,
+                        double& mid) {
+    const double t = cf.a2 * s;
+    mid = (col.gjj - t) + cf.bq;
+    const double e =
+        ((cf.E0 + cf.E1 * col.xnj) + (col.gq + 7.1 * kU * (fabs(t) + cf.bq))) * (1.0 + 16.0 * kU);
+    lo = fmax(mid - e, 0.0) * ((1.0 - gamc) * (1.0 - 8.0 * kU));
+    hi = (mid + e) * ((1.0 + gamc) * (1.0 + 8.0 * kU));
+    if (!(lo <= hi)) {  // non-finite: never decides
+        lo = 0.0;
+        hi = INFINITY;
+    }
+}
+
+// One warp decides column `from` on per-lane intervals (k = lane + 32q):
+// 0 = provably no move, 1 = provably moves to `to`, 2 = undecidable.
+// Same decision logic as hart_decide_warp_w (hartigan.cuh).
+template <int KPL>
+RESPCA_DEV int gram_decide(int from, int c, const GramCoef* cf, const int* cnt, const double (&lo)[KPL],
+                           const double (&hi)[KPL], const double (&mid)[KPL], int& to) {
+    const int lane = threadIdx.x & 31;
+    if (cnt[from] <= 1) return 0;  // kmeans.cpp:105
+    const int fq = from >> 5, fl_ = from & 31;
+    double flo = 0, fhi = 0, fmid = 0;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q)
+        if (q == fq) {
+            flo = __shfl_sync(0xffffffffu, lo[q], fl_);
+            fhi = __shfl_sync(0xffffffffu, hi[q], fl_);
+            fmid = __shfl_sync(0xffffffffu, mid[q], fl_);
+        }
+    const double w_a = cf[from].wa;
+    const double g_lo = w_a * flo, g_hi = w_a * fhi, g_mid = w_a * fmid;
+    double bd = INFINITY;
+    int bk = 0x7fffffff;
+    bool none = true;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= c || k == from) continue;
+        const double w_b = cf[k].wb;
+        none &= !(w_b * lo[q] - g_hi < -1e-12);  // kmeans.cpp:116, best_delta = −1e-12
+        const double dmid = w_b * mid[q] - g_mid;
+        if (dmid < bd) {
+            bd = dmid;
+            bk = k;
+        }
+    }
+    none = __all_sync(0xffffffffu, none);
+    if (none) return 0;
+    warp_argmin(bd, bk);
+    if (bk >= c) return 2;
+    const int bq_ = bk >> 5, bl = bk & 31;
+    double bhi = 0;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q)
+        if (q == bq_) bhi = __shfl_sync(0xffffffffu, hi[q], bl);
+    const double dhi_k = cf[bk].wb * bhi - g_lo;
+    bool ok = dhi_k < -1e-12;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        if (k >= c || k == from || k == bk) continue;
+        const double dlo = cf[k].wb * lo[q] - g_hi;
+        if (k < bk) ok &= dhi_k < dlo;  // an earlier k must lose strictly
+        else ok &= dhi_k <= dlo;        // a later k never replaces an equal delta
+    }
+    ok = __all_sync(0xffffffffu, ok);
+    if (!ok) return 2;
+    to = bk;
+    return 1;
+}
+
+constexpr int GRAM_THREADS = 1024;
+
+// The move m: from → to (kmeans.cpp:122-135) on one side's scalars (side 0 =
+// from, 1 = to): Q, A, ES, EQ, Δ and the decision coefficients.  sv = Ŝ_k[m]
+// before the move.
+RESPCA_DEV void gram_side(int side, GramScal& S, GramCoef& cf, int& cnt, double sv, double gmm, double xnm,
+                          double xlm, double gamG) {
+    const double nk = (double)cnt;
+    const double g2 = gamG * xnm * xnm;
+    const double gx = gamG * xnm;
+    // Q: ‖Σ ∓ x_m‖² = Q ∓ 2x_m·Σ + ‖x_m‖²  (two rounded adds: ≤ 2.01u of the magnitudes)
+    const double q = side ? (S.Q + 2.0 * sv) + gmm : (S.Q - 2.0 * sv) + gmm;
+    const double eq = ((S.EQ + 2.0 * xnm * S.ES) + (g2 + 2.02 * kU * (fabs(S.Q) + 2.0 * fabs(sv) + gmm))) * kSlack;
+    // A stays an upper bound of Σ‖x_m‖ over the members
+    const double A = side ? (S.A + xnm) * kSlack : fmax(S.A - xlm * (1.0 - 4.0 * kU), 0.0) * kSlack;
+    // S: one rounded ∓ Ĝ[j][m] per entry; |Ŝ′| ≤ ‖x_j‖(A′ + ES + γ_G‖x_m‖)
+    const double es = ((S.ES + gx) + kU * 1.01 * ((A + S.ES) + gx)) * kSlack;
+    // Δ: c′ − μ′ = n(c − μ)/(n ∓ 1) + ρ, ‖ρ‖ ≤ 3.01u(n‖c‖ + ‖x_m‖)/(n ∓ 1), ‖c‖ ≤ ‖μ‖ + Δ
+    const double dl = ((S.Dl * nk + 3.02 * kU * (nk * (cf.mn + S.Dl) + xnm)) / (side ? nk + 1.0 : nk - 1.0)) * kSlack;
+    S.Q = q;
+    S.EQ = eq;
+    S.A = A;
+    S.ES = es;
+    S.Dl = dl;
+    cnt = side ? cnt + 1 : cnt - 1;
+    gram_coef(S, cnt, cf);
+}
+
+// ---- thread-block cluster helpers (DSMEM + cluster barrier)
+RESPCA_DEV uint32_t gcl_smem(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+RESPCA_DEV uint32_t gcl_map(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(gcl_smem(p)), "r"(rank));
+    return r;
+}
+RESPCA_DEV int gcl_ld_i32(uint32_t a) {
+    int v;
+    asm volatile("ld.shared::cluster.b32 %0, [%1];\n" : "=r"(v) : "r"(a) : "memory");
+    return v;
+}
+RESPCA_DEV double gcl_ld_f64(uint32_t a) {
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];\n" : "=d"(v) : "r"(a) : "memory");
+    return v;
+}
+RESPCA_DEV void gcl_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+RESPCA_DEV uint32_t gcl_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+    return r;
+}
+RESPCA_DEV uint32_t gcl_size() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_nctarank;\n" : "=r"(r));
+    return r;
+}
+constexpr int GRAM_MAXCL = 16;
+
+// One thread-block cluster per restart.  Every CTA keeps a replica of the
+// per-centroid state (identical updates from identical inputs); a window of
+// 32·CL columns is decided by all warps of the cluster (CTA r, warp w →
+// column cursor + 32r + w); the first column that is not provably "no move"
+// is found by every warp from the CTAs' window results (DSMEM); a move updates
+// Ŝ_from, Ŝ_to on every CTA's slice of the n columns.  One cluster barrier per
+// window and one per move.
+template <typename T, int KPL>
+__global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int c = a.c, n = a.n;
+    const int64_t d = a.d;
+    GramCoef* cf = reinterpret_cast<GramCoef*>(sm);
+    GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
+    double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
+    int* cnt = reinterpret_cast<int*>(dist + c);
+    __shared__ int s_res[2][32];         // per window parity: status | to << 2 | from << 17
+    __shared__ double s_sv[2][32][2];    // Ŝ_from[j], Ŝ_to[j] of a provable move
+    __shared__ int s_xres;               // exact fallback verdict (CTA 0)
+    __shared__ double s_xsv[2];
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rank = (int)gcl_rank(), CL = (int)gcl_size();
+    const int W = 32 * CL;
+    const T* M = static_cast<const T*>(a.M);
+    const double gamG = a.gamG, gamc = a.gamc;
+    // this CTA's slice of the O(n) update (even bounds: double2 access)
+    const int per = ((n + CL - 1) / CL + 1) & ~1;
+    const int u0 = min(n, rank * per), u1 = min(n, u0 + per);
+
+    for (int k = tid; k < c; k += blockDim.x) {
+        const int ck = a.counts[k];
+        cnt[k] = ck;
+        sc[k] = a.scal0[k];
+        gram_coef(sc[k], ck, cf[k]);
+    }
+    __syncthreads();
+
+    unsigned long long moves = 0, windows = 0, fallbacks = 0, replay_work = 0;
+    unsigned long long tph[4] = {0, 0, 0, 0};  // SM cycles (thread 0): decide+pick, fallback, update, -
+    unsigned long long tmk = clock64();
+    auto lap = [&](int slot) {
+        if (tid == 0) {
+            const unsigned long long t = clock64();
+            tph[slot] += t - tmk;
+            tmk = t;
+        }
+    };
+    int nlog = 0, replayed = 0, pass = 0, par = 0;
+    const bool vec2 = (n % 2) == 0;
+    for (;;) {
+        int improved = 0;
+        int cursor = 0;
+        while (cursor < n) {
+            // ---- decide the window (warp per column, lanes over k)
+            const int j = cursor + 32 * rank + warp;
+            int st = 0, to = -1, wfrom = 0;
+            if (j < n) {
+                double sv[KPL];
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) {
+                    const int k = lane + 32 * q;
+                    sv[q] = k < c ? __ldcg(a.S + (int64_t)k * n + j) : 0.0;
+                }
+                const int from = __ldcg(a.labels + j);
+                wfrom = from;
+                GramCol col;
+                col.gjj = __ldg(a.xx + j);
+                col.xnj = __ldg(a.xn + j);
+                if (cnt[from] > 1) {
+                    col.gq = gamG * col.xnj * col.xnj * (1.0 + 4.0 * kU) + 7.1 * kU * col.gjj;
+                    double lo[KPL], hi[KPL], mid[KPL];
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const int k = lane + 32 * q;
+                        if (k < c) gram_iv(col, cf[k], sv[q], gamc, lo[q], hi[q], mid[q]);
+                        else lo[q] = hi[q] = mid[q] = INFINITY;
+                    }
+                    st = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, to);
+                    if (st == 1) {  // stash Ŝ_from[j], Ŝ_to[j] for the update
+                        double vf = 0.0, vt = 0.0;
+#pragma unroll
+                        for (int q = 0; q < KPL; ++q) {
+                            if (q == (from >> 5)) vf = __shfl_sync(0xffffffffu, sv[q], from & 31);
+                            if (q == (to >> 5)) vt = __shfl_sync(0xffffffffu, sv[q], to & 31);
+                        }
+                        if (lane == 0) {
+                            s_sv[par][warp][0] = vf;
+                            s_sv[par][warp][1] = vt;
+                        }
+                    }
+                }
+            }
+            if (lane == 0) s_res[par][warp] = st | ((to < 0 ? 0 : to) << 2) | (wfrom << 17);
+            gcl_sync();
+            // ---- every warp: the first candidate of the window, CTA by CTA
+            int v[GRAM_MAXCL];
+#pragma unroll
+            for (int r = 0; r < GRAM_MAXCL; ++r)
+                if (r < CL) v[r] = gcl_ld_i32(gcl_map(&s_res[par][lane], (uint32_t)r));
+            int pr = -1, pw = 0, w = 0;
+#pragma unroll
+            for (int r = 0; r < GRAM_MAXCL; ++r)
+                if (r < CL && pr < 0) {
+                    const unsigned bal = __ballot_sync(0xffffffffu, (v[r] & 3) != 0);
+                    if (bal) {
+                        pr = r;
+                        pw = __ffs(bal) - 1;
+                        w = __shfl_sync(0xffffffffu, v[r], pw);
+                    }
+                }
+            ++windows;
+            lap(0);
+            if (pr < 0) {
+                cursor += W;
+                par ^= 1;
+                continue;
+            }
+            const int jj = cursor + 32 * pr + pw;
+            cursor = jj + 1;
+            // the column's label as its warp read it (labels[jj] is rewritten below)
+            const int from = w >> 17;
+            int mst = w & 3, mto = (w >> 2) & 0x7fff;
+            double sf = 0.0, stv = 0.0;
+            if (mst == 1) {
+                sf = gcl_ld_f64(gcl_map(&s_sv[par][pw][0], (uint32_t)pr));
+                stv = gcl_ld_f64(gcl_map(&s_sv[par][pw][1], (uint32_t)pr));
+            } else {
+                // ---- near-tie (CTA 0): the reference's own chain on the
+                //      reference's centroids (logged moves replayed, kmeans.cpp:128-129)
+                ++fallbacks;
+                if (rank == 0) {
+                    for (int64_t i = tid; i < d; i += blockDim.x) {
+                        for (int e = replayed; e < nlog; ++e) {
+                            const int* lg = a.log + 5 * (int64_t)e;
+                            const int m = __ldcg(lg), f = __ldcg(lg + 1), t = __ldcg(lg + 2);
+                            const double nf = (double)__ldcg(lg + 3), nt = (double)__ldcg(lg + 4);
+                            const double x = (double)M[(int64_t)m * d + i];
+                            double* cfp = a.Cs + (int64_t)f * d + i;
+                            double* ctp = a.Cs + (int64_t)t * d + i;
+                            *cfp = (*cfp * nf - x) / (nf - 1.0);
+                            *ctp = (*ctp * nt + x) / (nt + 1.0);
+                        }
+                    }
+                    __syncthreads();
+                    for (int k = tid; k < c; k += blockDim.x) {  // kmeans.cpp:12-19
+                        const T* x = M + (int64_t)jj * d;
+                        const double* ck = a.Cs + (int64_t)k * d;
+                        double s = 0.0;
+                        for (int64_t i = 0; i < d; ++i) {
+                            const double t = (double)x[i] - ck[i];
+                            s += t * t;
+                        }
+                        dist[k] = s;
+                    }
+                    __syncthreads();
+                    if (warp == 0) {
+                        double lo[KPL], hi[KPL], mid[KPL];
+#pragma unroll
+                        for (int q = 0; q < KPL; ++q) {
+                            const int k = lane + 32 * q;
+                            lo[q] = hi[q] = mid[q] = k < c ? dist[k] : INFINITY;
+                        }
+                        int t2 = -1;
+                        const int s2 = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, t2);
+                        if (lane == 0) {
+                            // exact values: 2 only for NaN (never moves)
+                            s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;
+                            if (s2 == 1) {
+                                s_xsv[0] = __ldcg(a.S + (int64_t)from * n + jj);
+                                s_xsv[1] = __ldcg(a.S + (int64_t)t2 * n + jj);
+                            }
+                        }
+                    }
+                }
+                replay_work += (unsigned long long)(nlog - replayed);
+                replayed = nlog;
+                gcl_sync();
+                const int xr = gcl_ld_i32(gcl_map(&s_xres, 0));
+                mst = xr & 3;
+                mto = xr >> 2;
+                if (mst == 1) {
+                    sf = gcl_ld_f64(gcl_map(&s_xsv[0], 0));
+                    stv = gcl_ld_f64(gcl_map(&s_xsv[1], 0));
+                }
+                lap(1);
+            }
+            if (mst == 1) {
+                // ---- the move (kmeans.cpp:122-135): replicated scalars on two
+                //      threads of every CTA, this CTA's slice of Ŝ_from, Ŝ_to
+                const int f = from, t = mto;
+                const double gmm = __ldg(a.xx + jj), xnm = __ldg(a.xn + jj), xlm = __ldg(a.xl + jj);
+                int* lg = a.log + 5 * (int64_t)nlog;
+                if (tid == 0) {  // the log holds the counts before the move
+                    if (rank == 0) {
+                        lg[0] = jj;
+                        lg[1] = f;
+                        lg[2] = t;
+                        lg[3] = cnt[f];
+                        __stcg(a.labels + jj, t);
+                    }
+                    gram_side(0, sc[f], cf[f], cnt[f], sf, gmm, xnm, xlm, gamG);
+                }
+                if (tid == 32) {
+                    if (rank == 0) lg[4] = cnt[t];
+                    gram_side(1, sc[t], cf[t], cnt[t], stv, gmm, xnm, xlm, gamG);
+                }
+                const double* gm = a.G + (int64_t)jj * n;
+                double* Sf = a.S + (int64_t)f * n;
+                double* St = a.S + (int64_t)t * n;
+                if (vec2) {
+                    const double2* g2 = reinterpret_cast<const double2*>(gm);
+                    double2* f2 = reinterpret_cast<double2*>(Sf);
+                    double2* t2 = reinterpret_cast<double2*>(St);
+                    constexpr int U = 2;
+                    for (int b = (u0 >> 1) + tid; b < (u1 >> 1); b += U * GRAM_THREADS) {
+                        double2 gv[U], fv[U], tv[U];
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int q = b + u * GRAM_THREADS;
+                            if (q < (u1 >> 1)) {
+                                gv[u] = __ldcg(g2 + q);
+                                fv[u] = __ldcg(f2 + q);
+                                tv[u] = __ldcg(t2 + q);
+                            }
+                        }
+#pragma unroll
+                        for (int u = 0; u < U; ++u) {
+                            const int q = b + u * GRAM_THREADS;
+                            if (q < (u1 >> 1)) {
+                                __stcg(f2 + q, make_double2(fv[u].x - gv[u].x, fv[u].y - gv[u].y));
+                                __stcg(t2 + q, make_double2(tv[u].x + gv[u].x, tv[u].y + gv[u].y));
+                            }
+                        }
+                    }
+                } else {
+                    for (int q = u0 + tid; q < u1; q += GRAM_THREADS) {
+                        const double gv = __ldcg(gm + q);
+                        const double fv = __ldcg(Sf + q), tv = __ldcg(St + q);
+                        __stcg(Sf + q, fv - gv);
+                        __stcg(St + q, tv + gv);
+                    }
+                }
+                ++nlog;
+                ++moves;
+                improved = 1;
+                gcl_sync();
+                lap(2);
+            }
+            par ^= 1;
+        }
+        ++pass;
+        if (!improved || pass >= a.max_pass) break;
+    }
+    if (rank == 0) {
+        for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];
+        if (tid == 0) {
+            a.stats[0] = moves;
+            a.stats[1] = (unsigned long long)pass;
+            a.stats[2] = windows;
+            a.stats[3] = fallbacks;
+            a.stats[4] = replay_work;
+            for (int q = 0; q < 4; ++q) a.stats[5 + q] = tph[q];
+        }
+    }
+    gcl_sync();  // no CTA leaves while another may still read its shared memory
+}
+
+}  // namespace respca_dev

@@ -130,9 +130,6 @@ struct HartGlobal {
     alignas(128) unsigned long long first[3][16];  // per-round election slots, round r uses r % 3
     alignas(128) unsigned long long xres;          // exact-fallback verdict broadcast
     alignas(128) unsigned long long moves, exact_fallbacks, rounds, passes, blocks, refreshed;
-    // flag election: per-CTA candidate + round flag, double-buffered by round parity
-    alignas(128) unsigned long long ecand[2][160];
-    alignas(128) unsigned eflag[2][160];
     unsigned long long t_kernel, t_load, t_cols;  // globaltimer (CTA 0): whole kernel, block loads, column fills
     unsigned long long stale_sum, heavy_blocks;   // CTA 0: stale centroids over all block entries, entries with > 8
     unsigned long long tsub1, tsub2, redos, act_cycles, act_rounds, dq_cycles;
@@ -382,7 +379,6 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     __shared__ int s_lab[MAXQ];
     __shared__ int s_nstale;
     __shared__ __align__(8) uint64_t s_bar;  // column fills (bulk copies)
-    __shared__ unsigned long long s_cand, s_first;  // this CTA's candidate / the elected one
 
 
     const uint32_t col_bytes = (uint32_t)(d * (int64_t)sizeof(T));
@@ -391,7 +387,6 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
     if (tid == 0) {
         mbar_init(&s_bar, 1);
         asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-        s_cand = ~0ULL;
     }
     // ---- replicated sequential state
     for (int k = tid; k < c; k += blockDim.x) {
@@ -800,8 +795,8 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                     __stcg(cd + 1, Es[warp * c + from]);
                     __stcg(cd + 2, to >= 0 ? As[warp * c + to] : 0.0);
                     __stcg(cd + 3, to >= 0 ? Es[warp * c + to] : INFINITY);
-                    __threadfence();  // visible before this CTA's flag (published by thread 0)
-                    atomicMin(&s_cand, pack4(j, st, from, to));
+                    __threadfence();
+                    atomicMin(&hg->first[r % 3][0], pack4(j, st, from, to));
                 }
                 if (a.diag && st == 0 && cnt[from] > 1) {
                     // diagnostics: relative margin of a "no move" decision
@@ -820,45 +815,16 @@ __global__ void __launch_bounds__(512, 1) k_hart_all(const T* __restrict__ M, Ha
                 }
             }
         }
+        // slot (r+1)%3 is next written after this barrier and last read before
+        // barrier r-1 completed, so resetting it here cannot race
+        if (blockIdx.x == 0 && tid == 0) hg->first[(r + 1) % 3][0] = ~0ULL;
         lap(4);
-        // ---- election by flags: every CTA publishes its smallest candidate
-        //      and the round number; every CTA gathers all G and takes the
-        //      minimum (a CTA is never two rounds ahead of another — it needs
-        //      their flags of the round before — so two slots suffice)
-        __syncthreads();
-        const int par = r & 1;
-        if (tid == 0) {
-            __stcg(&hg->ecand[par][blockIdx.x], s_cand);
-            __threadfence();
-            *reinterpret_cast<volatile unsigned*>(&hg->eflag[par][blockIdx.x]) = (unsigned)(r + 1);
-        }
-        if (warp == 0) {
-            unsigned long long m = ~0ULL;
-            for (int g2 = lane; g2 < G; g2 += 32) {
-                volatile unsigned* fl = &hg->eflag[par][g2];
-                while (*fl != (unsigned)(r + 1)) __nanosleep(20);
-            }
-            __threadfence();
-            for (int g2 = lane; g2 < G; g2 += 32) {
-                const unsigned long long v = __ldcg(&hg->ecand[par][g2]);
-                m = v < m ? v : m;
-            }
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-                const unsigned long long w = __shfl_xor_sync(0xffffffffu, m, o);
-                m = w < m ? w : m;
-            }
-            if (lane == 0) {
-                s_first = m;
-                s_cand = ~0ULL;  // next round's candidate
-            }
-        }
-        __syncthreads();
+        grid_barrier(hg);
         lap(5);
 
         // ---- phase 3: settle (identically in every CTA)
         ++rounds;
-        const unsigned long long f = s_first;
+        const unsigned long long f = __ldcg(&hg->first[r % 3][0]);
         if (f == ~0ULL) {
             cursor = bend;
         } else {

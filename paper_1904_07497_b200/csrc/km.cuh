@@ -805,17 +805,51 @@ __global__ void __launch_bounds__(256) k_moved_scale(const double* __restrict__ 
 
 // The reference's exact sequential chains for the Lloyd stop (used only when
 // the tree-summed test lands within 1e-9 of its threshold).
-__global__ void k_moved_scale_exact(const double* __restrict__ next, const double* __restrict__ C,
-                                    int64_t N, double* __restrict__ out) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+// The reference's sequential chains (kmeans.cpp:150-155) on one thread; the
+// other threads stage the next chunk of both operands in shared memory, so the
+// chain runs at add latency instead of load latency.
+constexpr int MSE_CH = 1024;
+__global__ void __launch_bounds__(256) k_moved_scale_exact(const double* __restrict__ next,
+                                                           const double* __restrict__ C, int64_t N,
+                                                           double* __restrict__ out) {
+    __shared__ double sn[2][MSE_CH], sc[2][MSE_CH];
+    const int tid = threadIdx.x;
     double moved = 0.0, scale = 0.0;
-    for (int64_t k = 0; k < N; ++k) {
-        const double t = next[k] - C[k];
-        moved += t * t;
-        scale += C[k] * C[k];
+    const int64_t nch = (N + MSE_CH - 1) / MSE_CH;
+    auto stage = [&](int64_t ch, int b) {
+        const int64_t k0 = ch * MSE_CH;
+        for (int i = tid; i < MSE_CH; i += blockDim.x) {
+            const int64_t k = k0 + i;
+            sn[b][i] = k < N ? next[k] : 0.0;
+            sc[b][i] = k < N ? C[k] : 0.0;
+        }
+    };
+    if (nch > 0) stage(0, 0);
+    __syncthreads();
+    for (int64_t ch = 0; ch < nch; ++ch) {
+        const int b = (int)(ch & 1);
+        if (tid == 0) {
+            const int lim = (int)(N - ch * MSE_CH < MSE_CH ? N - ch * MSE_CH : MSE_CH);
+            for (int i = 0; i < lim; ++i) {
+                const double t = sn[b][i] - sc[b][i];
+                moved += t * t;
+                scale += sc[b][i] * sc[b][i];
+            }
+        } else if (ch + 1 < nch) {
+            // threads 1.. stage the next chunk meanwhile
+            const int64_t k0 = (ch + 1) * MSE_CH;
+            for (int i = tid - 1; i < MSE_CH; i += blockDim.x - 1) {
+                const int64_t k = k0 + i;
+                sn[b ^ 1][i] = k < N ? next[k] : 0.0;
+                sc[b ^ 1][i] = k < N ? C[k] : 0.0;
+            }
+        }
+        __syncthreads();
     }
-    out[0] = moved;
-    out[1] = scale;
+    if (tid == 0) {
+        out[0] = moved;
+        out[1] = scale;
+    }
 }
 
 __global__ void k_count_labels(const int* __restrict__ labels, int n, int* __restrict__ counts) {

@@ -23,6 +23,7 @@
 #include "km.cuh"
 #include "hartigan.cuh"
 #include "hartigan_ws.cuh"
+#include "hart_gram.cuh"
 #include "tc_screen.cuh"
 
 namespace respca_host {
@@ -77,6 +78,24 @@ template <typename T>
 struct LanePool : PoolBase {
     std::vector<std::unique_ptr<KmLane<T>>> lanes;
 };
+
+// cudaFuncSetAttribute only when a kernel needs more dynamic shared memory
+// than already granted: the call is not free while other streams run kernels
+// (restart lanes launch side by side), so each function is raised once.
+inline void smem_at_least(const void* f, size_t bytes) {
+    static std::mutex mu;
+    static std::vector<std::pair<const void*, size_t>> granted;
+    std::lock_guard<std::mutex> g(mu);
+    for (auto& e : granted)
+        if (e.first == f) {
+            if (e.second >= bytes) return;
+            CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+            e.second = bytes;
+            return;
+        }
+    CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    granted.emplace_back(f, bytes);
+}
 
 template <typename T>
 struct KMeansEngine {
@@ -136,7 +155,7 @@ struct KMeansEngine {
         static_assert(TJ == 128, "tile");
         const size_t sm = sizeof(T) * 2 * TJ * 36 + sizeof(double) * 2 * TK * 36;
         auto kf = k_dist_dmma<T, WK, MJ, NK>;
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        smem_at_least((const void*)kf, (size_t)(sm));
         kf<<<grid, 256, sm, st>>>(Mp, C, ver, d, nn, c, cps, part.p, xxp.p);
     }
 
@@ -192,7 +211,7 @@ struct KMeansEngine {
         part.ensure((size_t)ns * n * c);
         xxp.ensure((size_t)ns * n);
         auto kf = k_screen_tc<T>;
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+        smem_at_least((const void*)kf, (size_t)(TC_SMEM));
         kf<<<dim3(tiles, ns), TC_THREADS, TC_SMEM, st>>>(M, tcCb.p, d, d_pad, n, c, kbps, part.p,
                                                          xxp.p, tcerr.p);
         ln.add(2);
@@ -248,7 +267,7 @@ struct KMeansEngine {
         const int kbps = (int)((total_kb + ns - 1) / ns);
         part.ensure((size_t)ns * n * c);
         xxp.ensure((size_t)ns * n);
-        CK(cudaFuncSetAttribute(k_screen_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM));
+        smem_at_least((const void*)k_screen_tma, (size_t)(TC_SMEM));
         k_screen_tma<<<dim3(tiles, ns), TM_THREADS, TC_SMEM, st>>>(mapA, mapB, d, n, c, kbps, part.p, xxp.p,
                                                                    tcerr.p);
         ln.add(2);
@@ -364,7 +383,10 @@ struct KMeansEngine {
         double margin;
         bool v = verdict(h[0], h[1], margin);
         if (margin < 1e-9 && h[0] != 0.0) {  // too close for a tree sum: reference chain
-            k_moved_scale_exact<<<1, 32, 0, st>>>(nxt, C, N, msp.p + 2 * 512);
+            if (trace_on())
+                std::fprintf(stderr, "[respca] lloyd stop: exact chain (moved %.17g scale %.17g margin %.3g)\n", h[0],
+                             h[1], margin);
+            k_moved_scale_exact<<<1, 256, 0, st>>>(nxt, C, N, msp.p + 2 * 512);
             ln.add();
             CK(cudaMemcpyAsync(h, msp.p + 2 * 512, sizeof(h), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
@@ -382,12 +404,20 @@ struct KMeansEngine {
         double* nxt = nextC.p;
         const auto t_lloyd0 = HClock::now();
         for (; it < max_iters; ++it) {
+            const auto ts0 = HClock::now();
             assign(cur, labels);
+            const double ta = since(ts0);
             fetch_labels(labels);
+            const double tf = since(ts0);
             repair_if_needed(cur, labels);
+            const double tr = since(ts0);
             means(nxt);
+            const double tm = since(ts0);
             if (stats) stats->lloyd_steps++;
             const bool stop = stop_test(nxt, cur, tol);
+            if (trace_on() && since(ts0) > 0.015)
+                std::fprintf(stderr, "[respca] slow lloyd step %llu: assign %.4f fetch %.4f repair %.4f means %.4f stop %.4f\n",
+                             (unsigned long long)it, ta, tf, tr, tm, since(ts0));
             std::swap(cur, nxt);
             if (stop) {
                 ++it;
@@ -399,6 +429,9 @@ struct KMeansEngine {
             CK(cudaStreamSynchronize(st));
             stats->t_lloyd += since(t_lloyd0);
         }
+        // lanes enter the refinement together: a persistent grid holds its SMs,
+        // and a lane's short Lloyd kernels queued behind another lane's long
+        // refinement kernel on a shared hardware queue would wait for it
         if (before_hartigan) before_hartigan();
         const auto t_h0 = HClock::now();
         hartigan(C, labels);
@@ -445,6 +478,20 @@ struct KMeansEngine {
         CK(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
         optin -= 4096;  // the kernel's static shared memory + headroom
         const int avail = std::min(HART_MAXG, hart_ctas > 0 ? std::min(hart_ctas, nsm) : nsm);
+        if (const char* e = std::getenv("RESPCA_HART_GEOM")) {  // "cache,cpb,R,stages" (experiments)
+            int ca = 1, cp = 2, rr = 16, stg = 3;
+            if (std::sscanf(e, "%d,%d,%d,%d", &ca, &cp, &rr, &stg) == 4) {
+                HartGeom g;
+                g.cache = ca != 0;
+                g.cpb = cp;
+                g.G = std::max(1, std::min(avail, ceil_div(n, cp)));
+                g.B = g.G * cp;
+                g.R = rr;
+                g.stages = stg;
+                g.smem = hart_smem(cp, g.cache, g.B, rr, stg);
+                if (g.smem <= (size_t)optin) return g;
+            }
+        }
         for (int pass = 0; pass < 2; ++pass) {
             const bool cache = pass == 0;  // owned columns cached in shared memory, else streamed
             for (int cpb = cache ? 8 : 4; cpb >= 1; --cpb) {
@@ -468,7 +515,161 @@ struct KMeansEngine {
         }
         throw InvalidArg("hartigan: c too large for the device's shared memory");
     }
+    // ---- Gram-matrix refinement (hart_gram.cuh).  kmeans(X) computes
+    //      G = XᵀX once; every restart's refinement borrows it for the call.
+    const double* gram = nullptr;  // borrowed G, diag, norm bounds (nullptr: per-pass path)
+    const double *gram_xx = nullptr, *gram_xn = nullptr, *gram_xl = nullptr;
+    cudaEvent_t gram_ev = nullptr;  // G complete on the engine's stream
+    DBuf<double> gG, gxx, gxn, gxl, gS;
+    DBuf<GramScal> gsc;
+    DBuf<int> glog;
+    DBuf<unsigned long long> gstats;
+    static constexpr int kGramMaxC = 256;
+
+    static int gram_env() {  // RESPCA_HART_GRAM: 0 off, 1 on where it fits (default)
+        static const int v = [] {
+            const char* e = std::getenv("RESPCA_HART_GRAM");
+            return e ? std::atoi(e) : 1;
+        }();
+        return v;
+    }
+    bool gram_fits() const {
+        if (gram_env() == 0 || c < 2 || c > kGramMaxC || n > 32768) return false;
+        size_t fr = 0, tot = 0;
+        CK(cudaMemGetInfo(&fr, &tot));
+        return (double)n * (double)n * 8.0 <= 0.4 * (double)fr;
+    }
+    bool gram_path() const { return gram != nullptr && c >= 2 && c <= kGramMaxC && !hart_ws_on(); }
+    double gram_gamma() const { return (2.2 * (double)d + 4.0) * kU; }
+    // G = MᵀM on the FP64 tensor cores + its diagonal bounds; the event marks completion
+    void compute_gram() {
+        gG.ensure((size_t)n * n);
+        gxx.ensure(n);
+        gxn.ensure(n);
+        gxl.ensure(n);
+        const long long nb = ceil_div(n, GR_T);
+        const long long tiles = nb * (nb + 1) / 2;
+        const size_t sm = gram_smem<T>();
+        smem_at_least((const void*)k_gram<T>, (size_t)(sm));
+        cudaEvent_t e0 = nullptr, e1 = nullptr;
+        if (trace_on()) {
+            CK(cudaEventCreate(&e0));
+            CK(cudaEventCreate(&e1));
+            CK(cudaEventRecord(e0, st));
+        }
+        k_gram<T><<<(unsigned)tiles, 256, sm, st>>>(M, d, n, gG.p);
+        if (trace_on()) {
+            CK(cudaEventRecord(e1, st));
+            CK(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, e0, e1));
+            std::fprintf(stderr, "[respca] gram: n=%d d=%lld %lld tiles %.3f ms (%.1f TFLOP/s)\n", n, (long long)d,
+                         tiles, ms, 2.0 * (double)tiles * GR_T * GR_T * (double)d / (ms * 1e-3) / 1e12);
+            cudaEventDestroy(e0);
+            cudaEventDestroy(e1);
+        }
+        k_gram_diag<<<ceil_div(n, 256), 256, 0, st>>>(gG.p, n, gram_gamma(), gxx.p, gxn.p, gxl.p);
+        ln.add(2);
+        if (!gram_ev) CK(cudaEventCreateWithFlags(&gram_ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(gram_ev, st));
+        gram = gG.p;
+        gram_xx = gxx.p;
+        gram_xn = gxn.p;
+        gram_xl = gxl.p;
+    }
+    void lend_gram(KMeansEngine& o) const {
+        o.gram = gram;
+        o.gram_xx = gram_xx;
+        o.gram_xn = gram_xn;
+        o.gram_xl = gram_xl;
+        o.gram_ev = gram_ev;
+    }
+    void drop_gram() {
+        gram = gram_xx = gram_xn = gram_xl = nullptr;
+    }
+    void gram_reserve() {
+        gS.ensure((size_t)n * c);
+        gsc.ensure(c);
+        glog.ensure((size_t)5 * 50 * n);
+        gstats.ensure(16);
+        hst.ensure<unsigned long long>(16);
+    }
+    // hartigan_refine on the Gram matrix: labels (device) in/out; C (device,
+    // the start centroids = means_of(labels)) is scratch for exact fallbacks
+    void hartigan_gram(double* C, int* labels) {
+        upload_groups();
+        gram_reserve();
+        if (gram_ev) CK(cudaStreamWaitEvent(st, gram_ev, 0));
+        const double gamG = gram_gamma();
+        k_gram_s0<<<dim3(ceil_div(n, 256), c), 256, 0, st>>>(gram, goff.p, members.p, n, gS.p);
+        k_gram_scal<<<ceil_div(c, 128), 128, 0, st>>>(gS.p, gram_xn, goff.p, members.p, n, c, gamG, gsc.p);
+        GramArgs a{};
+        a.G = gram;
+        a.xx = gram_xx;
+        a.xn = gram_xn;
+        a.xl = gram_xl;
+        a.S = gS.p;
+        a.scal0 = gsc.p;
+        a.labels = labels;
+        a.counts = counts.p;
+        a.Cs = C;
+        a.log = glog.p;
+        a.stats = gstats.p;
+        a.M = M;
+        a.d = d;
+        a.n = n;
+        a.c = c;
+        a.max_pass = 50;  // kmeans.cpp:101
+        a.gamG = gamG;
+        a.gamc = ((double)d + 3.0) * kU * 1.02;
+        const size_t sm = (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double) + 2 * sizeof(int)) + 64;
+        // one cluster of CL CTAs (one SM each) per restart
+        int CL = std::max(1, std::min(8, n / 1024));
+        if (const char* e = std::getenv("RESPCA_GRAM_CL")) CL = std::max(1, std::min(GRAM_MAXCL, std::atoi(e)));
+        auto launch = [&](auto kf) {
+            smem_at_least((const void*)kf, (size_t)(sm));
+            if (CL > 8) CK(cudaFuncSetAttribute((const void*)kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+            for (;; CL = std::max(1, CL / 2)) {
+                cudaLaunchConfig_t lc = {};
+                lc.gridDim = dim3(CL);
+                lc.blockDim = dim3(GRAM_THREADS);
+                lc.dynamicSmemBytes = sm;
+                lc.stream = st;
+                cudaLaunchAttribute at[1];
+                at[0].id = cudaLaunchAttributeClusterDimension;
+                at[0].val.clusterDim.x = CL;
+                at[0].val.clusterDim.y = 1;
+                at[0].val.clusterDim.z = 1;
+                lc.attrs = at;
+                lc.numAttrs = 1;
+                const cudaError_t e = cudaLaunchKernelEx(&lc, kf, a);
+                if (e == cudaSuccess) break;
+                if (CL == 1) CK(e);
+                (void)cudaGetLastError();  // cluster not schedulable: halve it
+            }
+        };
+        if (c <= 32) launch(k_hart_gram<T, 1>);
+        else if (c <= 64) launch(k_hart_gram<T, 2>);
+        else if (c <= 128) launch(k_hart_gram<T, 4>);
+        else launch(k_hart_gram<T, 8>);
+        ln.add(3);
+        if (stats) {
+            unsigned long long* hh = hst.ensure<unsigned long long>(16);
+            CK(cudaMemcpyAsync(hh, gstats.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            stats->hartigan_moves += hh[0];
+            stats->hartigan_passes += hh[1];
+            stats->hartigan_rounds += hh[2];
+            stats->exact_fallbacks += hh[3];
+            if (trace_on())
+                std::fprintf(stderr, "[respca] hartigan(gram, CL=%d): %llu passes %llu windows %llu moves %llu fallbacks (replayed %llu moves); "
+                             "cycles/1.965GHz: decide %.3fs fallback %.3fs update %.3fs\n",
+                             CL, hh[1], hh[2], hh[0], hh[3], hh[4], hh[5] / 1.965e9, hh[6] / 1.965e9, hh[7] / 1.965e9);
+        }
+    }
+
     void hart_reserve() {
+        if (gram_path()) gram_reserve();
         const HartGeom g = hart_geometry();
         const size_t nc = (size_t)n * c;
         hA.ensure(nc);
@@ -507,7 +708,7 @@ struct KMeansEngine {
         ln.add();
         const int G = hgm.G, cpb = hgm.cpb;
         auto kf = cpb <= 2 ? k_hart_ws<T, 2> : (cpb <= 4 ? k_hart_ws<T, 4> : k_hart_ws<T, 8>);
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)hgm.smem));
+        smem_at_least((const void*)kf, (size_t)(hgm.smem));
         HartWsArgs a{};
         a.g = hglob.p;
         a.labels = labels;
@@ -565,6 +766,10 @@ struct KMeansEngine {
         groups.build(h_labels.data(), n, c);
         CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
                            cudaMemcpyHostToDevice, st));
+        if (gram_path()) {
+            hartigan_gram(C, labels);
+            return;
+        }
         hart_reserve();
         const HartGeom hgm = hart_geometry();
         if (hart_ws_on()) {
@@ -585,7 +790,7 @@ struct KMeansEngine {
         const bool cache = hgm.cache;
         const size_t smem = hgm.smem;
         auto kf = cpb <= 2 ? k_hart_all<T, 2> : (cpb <= 4 ? k_hart_all<T, 4> : k_hart_all<T, 8>);
-        CK(cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        smem_at_least((const void*)kf, (size_t)(smem));
         HartArgs a{};
         a.g = hglob.p;
         a.labels = labels;
@@ -704,7 +909,7 @@ struct KMeansEngine {
         while ((int)chosen.size() < c) {
             const int last = chosen.back();
             const size_t ppsm = sizeof(T) * 2 * 4 * (32 * 33 + 32);
-            CK(cudaFuncSetAttribute(k_pp_d2<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)ppsm));
+            smem_at_least((const void*)k_pp_d2<T>, (size_t)(ppsm));
             k_pp_d2<T><<<ceil_div(n, 64), 64, ppsm, st>>>(M, d, n, last, d2.p);
             ln.add();
             CK(cudaMemcpyAsync(hd2.data(), d2.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -769,6 +974,11 @@ struct KMeansEngine {
         if (c == 0) throw InvalidArg("kmeans: c must be >= 1");
         if ((int64_t)c > n) throw InvalidArg("kmeans: c exceeds column count");
         const int L = lanes_for(n_restarts);
+        struct GramScope {
+            KMeansEngine* e;
+            ~GramScope() { e->drop_gram(); }
+        } gram_scope{this};
+        if (gram_fits()) compute_gram();
         if (L > 1) {
             kmeans_lanes(L, max_iters, n_restarts, seed, tol, labels, C, inertia_out, iters_out);
         } else {
@@ -850,6 +1060,7 @@ struct KMeansEngine {
             ln_.e.stats = stats ? &ln_.st : nullptr;
             ln_.e.hart_ctas = std::max(1, nsm / L);
             ln_.e.bind(M, d, n, c);
+            lend_gram(ln_.e);
             // every buffer a lane touches is allocated before the lanes run
             // (cudaFree would synchronise the device under them)
             ln_.e.reserve_full_screen();
@@ -960,8 +1171,8 @@ struct KMeansEngine {
                     const double in = e.inertia(ln_.wc.p, ln_.wl.p);
                     if (e.stats) e.stats->t_inertia += since(ti);
                     if (trace_on())
-                        std::fprintf(stderr, "[respca] lane %d restart %llu: seeded at %.3fs, done at %.3fs\n", l,
-                                     (unsigned long long)r, t_pp_end, since(t_k0));
+                        std::fprintf(stderr, "[respca] lane %d restart %llu: seeded at %.3fs, done at %.3fs (lloyd %.3fs, hartigan %.3fs)\n", l,
+                                     (unsigned long long)r, t_pp_end, since(t_k0), ln_.st.t_lloyd, ln_.st.t_hart);
                     if (in < ln_.best_in) {
                         ln_.best_in = in;
                         ln_.best_r = (int)r;
@@ -983,6 +1194,7 @@ struct KMeansEngine {
         std::vector<std::thread> threads;
         for (int l = 0; l < L; ++l) threads.emplace_back(body, l);
         for (auto& t : threads) t.join();
+        for (int l = 0; l < L; ++l) lanes[l]->e.drop_gram();
         if (trace_on()) std::fprintf(stderr, "[respca] lanes joined at %.3fs\n", since(t_k0));
         for (int l = 0; l < L; ++l) {
             auto& lp = lanes[l];
