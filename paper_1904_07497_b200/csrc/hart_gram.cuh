@@ -244,6 +244,7 @@ struct GramArgs {
     const void* M;     // the data (T), for the exact fallback
     int64_t d;
     int n, c, max_pass;
+    int force_exact;   // tests: every candidate goes through the exact fallback
     double gamG, gamc;
 };
 
@@ -351,7 +352,8 @@ RESPCA_DEV int gram_decide(int from, int c, const GramCoef* cf, const int* cnt, 
     return 1;
 }
 
-constexpr int GRAM_THREADS = 1024;
+constexpr int GRAM_THREADS = 512;
+constexpr int GRAM_WARPS = GRAM_THREADS / 32;
 
 // The move m: from → to (kmeans.cpp:122-135) on one side's scalars (side 0 =
 // from, 1 = to): Q, A, ES, EQ, Δ and the decision coefficients.  sv = Ŝ_k[m]
@@ -411,13 +413,34 @@ RESPCA_DEV uint32_t gcl_size() {
 }
 constexpr int GRAM_MAXCL = 16;
 
+// A move's new per-centroid state for both sides (what every CTA's replica
+// takes over once the move is elected), as 8-byte words for DSMEM copies.
+struct GramSpec {
+    GramScal s[2];
+    GramCoef cf[2];
+    double cnt[2];  // new counts (exact small integers)
+};
+constexpr int GRAM_SPEC_WORDS = sizeof(GramSpec) / 8;
+
+RESPCA_DEV void gcl_st_i32(uint32_t a, int v) {
+    asm volatile("st.shared::cluster.b32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
+}
+RESPCA_DEV double gcl_ld_w(uint32_t a) { return gcl_ld_f64(a); }
+
 // One thread-block cluster per restart.  Every CTA keeps a replica of the
-// per-centroid state (identical updates from identical inputs); a window of
-// 32·CL columns is decided by all warps of the cluster (CTA r, warp w →
-// column cursor + 32r + w); the first column that is not provably "no move"
-// is found by every warp from the CTAs' window results (DSMEM); a move updates
-// Ŝ_from, Ŝ_to on every CTA's slice of the n columns.  One cluster barrier per
-// window and one per move.
+// per-centroid state.  A window of GRAM_WARPS·CL columns is decided by all
+// warps of the cluster (CTA r, warp w → column cursor + GRAM_WARPS·r + w); each
+// warp pushes its verdict into every CTA's shared memory, so after the one
+// cluster barrier per window every warp finds the first column that is not
+// provably "no move" from local shared memory.  A warp that finds a provable
+// move also computes the move's new per-centroid state (both sides)
+// speculatively; if its column is elected, every CTA copies it (DSMEM) into
+// its replica.  The move's O(n) update is applied during the next window, off
+// the critical path:
+//   * each deciding warp applies it to its own column's Ŝ_from, Ŝ_to in
+//     registers (one Ĝ element) before deciding, and writes them back;
+//   * each CTA applies it to its slice of the other columns while its warps
+//     decide (loads first, stores after).
 template <typename T, int KPL>
 __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -427,18 +450,21 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
     double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
     int* cnt = reinterpret_cast<int*>(dist + c);
-    __shared__ int s_res[2][32];         // per window parity: status | to << 2 | from << 17
-    __shared__ double s_sv[2][32][2];    // Ŝ_from[j], Ŝ_to[j] of a provable move
-    __shared__ int s_xres;               // exact fallback verdict (CTA 0)
-    __shared__ double s_xsv[2];
+    __shared__ int s_res[2][GRAM_MAXCL][GRAM_WARPS];  // every CTA's verdicts: status | to << 2 | from << 17
+    __shared__ __align__(16) GramSpec s_spec[2][GRAM_WARPS];  // this CTA's speculative move states
+    __shared__ int s_xres;                            // exact fallback verdict (CTA 0)
+    __shared__ __align__(16) GramSpec s_xspec;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rank = (int)gcl_rank(), CL = (int)gcl_size();
-    const int W = 32 * CL;
+    const int W = GRAM_WARPS * CL;
     const T* M = static_cast<const T*>(a.M);
     const double gamG = a.gamG, gamc = a.gamc;
-    // this CTA's slice of the O(n) update (even bounds: double2 access)
-    const int per = ((n + CL - 1) / CL + 1) & ~1;
+    // this CTA's slice of the O(n) update
+    const int per = (n + CL - 1) / CL;
     const int u0 = min(n, rank * per), u1 = min(n, u0 + per);
+    constexpr int UPT = 3;  // slice elements per thread held across the window
+    // my verdict slot in every CTA of the cluster
+    uint32_t res_slot[2] = {0, 0};
 
     for (int k = tid; k < c; k += blockDim.x) {
         const int ck = a.counts[k];
@@ -447,9 +473,10 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
         gram_coef(sc[k], ck, cf[k]);
     }
     __syncthreads();
+    gcl_sync();  // every replica initialised before remote stores land
 
     unsigned long long moves = 0, windows = 0, fallbacks = 0, replay_work = 0;
-    unsigned long long tph[4] = {0, 0, 0, 0};  // SM cycles (thread 0): decide+pick, fallback, update, -
+    unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SM cycles (thread 0): see the host trace
     unsigned long long tmk = clock64();
     auto lap = [&](int slot) {
         if (tid == 0) {
@@ -458,29 +485,84 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             tmk = t;
         }
     };
+    // the speculative state of a move found by this warp at column j (lanes 0, 1)
+    auto speculate = [&](GramSpec* out, int j, int f, int t, double sf, double stv, double gmm, double xnm) {
+        if (lane < 2) {
+            const double xlm = __ldg(a.xl + j);
+            GramScal S = sc[lane ? t : f];
+            GramCoef C = cf[lane ? t : f];
+            int ck = cnt[lane ? t : f];
+            gram_side(lane, S, C, ck, lane ? stv : sf, gmm, xnm, xlm, gamG);
+            out->s[lane] = S;
+            out->cf[lane] = C;
+            out->cnt[lane] = (double)ck;
+        }
+    };
     int nlog = 0, replayed = 0, pass = 0, par = 0;
-    const bool vec2 = (n % 2) == 0;
+    // the pending move (uniform over the cluster)
+    int pj = -1, pf = 0, pt = 0;
     for (;;) {
         int improved = 0;
         int cursor = 0;
         while (cursor < n) {
-            // ---- decide the window (warp per column, lanes over k)
-            const int j = cursor + 32 * rank + warp;
-            int st = 0, to = -1, wfrom = 0;
+            const int j = cursor + GRAM_WARPS * rank + warp;
+            const bool mv = pj >= 0;
+            // ---- (1) loads: the window column, and this thread's slice of the pending update
+            double sv[KPL];
+            int from = 0;
+            double gjj = 0.0, xnj = 0.0, gj = 0.0;
             if (j < n) {
-                double sv[KPL];
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) {
                     const int k = lane + 32 * q;
                     sv[q] = k < c ? __ldcg(a.S + (int64_t)k * n + j) : 0.0;
                 }
-                const int from = __ldcg(a.labels + j);
-                wfrom = from;
-                GramCol col;
-                col.gjj = __ldg(a.xx + j);
-                col.xnj = __ldg(a.xn + j);
+                from = j == pj ? pt : __ldcg(a.labels + j);  // labels[pj] is published below
+                gjj = __ldg(a.xx + j);
+                xnj = __ldg(a.xn + j);
+                if (mv) gj = __ldcg(a.G + (int64_t)pj * n + j);
+            }
+            double ug[UPT], uf[UPT], ut[UPT];
+            if (mv) {
+#pragma unroll
+                for (int e = 0; e < UPT; ++e) {
+                    const int q = u0 + tid + e * GRAM_THREADS;
+                    if (q < u1 && (q < cursor || q >= cursor + W)) {
+                        ug[e] = __ldcg(a.G + (int64_t)pj * n + q);
+                        uf[e] = __ldcg(a.S + (int64_t)pf * n + q);
+                        ut[e] = __ldcg(a.S + (int64_t)pt * n + q);
+                    }
+                }
+            }
+            lap(2);
+            // ---- (2) the replicas take over the elected move's state (published by
+            //      the warp that found it, or by CTA 0 after an exact fallback)
+            if (mv) {
+                ++nlog;
+                __syncthreads();
+            }
+            lap(3);
+            // ---- (3) decide the window column (lanes over k)
+            int st = 0, to = -1;
+            if (j < n) {
+                if (mv) {  // this column's Ŝ_from, Ŝ_to after the pending move
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const int k = lane + 32 * q;
+                        if (k == pf) {
+                            sv[q] = sv[q] - gj;
+                            __stcg(a.S + (int64_t)k * n + j, sv[q]);
+                        } else if (k == pt) {
+                            sv[q] = sv[q] + gj;
+                            __stcg(a.S + (int64_t)k * n + j, sv[q]);
+                        }
+                    }
+                }
                 if (cnt[from] > 1) {
-                    col.gq = gamG * col.xnj * col.xnj * (1.0 + 4.0 * kU) + 7.1 * kU * col.gjj;
+                    GramCol col;
+                    col.gjj = gjj;
+                    col.xnj = xnj;
+                    col.gq = gamG * xnj * xnj * (1.0 + 4.0 * kU) + 7.1 * kU * gjj;
                     double lo[KPL], hi[KPL], mid[KPL];
 #pragma unroll
                     for (int q = 0; q < KPL; ++q) {
@@ -489,38 +571,64 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         else lo[q] = hi[q] = mid[q] = INFINITY;
                     }
                     st = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, to);
-                    if (st == 1) {  // stash Ŝ_from[j], Ŝ_to[j] for the update
+                    if (a.force_exact && st == 1) st = 2;
+                    if (st != 0 && lane == 0 && j + 1 < n) {
+                        // a candidate: the Ĝ elements the next window's columns need, to L2
+                        const int e1 = min(n, j + 1 + W);
+                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.G + (int64_t)j * n + j + 1);
+                        const uintptr_t s0 = b0 & ~(uintptr_t)15;
+                        const unsigned bytes = (unsigned)((b0 + (uintptr_t)(e1 - j - 1) * 8 - s0 + 15) & ~(uintptr_t)15);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s0), "r"(bytes) : "memory");
+                    }
+                    if (st == 1) {  // speculative move state: Ŝ_from[j], Ŝ_to[j] from the lanes
                         double vf = 0.0, vt = 0.0;
 #pragma unroll
                         for (int q = 0; q < KPL; ++q) {
                             if (q == (from >> 5)) vf = __shfl_sync(0xffffffffu, sv[q], from & 31);
                             if (q == (to >> 5)) vt = __shfl_sync(0xffffffffu, sv[q], to & 31);
                         }
-                        if (lane == 0) {
-                            s_sv[par][warp][0] = vf;
-                            s_sv[par][warp][1] = vt;
-                        }
+                        speculate(&s_spec[par][warp], j, from, to, vf, vt, gjj, xnj);
                     }
                 }
             }
-            if (lane == 0) s_res[par][warp] = st | ((to < 0 ? 0 : to) << 2) | (wfrom << 17);
-            gcl_sync();
-            // ---- every warp: the first candidate of the window, CTA by CTA
-            int v[GRAM_MAXCL];
+            lap(4);
+            // ---- (4) push the verdict to every CTA; this thread's slice of the pending update
+            if (lane < CL)
+                gcl_st_i32(gcl_map(&s_res[par][rank][warp], (uint32_t)lane),
+                           st | ((to < 0 ? 0 : to) << 2) | (from << 17));
+            if (mv) {
 #pragma unroll
-            for (int r = 0; r < GRAM_MAXCL; ++r)
-                if (r < CL) v[r] = gcl_ld_i32(gcl_map(&s_res[par][lane], (uint32_t)r));
-            int pr = -1, pw = 0, w = 0;
-#pragma unroll
-            for (int r = 0; r < GRAM_MAXCL; ++r)
-                if (r < CL && pr < 0) {
-                    const unsigned bal = __ballot_sync(0xffffffffu, (v[r] & 3) != 0);
-                    if (bal) {
-                        pr = r;
-                        pw = __ffs(bal) - 1;
-                        w = __shfl_sync(0xffffffffu, v[r], pw);
+                for (int e = 0; e < UPT; ++e) {
+                    const int q = u0 + tid + e * GRAM_THREADS;
+                    if (q < u1 && (q < cursor || q >= cursor + W)) {
+                        __stcg(a.S + (int64_t)pf * n + q, uf[e] - ug[e]);
+                        __stcg(a.S + (int64_t)pt * n + q, ut[e] + ug[e]);
                     }
                 }
+                // slices longer than UPT·GRAM_THREADS (small clusters): the rest in place
+                for (int q = u0 + tid + UPT * GRAM_THREADS; q < u1; q += GRAM_THREADS)
+                    if (q < cursor || q >= cursor + W) {
+                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
+                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
+                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
+                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
+                    }
+                pj = -1;
+            }
+            lap(5);
+            gcl_sync();
+            lap(6);
+            // ---- (5) every warp: the first candidate of the window, CTA by CTA (local)
+            int pr = -1, pw = 0, w = 0;
+            for (int r = 0; r < CL && pr < 0; ++r) {
+                const int v = lane < GRAM_WARPS ? s_res[par][r][lane] : 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
+                if (bal) {
+                    pr = r;
+                    pw = __ffs(bal) - 1;
+                    w = __shfl_sync(0xffffffffu, v, pw);
+                }
+            }
             ++windows;
             lap(0);
             if (pr < 0) {
@@ -528,15 +636,13 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 par ^= 1;
                 continue;
             }
-            const int jj = cursor + 32 * pr + pw;
+            const int jj = cursor + GRAM_WARPS * pr + pw;
             cursor = jj + 1;
-            // the column's label as its warp read it (labels[jj] is rewritten below)
-            const int from = w >> 17;
+            const int mfrom = w >> 17;
             int mst = w & 3, mto = (w >> 2) & 0x7fff;
-            double sf = 0.0, stv = 0.0;
+            uint32_t spec_src = 0;
             if (mst == 1) {
-                sf = gcl_ld_f64(gcl_map(&s_sv[par][pw][0], (uint32_t)pr));
-                stv = gcl_ld_f64(gcl_map(&s_sv[par][pw][1], (uint32_t)pr));
+                spec_src = gcl_map(&s_spec[par][pw], (uint32_t)pr);
             } else {
                 // ---- near-tie (CTA 0): the reference's own chain on the
                 //      reference's centroids (logged moves replayed, kmeans.cpp:128-129)
@@ -574,14 +680,12 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                             lo[q] = hi[q] = mid[q] = k < c ? dist[k] : INFINITY;
                         }
                         int t2 = -1;
-                        const int s2 = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, t2);
-                        if (lane == 0) {
-                            // exact values: 2 only for NaN (never moves)
-                            s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;
-                            if (s2 == 1) {
-                                s_xsv[0] = __ldcg(a.S + (int64_t)from * n + jj);
-                                s_xsv[1] = __ldcg(a.S + (int64_t)t2 * n + jj);
-                            }
+                        const int s2 = gram_decide<KPL>(mfrom, c, cf, cnt, lo, hi, mid, t2);
+                        if (lane == 0) s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;  // exact: 2 only for NaN
+                        if (s2 == 1) {
+                            const double sf = __ldcg(a.S + (int64_t)mfrom * n + jj);
+                            const double stv = __ldcg(a.S + (int64_t)t2 * n + jj);
+                            speculate(&s_xspec, jj, mfrom, t2, sf, stv, __ldg(a.xx + jj), __ldg(a.xn + jj));
                         }
                     }
                 }
@@ -591,79 +695,53 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 const int xr = gcl_ld_i32(gcl_map(&s_xres, 0));
                 mst = xr & 3;
                 mto = xr >> 2;
-                if (mst == 1) {
-                    sf = gcl_ld_f64(gcl_map(&s_xsv[0], 0));
-                    stv = gcl_ld_f64(gcl_map(&s_xsv[1], 0));
-                }
+                spec_src = gcl_map(&s_xspec, 0);
                 lap(1);
             }
             if (mst == 1) {
-                // ---- the move (kmeans.cpp:122-135): replicated scalars on two
-                //      threads of every CTA, this CTA's slice of Ŝ_from, Ŝ_to
-                const int f = from, t = mto;
-                const double gmm = __ldg(a.xx + jj), xnm = __ldg(a.xn + jj), xlm = __ldg(a.xl + jj);
-                int* lg = a.log + 5 * (int64_t)nlog;
-                if (tid == 0) {  // the log holds the counts before the move
-                    if (rank == 0) {
+                // pending for the next window: the log (CTA 0) and the replicas
+                // take the elected state now (warp 0), the Ŝ update later
+                if (warp == 0) {
+                    const int f = mfrom, t = mto;
+                    if (lane == 0 && rank == 0) {  // the log holds the counts before the move
+                        int* lg = a.log + 5 * (int64_t)nlog;
                         lg[0] = jj;
                         lg[1] = f;
                         lg[2] = t;
                         lg[3] = cnt[f];
+                        lg[4] = cnt[t];
                         __stcg(a.labels + jj, t);
                     }
-                    gram_side(0, sc[f], cf[f], cnt[f], sf, gmm, xnm, xlm, gamG);
-                }
-                if (tid == 32) {
-                    if (rank == 0) lg[4] = cnt[t];
-                    gram_side(1, sc[t], cf[t], cnt[t], stv, gmm, xnm, xlm, gamG);
-                }
-                const double* gm = a.G + (int64_t)jj * n;
-                double* Sf = a.S + (int64_t)f * n;
-                double* St = a.S + (int64_t)t * n;
-                if (vec2) {
-                    const double2* g2 = reinterpret_cast<const double2*>(gm);
-                    double2* f2 = reinterpret_cast<double2*>(Sf);
-                    double2* t2 = reinterpret_cast<double2*>(St);
-                    constexpr int U = 2;
-                    for (int b = (u0 >> 1) + tid; b < (u1 >> 1); b += U * GRAM_THREADS) {
-                        double2 gv[U], fv[U], tv[U];
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int q = b + u * GRAM_THREADS;
-                            if (q < (u1 >> 1)) {
-                                gv[u] = __ldcg(g2 + q);
-                                fv[u] = __ldcg(f2 + q);
-                                tv[u] = __ldcg(t2 + q);
-                            }
-                        }
-#pragma unroll
-                        for (int u = 0; u < U; ++u) {
-                            const int q = b + u * GRAM_THREADS;
-                            if (q < (u1 >> 1)) {
-                                __stcg(f2 + q, make_double2(fv[u].x - gv[u].x, fv[u].y - gv[u].y));
-                                __stcg(t2 + q, make_double2(tv[u].x + gv[u].x, tv[u].y + gv[u].y));
-                            }
-                        }
-                    }
-                } else {
-                    for (int q = u0 + tid; q < u1; q += GRAM_THREADS) {
-                        const double gv = __ldcg(gm + q);
-                        const double fv = __ldcg(Sf + q), tv = __ldcg(St + q);
-                        __stcg(Sf + q, fv - gv);
-                        __stcg(St + q, tv + gv);
+                    double wv = 0.0;
+                    if (lane < GRAM_SPEC_WORDS) wv = gcl_ld_w(spec_src + 8u * (uint32_t)lane);
+                    __syncwarp();
+                    if (lane < GRAM_SPEC_WORDS) {
+                        GramSpec* loc = &s_xspec;  // staging: reuse is safe (see below)
+                        (void)loc;
+                        // scatter the words into the replica
+                        const int side = lane < 5 ? 0 : lane < 10 ? 1 : lane < 17 ? 0 : lane < 24 ? 1 : lane - 24;
+                        const int k = side ? t : f;
+                        double* dst;
+                        if (lane < 10) dst = reinterpret_cast<double*>(&sc[k]) + (lane < 5 ? lane : lane - 5);
+                        else if (lane < 24) dst = reinterpret_cast<double*>(&cf[k]) + (lane < 17 ? lane - 10 : lane - 17);
+                        else dst = nullptr;
+                        if (dst) *dst = wv;
+                        else cnt[k] = (int)wv;
                     }
                 }
-                ++nlog;
+                pj = jj;
+                pf = mfrom;
+                pt = mto;
                 ++moves;
                 improved = 1;
-                gcl_sync();
-                lap(2);
             }
             par ^= 1;
         }
         ++pass;
         if (!improved || pass >= a.max_pass) break;
     }
+    // the last move's label was written when it was elected; its Ŝ update is not needed
+    __syncthreads();
     if (rank == 0) {
         for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];
         if (tid == 0) {
@@ -672,7 +750,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             a.stats[2] = windows;
             a.stats[3] = fallbacks;
             a.stats[4] = replay_work;
-            for (int q = 0; q < 4; ++q) a.stats[5 + q] = tph[q];
+            for (int q = 0; q < 8; ++q) a.stats[5 + q] = tph[q];
         }
     }
     gcl_sync();  // no CTA leaves while another may still read its shared memory

@@ -620,6 +620,7 @@ struct KMeansEngine {
         a.n = n;
         a.c = c;
         a.max_pass = 50;  // kmeans.cpp:101
+        a.force_exact = env_int("RESPCA_GRAM_FORCE_EXACT", 0);
         a.gamG = gamG;
         a.gamc = ((double)d + 3.0) * kU * 1.02;
         const size_t sm = (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double) + 2 * sizeof(int)) + 64;
@@ -653,18 +654,21 @@ struct KMeansEngine {
         else if (c <= 128) launch(k_hart_gram<T, 4>);
         else launch(k_hart_gram<T, 8>);
         ln.add(3);
-        if (stats) {
+        if (stats || trace_on()) {
             unsigned long long* hh = hst.ensure<unsigned long long>(16);
             CK(cudaMemcpyAsync(hh, gstats.p, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
-            stats->hartigan_moves += hh[0];
-            stats->hartigan_passes += hh[1];
-            stats->hartigan_rounds += hh[2];
-            stats->exact_fallbacks += hh[3];
+            if (stats) {
+                stats->hartigan_moves += hh[0];
+                stats->hartigan_passes += hh[1];
+                stats->hartigan_rounds += hh[2];
+                stats->exact_fallbacks += hh[3];
+            }
             if (trace_on())
                 std::fprintf(stderr, "[respca] hartigan(gram, CL=%d): %llu passes %llu windows %llu moves %llu fallbacks (replayed %llu moves); "
-                             "cycles/1.965GHz: decide %.3fs fallback %.3fs update %.3fs\n",
-                             CL, hh[1], hh[2], hh[0], hh[3], hh[4], hh[5] / 1.965e9, hh[6] / 1.965e9, hh[7] / 1.965e9);
+                             "s at 1.965GHz: pick %.3f fallback %.3f loads %.3f sync %.3f decide %.3f push+slice %.3f barrier %.3f\n",
+                             CL, hh[1], hh[2], hh[0], hh[3], hh[4], hh[5] / 1.965e9, hh[6] / 1.965e9, hh[7] / 1.965e9, hh[8] / 1.965e9, hh[9] / 1.965e9, hh[10] / 1.965e9,
+                             hh[11] / 1.965e9);
         }
     }
 
@@ -978,9 +982,11 @@ struct KMeansEngine {
             KMeansEngine* e;
             ~GramScope() { e->drop_gram(); }
         } gram_scope{this};
-        if (gram_fits()) compute_gram();
+        const bool want_gram = gram_fits();
+        const bool overlap = L > 1 && env_int("RESPCA_GRAM_OVERLAP", 1) != 0;
+        if (want_gram && !overlap) compute_gram();
         if (L > 1) {
-            kmeans_lanes(L, max_iters, n_restarts, seed, tol, labels, C, inertia_out, iters_out);
+            kmeans_lanes(L, max_iters, n_restarts, seed, tol, labels, C, inertia_out, iters_out, want_gram && overlap);
         } else {
             std::mt19937_64 rng(seed);
             double best = std::numeric_limits<double>::infinity();
@@ -1037,7 +1043,7 @@ struct KMeansEngine {
     // smallest inertia (strict <, kmeans.cpp:246); the first restart that
     // throws decides the exception.
     void kmeans_lanes(int L, uint64_t max_iters, uint64_t n_restarts, uint64_t seed, double tol,
-                      int* labels, double* C, double* inertia_out, uint64_t* iters_out) {
+                      int* labels, double* C, double* inertia_out, uint64_t* iters_out, bool want_gram = false) {
         int dev = 0, nsm = 148;
         CK(cudaGetDevice(&dev));
         CK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
@@ -1048,6 +1054,9 @@ struct KMeansEngine {
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, st));  // M is complete on the caller's stream
+        // G = MᵀM on the caller's stream, overlapping the lanes' seeding and
+        // Lloyd steps; the refinements wait for it (gram_ev)
+        if (want_gram) compute_gram();
         while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
             CK(cudaStreamCreateWithFlags(&lanes.back()->e.st, cudaStreamNonBlocking));

@@ -1,0 +1,98 @@
+"""The Gram-matrix Hartigan refinement (csrc/hart_gram.cuh) against the oracle's
+kmeans (kmeans.cpp:96-139, 237-250): labels, centroids, inertia and Lloyd
+iterations bit-identical, on data built to stress it —
+
+* integer-valued columns (exact distance ties),
+* duplicate columns, tiny and large magnitudes,
+* clusters of 1, 2, 4 and 8 CTAs (RESPCA_GRAM_CL), the per-pass path
+  (RESPCA_HART_GRAM=0) on the same inputs, and every move forced through the
+  exact fallback (RESPCA_GRAM_FORCE_EXACT=1: the logged moves are replayed
+  onto the reference's centroids and the reference's own chain decides).
+
+Each configuration runs in a subprocess: the switches are read once per
+process.  RESPCA_TRACE=1 makes the engine report which refinement ran and how
+many exact fallbacks it took."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+from oracle import oracle as O
+from paper_1904_07497_b200 import respca as R
+from paper_1904_07497_b200.respca import KMeansConfig
+from helpers import bitwise
+orc = O.port()
+rng = np.random.default_rng(7)
+cases = []
+# integer grid: many exact ties
+cases.append(("ints", rng.integers(-2, 3, (8, 600)).astype(float), 6, 3, 3))
+cases.append(("ints-wide", rng.integers(-1, 2, (5, 1500)).astype(float), 12, 1, 2))
+# duplicates + a perturbed copy
+base = rng.uniform(-1, 1, (16, 40))
+dup = np.asfortranarray(np.concatenate([base] * 6, axis=1))
+dup[:, 3] += 1e-9
+cases.append(("dups", dup, 7, 5, 2))
+# magnitudes far from 1
+cases.append(("tiny", rng.normal(0, 1e-150, (24, 700)), 9, 2, 2))
+cases.append(("large", rng.normal(0, 1e150, (24, 700)), 9, 4, 2))
+# mixture with a sparse heavy part (the RPCA shape)
+X = rng.normal(0, 1, (64, 2500)) + (rng.random((64, 2500)) < 0.1) * rng.uniform(-50, 50, (64, 2500))
+cases.append(("rpca", X, 20, 11, 2))
+bad = 0
+for name, m, c, seed, restarts in cases:
+    m = np.asfortranarray(m)
+    a = R.kmeans(m, KMeansConfig(c=c, seed=seed, n_restarts=restarts))
+    lab, cen, inertia, it = orc.kmeans(m, c, 100, restarts, seed, 1e-6)
+    ok = (a.assignment == lab).all() and bitwise(a.centroids, cen) and a.inertia == inertia and a.iters_run == it
+    print("CASE", name, "OK" if ok else "BAD", int((a.assignment != lab).sum()), flush=True)
+    bad += not ok
+sys.exit(1 if bad else 0)
+"""
+
+
+def run(env_extra):
+    env = dict(os.environ, RESPCA_TRACE="1", **env_extra)
+    r = subprocess.run([sys.executable, "-c", SCRIPT], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=600)
+    return r
+
+
+@pytest.mark.parametrize("cl", ["1", "2", "4", "8"])
+def test_gram_refinement_bitwise(cl):
+    r = run({"RESPCA_GRAM_CL": cl})
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK ") == 6, r.stdout
+    # the Gram refinement ran, with the requested cluster size
+    runs = [ln for ln in r.stderr.splitlines() if "hartigan(gram, CL=" in ln]
+    assert runs and all(f"CL={cl})" in ln for ln in runs), r.stderr[-2000:]
+
+
+def fallbacks(stderr):
+    return sum(int(ln.split(" fallbacks")[0].split()[-1]) for ln in stderr.splitlines()
+               if "hartigan(gram, CL=" in ln)
+
+
+@pytest.mark.parametrize("cl", ["1", "4"])
+def test_gram_exact_fallback_bitwise(cl):
+    """Every provable move routed through the exact fallback (log replay onto
+    the reference's centroids + the reference's chain): same results."""
+    r = run({"RESPCA_GRAM_CL": cl, "RESPCA_GRAM_FORCE_EXACT": "1"})
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK ") == 6, r.stdout
+    assert fallbacks(r.stderr) > 100, r.stderr[-2000:]
+
+
+def test_per_pass_refinement_bitwise():
+    r = run({"RESPCA_HART_GRAM": "0"})
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK ") == 6, r.stdout
+    assert "hartigan(gram" not in r.stderr
