@@ -426,6 +426,9 @@ RESPCA_DEV void gcl_st_i32(uint32_t a, int v) {
     asm volatile("st.shared::cluster.b32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
 }
 RESPCA_DEV double gcl_ld_w(uint32_t a) { return gcl_ld_f64(a); }
+RESPCA_DEV void gcl_st_f64(uint32_t a, double v) {
+    asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
+}
 
 // One thread-block cluster per restart.  Every CTA keeps a replica of the
 // per-centroid state.  A window of GRAM_WARPS·CL columns is decided by all
@@ -450,8 +453,13 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
     double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
     int* cnt = reinterpret_cast<int*>(dist + c);
-    __shared__ int s_res[2][GRAM_MAXCL][GRAM_WARPS];  // every CTA's verdicts: status | to << 2 | from << 17
+    double* swin = reinterpret_cast<double*>(cnt + ((c + 1) & ~1));  // [c][GRAM_WARPS + 1] the window's Ŝ block
+    __shared__ int s_wfrom[GRAM_WARPS];
+    __shared__ double s_wg[GRAM_WARPS][2];            // Ĝ_jj, ‖x_j‖ bound of the window's columns
+    __shared__ int s_loc[2][GRAM_WARPS];              // this CTA's verdicts: status | to << 2 | from << 17
     __shared__ __align__(16) GramSpec s_spec[2][GRAM_WARPS];  // this CTA's speculative move states
+    __shared__ int s_first[2][GRAM_MAXCL][2];         // every CTA's first candidate: verdict, warp
+    __shared__ __align__(16) GramSpec s_fspec[2][GRAM_MAXCL];  // ... and its move state
     __shared__ int s_xres;                            // exact fallback verdict (CTA 0)
     __shared__ __align__(16) GramSpec s_xspec;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -507,21 +515,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
         while (cursor < n) {
             const int j = cursor + GRAM_WARPS * rank + warp;
             const bool mv = pj >= 0;
-            // ---- (1) loads: the window column, and this thread's slice of the pending update
-            double sv[KPL];
-            int from = 0;
-            double gjj = 0.0, xnj = 0.0, gj = 0.0;
-            if (j < n) {
-#pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    const int k = lane + 32 * q;
-                    sv[q] = k < c ? __ldcg(a.S + (int64_t)k * n + j) : 0.0;
-                }
-                from = j == pj ? pt : __ldcg(a.labels + j);  // labels[pj] is published below
-                gjj = __ldg(a.xx + j);
-                xnj = __ldg(a.xn + j);
-                if (mv) gj = __ldcg(a.G + (int64_t)pj * n + j);
-            }
+            // ---- (1) loads: this thread's slice of the pending update, and the
+            //      window's Ŝ block staged in shared memory (coalesced over columns);
+            //      the pending move is applied to the staged Ŝ_from, Ŝ_to entries
             double ug[UPT], uf[UPT], ut[UPT];
             if (mv) {
 #pragma unroll
@@ -534,29 +530,75 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                     }
                 }
             }
-            lap(2);
-            // ---- (2) the replicas take over the elected move's state (published by
-            //      the warp that found it, or by CTA 0 after an exact fallback)
-            if (mv) {
-                ++nlog;
-                __syncthreads();
+            {
+                const int jb = cursor + GRAM_WARPS * rank;
+                constexpr int SPT = (KPL * 32 * GRAM_WARPS + GRAM_THREADS - 1) / GRAM_THREADS;
+                double v[SPT], g[SPT];
+#pragma unroll
+                for (int u = 0; u < SPT; ++u) {  // all loads first
+                    const int e = tid + u * GRAM_THREADS;
+                    const int k = e / GRAM_WARPS, jc = jb + (e - k * GRAM_WARPS);
+                    v[u] = 0.0;
+                    g[u] = 0.0;
+                    if (k < c && jc < n) {
+                        v[u] = __ldcg(a.S + (int64_t)k * n + jc);
+                        if (mv && (k == pf || k == pt)) g[u] = __ldcg(a.G + (int64_t)pj * n + jc);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < SPT; ++u) {
+                    const int e = tid + u * GRAM_THREADS;
+                    const int k = e / GRAM_WARPS, jl = e - k * GRAM_WARPS, jc = jb + jl;
+                    if (k < c) {
+                        double x = v[u];
+                        if (mv && jc < n && (k == pf || k == pt)) {
+                            x = k == pf ? x - g[u] : x + g[u];
+                            __stcg(a.S + (int64_t)k * n + jc, x);
+                        }
+                        swin[k * (GRAM_WARPS + 1) + jl] = x;
+                    }
+                }
+                if (tid < GRAM_WARPS) {
+                    const int jc = jb + tid;
+                    s_wfrom[tid] = jc < n ? (jc == pj ? pt : __ldcg(a.labels + jc)) : 0;  // labels[pj] is published later
+                    s_wg[tid][0] = jc < n ? __ldg(a.xx + jc) : 0.0;
+                    s_wg[tid][1] = jc < n ? __ldg(a.xn + jc) : 0.0;
+                }
             }
+            lap(2);
+            if (mv) ++nlog;
+            __syncthreads();
             lap(3);
+            // ---- (2b) this thread's slice of the pending update (stores drain during the decide)
+            if (mv) {
+#pragma unroll
+                for (int e = 0; e < UPT; ++e) {
+                    const int q = u0 + tid + e * GRAM_THREADS;
+                    if (q < u1 && (q < cursor || q >= cursor + W)) {
+                        __stcg(a.S + (int64_t)pf * n + q, uf[e] - ug[e]);
+                        __stcg(a.S + (int64_t)pt * n + q, ut[e] + ug[e]);
+                    }
+                }
+                // slices longer than UPT·GRAM_THREADS (small clusters): the rest in place
+                for (int q = u0 + tid + UPT * GRAM_THREADS; q < u1; q += GRAM_THREADS)
+                    if (q < cursor || q >= cursor + W) {
+                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
+                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
+                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
+                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
+                    }
+                pj = -1;
+            }
             // ---- (3) decide the window column (lanes over k)
             int st = 0, to = -1;
+            const int from = s_wfrom[warp];
             if (j < n) {
-                if (mv) {  // this column's Ŝ_from, Ŝ_to after the pending move
+                const double gjj = s_wg[warp][0], xnj = s_wg[warp][1];
+                double sv[KPL];
 #pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        const int k = lane + 32 * q;
-                        if (k == pf) {
-                            sv[q] = sv[q] - gj;
-                            __stcg(a.S + (int64_t)k * n + j, sv[q]);
-                        } else if (k == pt) {
-                            sv[q] = sv[q] + gj;
-                            __stcg(a.S + (int64_t)k * n + j, sv[q]);
-                        }
-                    }
+                for (int q = 0; q < KPL; ++q) {
+                    const int k = lane + 32 * q;
+                    sv[q] = k < c ? swin[k * (GRAM_WARPS + 1) + warp] : 0.0;
                 }
                 if (cnt[from] > 1) {
                     GramCol col;
@@ -592,41 +634,46 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 }
             }
             lap(4);
-            // ---- (4) push the verdict to every CTA; this thread's slice of the pending update
-            if (lane < CL)
-                gcl_st_i32(gcl_map(&s_res[par][rank][warp], (uint32_t)lane),
-                           st | ((to < 0 ? 0 : to) << 2) | (from << 17));
-            if (mv) {
-#pragma unroll
-                for (int e = 0; e < UPT; ++e) {
-                    const int q = u0 + tid + e * GRAM_THREADS;
-                    if (q < u1 && (q < cursor || q >= cursor + W)) {
-                        __stcg(a.S + (int64_t)pf * n + q, uf[e] - ug[e]);
-                        __stcg(a.S + (int64_t)pt * n + q, ut[e] + ug[e]);
+            // ---- (4) this warp's verdict
+            if (lane == 0) s_loc[par][warp] = st | ((to < 0 ? 0 : to) << 2) | (from << 17);
+            __syncthreads();
+            // ---- (5) this CTA's first candidate (verdict, warp, move state) → every CTA
+            {
+                const int v = lane < GRAM_WARPS ? s_loc[par][lane] : 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
+                const int fw = bal ? __ffs(bal) - 1 : 0;
+                if (warp == fw) {
+                    const int fv = __shfl_sync(0xffffffffu, v, fw);
+                    if (bal && lane == 0) {
+                        // the first candidate's Ĝ column (every CTA's slice of its update) to L2
+                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.G + (int64_t)(cursor + GRAM_WARPS * rank + fw) * n);
+                        const uintptr_t s0 = b0 & ~(uintptr_t)15;
+                        const unsigned bytes = (unsigned)((b0 + (uintptr_t)n * 8 - s0 + 15) & ~(uintptr_t)15);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s0), "r"(bytes) : "memory");
+                    }
+                    if (lane < CL) {
+                        gcl_st_i32(gcl_map(&s_first[par][rank][0], (uint32_t)lane), bal ? fv : 0);
+                        gcl_st_i32(gcl_map(&s_first[par][rank][1], (uint32_t)lane), fw);
+                    }
+                    if ((fv & 3) == 1 && lane < GRAM_SPEC_WORDS) {
+                        const double word = reinterpret_cast<const double*>(&s_spec[par][fw])[lane];
+                        for (int r = 0; r < CL; ++r)
+                            gcl_st_f64(gcl_map(reinterpret_cast<double*>(&s_fspec[par][rank]) + lane, (uint32_t)r), word);
                     }
                 }
-                // slices longer than UPT·GRAM_THREADS (small clusters): the rest in place
-                for (int q = u0 + tid + UPT * GRAM_THREADS; q < u1; q += GRAM_THREADS)
-                    if (q < cursor || q >= cursor + W) {
-                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
-                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
-                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
-                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
-                    }
-                pj = -1;
             }
             lap(5);
             gcl_sync();
             lap(6);
-            // ---- (5) every warp: the first candidate of the window, CTA by CTA (local)
+            // ---- (6) every warp: the first candidate of the window (local shared memory)
             int pr = -1, pw = 0, w = 0;
-            for (int r = 0; r < CL && pr < 0; ++r) {
-                const int v = lane < GRAM_WARPS ? s_res[par][r][lane] : 0;
+            {
+                const int v = lane < CL ? s_first[par][lane][0] : 0;
                 const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
                 if (bal) {
-                    pr = r;
-                    pw = __ffs(bal) - 1;
-                    w = __shfl_sync(0xffffffffu, v, pw);
+                    pr = __ffs(bal) - 1;
+                    w = __shfl_sync(0xffffffffu, v, pr);
+                    pw = s_first[par][pr][1];
                 }
             }
             ++windows;
@@ -640,9 +687,10 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             cursor = jj + 1;
             const int mfrom = w >> 17;
             int mst = w & 3, mto = (w >> 2) & 0x7fff;
-            uint32_t spec_src = 0;
+            uint32_t spec_src = 0;  // the elected move's state: local copy, or CTA 0's after a fallback
+            const double* spec_loc = nullptr;
             if (mst == 1) {
-                spec_src = gcl_map(&s_spec[par][pw], (uint32_t)pr);
+                spec_loc = reinterpret_cast<const double*>(&s_fspec[par][pr]);
             } else {
                 // ---- near-tie (CTA 0): the reference's own chain on the
                 //      reference's centroids (logged moves replayed, kmeans.cpp:128-129)
@@ -713,7 +761,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         __stcg(a.labels + jj, t);
                     }
                     double wv = 0.0;
-                    if (lane < GRAM_SPEC_WORDS) wv = gcl_ld_w(spec_src + 8u * (uint32_t)lane);
+                    if (lane < GRAM_SPEC_WORDS) wv = spec_loc ? spec_loc[lane] : gcl_ld_w(spec_src + 8u * (uint32_t)lane);
                     __syncwarp();
                     if (lane < GRAM_SPEC_WORDS) {
                         GramSpec* loc = &s_xspec;  // staging: reuse is safe (see below)
@@ -729,6 +777,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         else cnt[k] = (int)wv;
                     }
                 }
+                lap(7);
                 pj = jj;
                 pf = mfrom;
                 pt = mto;

@@ -623,7 +623,8 @@ struct KMeansEngine {
         a.force_exact = env_int("RESPCA_GRAM_FORCE_EXACT", 0);
         a.gamG = gamG;
         a.gamc = ((double)d + 3.0) * kU * 1.02;
-        const size_t sm = (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double) + 2 * sizeof(int)) + 64;
+        const size_t sm = (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double)) +
+                          sizeof(int) * (size_t)((c + 1) & ~1) + sizeof(double) * (size_t)c * (GRAM_WARPS + 1) + 64;
         // one cluster of CL CTAs (one SM each) per restart
         int CL = std::max(1, std::min(8, n / 1024));
         if (const char* e = std::getenv("RESPCA_GRAM_CL")) CL = std::max(1, std::min(GRAM_MAXCL, std::atoi(e)));
@@ -666,9 +667,9 @@ struct KMeansEngine {
             }
             if (trace_on())
                 std::fprintf(stderr, "[respca] hartigan(gram, CL=%d): %llu passes %llu windows %llu moves %llu fallbacks (replayed %llu moves); "
-                             "s at 1.965GHz: pick %.3f fallback %.3f loads %.3f sync %.3f decide %.3f push+slice %.3f barrier %.3f\n",
+                             "s at 1.965GHz: pick %.3f fallback %.3f loads %.3f sync %.3f decide %.3f push+slice %.3f barrier %.3f replica %.3f\n",
                              CL, hh[1], hh[2], hh[0], hh[3], hh[4], hh[5] / 1.965e9, hh[6] / 1.965e9, hh[7] / 1.965e9, hh[8] / 1.965e9, hh[9] / 1.965e9, hh[10] / 1.965e9,
-                             hh[11] / 1.965e9);
+                             hh[11] / 1.965e9, hh[12] / 1.965e9);
         }
     }
 
