@@ -334,7 +334,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
                 print(f"e2e run {rep}: wall {el:.3f}s init {res.init_ms:.0f}ms loop {res.loop_ms:.0f}ms "
                       f"h2d {res.h2d_ms:.0f}ms d2h {res.d2h_ms:.0f}ms c-abi {res.wall_time:.3f}s",
                       file=sys.stderr, flush=True)
-        el = allmax(pg, max(r[0] for r in runs), local)
+        el = allmax(pg, statistics.median(r[0] for r in runs), local)  # median run; all in runs_s
         res = runs[-1][1]
         e2e = {"value": world * res.report.iters / el, "unit": "iters/s",
                "h2d_bytes_per_step": int(N_el * esize),
@@ -414,7 +414,7 @@ def main():
     ap.add_argument("--workload", default="C3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--e2e-runs", type=int, default=2)
+    ap.add_argument("--e2e-runs", type=int, default=5)
     ap.add_argument("--cpu-iters", type=int, default=1)
     ap.add_argument("--ref-max-steps", type=int, default=12)
     args = ap.parse_args()

@@ -742,6 +742,75 @@ __global__ void __launch_bounds__(64) k_pp_d2(const T* __restrict__ M, int64_t d
     }
 }
 
+// k-means++ distance update of R restarts seeded side by side: one pass over
+// the columns updates d2[r·n + j] = min(d2[r·n + j], sq_dist(col_j, col_last[r]))
+// for every restart (each chain exact, ascending i, as k_pp_d2).
+struct PPLast {
+    int v[8];
+};
+template <typename T, int R>
+__global__ void __launch_bounds__(64) k_pp_d2_multi(const T* __restrict__ M, int64_t d, int n, PPLast last,
+                                                    double* __restrict__ d2) {
+    constexpr int PD = 4, W = 2;
+    extern __shared__ __align__(16) unsigned char pp_sm[];
+    auto tile = reinterpret_cast<T(*)[PD][32][33]>(pp_sm);                           // [W][PD][32][33]
+    auto lastv = reinterpret_cast<T(*)[PD][R][32]>(pp_sm + sizeof(T) * W * PD * 32 * 33);  // [W][PD][R][32]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int j0 = (blockIdx.x * W + w) * 32;
+    if (j0 >= n) return;
+    const int64_t ntile = (d + 31) / 32;
+    auto issue = [&](int64_t t) {
+        const int slot = (int)(t % PD);
+        const int64_t i = t * 32 + lane;
+        const bool okr = i < d;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const T* src = okr ? M + (int64_t)last.v[r] * d + i : M;
+            if (sizeof(T) == 8) cp_async8(&lastv[w][slot][r][lane], src, okr);
+            else cp_async4(&lastv[w][slot][r][lane], src, okr);
+        }
+        for (int cc = 0; cc < 32; ++cc) {
+            const int j = j0 + cc;
+            const bool ok = okr && j < n;
+            const T* src = ok ? M + (int64_t)j * d + i : M;
+            if (sizeof(T) == 8) cp_async8(&tile[w][slot][cc][lane], src, ok);
+            else cp_async4(&tile[w][slot][cc][lane], src, ok);
+        }
+        cp_commit();
+    };
+    for (int64_t t = 0; t < PD - 1; ++t) {
+        if (t < ntile) issue(t);
+        else cp_commit();
+    }
+    double s[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[r] = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + PD - 1 < ntile) issue(t + PD - 1);
+        else cp_commit();
+        cp_wait<PD - 1>();
+        __syncwarp();
+        const int slot = (int)(t % PD);
+        const int lim = (int)((d - t * 32) < 32 ? (d - t * 32) : 32);
+        for (int q = 0; q < lim; ++q) {
+            const double x = (double)tile[w][slot][lane][q];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const double tt = x - (double)lastv[w][slot][r][q];
+                s[r] += tt * tt;
+            }
+        }
+        __syncwarp();
+    }
+    const int j = j0 + lane;
+    if (j < n)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double old = d2[(int64_t)r * n + j];
+            d2[(int64_t)r * n + j] = (s[r] < old) ? s[r] : old;
+        }
+}
+
 // Exact own-centroid distance sq_dist(col_j, C[:, label_j]) for every column
 // (inertia_of, kmeans.cpp:84-91; repair_empty, kmeans.cpp:51).
 template <typename T>

@@ -403,6 +403,7 @@ struct KMeansEngine {
         double* cur = C;
         double* nxt = nextC.p;
         const auto t_lloyd0 = HClock::now();
+        double lph[5] = {0, 0, 0, 0, 0};
         for (; it < max_iters; ++it) {
             const auto ts0 = HClock::now();
             assign(cur, labels);
@@ -415,15 +416,22 @@ struct KMeansEngine {
             const double tm = since(ts0);
             if (stats) stats->lloyd_steps++;
             const bool stop = stop_test(nxt, cur, tol);
-            if (trace_on() && since(ts0) > 0.015)
-                std::fprintf(stderr, "[respca] slow lloyd step %llu: assign %.4f fetch %.4f repair %.4f means %.4f stop %.4f\n",
-                             (unsigned long long)it, ta, tf, tr, tm, since(ts0));
+            if (trace_on()) {
+                lph[0] += ta;
+                lph[1] += tf - ta;
+                lph[2] += tr - tf;
+                lph[3] += tm - tr;
+                lph[4] += since(ts0) - tm;
+            }
             std::swap(cur, nxt);
             if (stop) {
                 ++it;
                 break;
             }
         }
+        if (trace_on())
+            std::fprintf(stderr, "[respca] lloyd %llu steps: assign %.4f fetch %.4f repair %.4f means %.4f stop %.4f\n",
+                         (unsigned long long)it, lph[0], lph[1], lph[2], lph[3], lph[4]);
         if (cur != C) CK(cudaMemcpyAsync(C, cur, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
         if (stats) {
             CK(cudaStreamSynchronize(st));
@@ -519,7 +527,8 @@ struct KMeansEngine {
     //      G = XᵀX once; every restart's refinement borrows it for the call.
     const double* gram = nullptr;  // borrowed G, diag, norm bounds (nullptr: per-pass path)
     const double *gram_xx = nullptr, *gram_xn = nullptr, *gram_xl = nullptr;
-    cudaEvent_t gram_ev = nullptr;  // G complete on the engine's stream
+    cudaEvent_t gram_ev = nullptr;  // G complete
+    cudaStream_t gram_st = nullptr;  // G's own stream (restart lanes)
     DBuf<double> gG, gxx, gxn, gxl, gS;
     DBuf<GramScal> gsc;
     DBuf<int> glog;
@@ -542,7 +551,8 @@ struct KMeansEngine {
     bool gram_path() const { return gram != nullptr && c >= 2 && c <= kGramMaxC && !hart_ws_on(); }
     double gram_gamma() const { return (2.2 * (double)d + 4.0) * kU; }
     // G = MᵀM on the FP64 tensor cores + its diagonal bounds; the event marks completion
-    void compute_gram() {
+    void compute_gram(cudaStream_t gs = nullptr) {
+        if (!gs) gs = st;
         gG.ensure((size_t)n * n);
         gxx.ensure(n);
         gxn.ensure(n);
@@ -555,11 +565,11 @@ struct KMeansEngine {
         if (trace_on()) {
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
-            CK(cudaEventRecord(e0, st));
+            CK(cudaEventRecord(e0, gs));
         }
-        k_gram<T><<<(unsigned)tiles, 256, sm, st>>>(M, d, n, gG.p);
+        k_gram<T><<<(unsigned)tiles, 256, sm, gs>>>(M, d, n, gG.p);
         if (trace_on()) {
-            CK(cudaEventRecord(e1, st));
+            CK(cudaEventRecord(e1, gs));
             CK(cudaEventSynchronize(e1));
             float ms = 0.f;
             CK(cudaEventElapsedTime(&ms, e0, e1));
@@ -568,10 +578,10 @@ struct KMeansEngine {
             cudaEventDestroy(e0);
             cudaEventDestroy(e1);
         }
-        k_gram_diag<<<ceil_div(n, 256), 256, 0, st>>>(gG.p, n, gram_gamma(), gxx.p, gxn.p, gxl.p);
+        k_gram_diag<<<ceil_div(n, 256), 256, 0, gs>>>(gG.p, n, gram_gamma(), gxx.p, gxn.p, gxl.p);
         ln.add(2);
         if (!gram_ev) CK(cudaEventCreateWithFlags(&gram_ev, cudaEventDisableTiming));
-        CK(cudaEventRecord(gram_ev, st));
+        CK(cudaEventRecord(gram_ev, gs));
         gram = gG.p;
         gram_xx = gxx.p;
         gram_xn = gxn.p;
@@ -945,6 +955,79 @@ struct KMeansEngine {
         return chosen;
     }
 
+    // k-means++ seedings (kmeans.cpp:172-224) of R ≤ 8 restarts side by side:
+    // one pass over the columns per pick serves every restart's d² update
+    // (k_pp_d2_multi); each restart draws from its own engine.  engs[r]: in =
+    // the restart's start state, out = its state after the seeding's draws.
+    template <int R>
+    void launch_pp_multi(const PPLast& lasts) {
+        const size_t sm = sizeof(T) * 2 * 4 * (32 * 33 + R * 32);
+        smem_at_least((const void*)k_pp_d2_multi<T, R>, sm);
+        k_pp_d2_multi<T, R><<<ceil_div(n, 64), 64, sm, st>>>(M, d, n, lasts, d2.p);
+        ln.add();
+    }
+    HBuf hpp;
+    std::vector<std::vector<int>> pp_joint(std::vector<std::mt19937_64>& engs) {
+        const int R = (int)engs.size();
+        if (R < 1 || R > 8) throw InvalidArg("pp_joint: 1..8 restarts");
+        if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
+        if ((int64_t)c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
+        std::vector<std::vector<int>> chosen(R);
+        std::vector<std::vector<char>> is_chosen(R, std::vector<char>(n, 0));
+        for (int r = 0; r < R; ++r) {
+            std::uniform_int_distribution<std::size_t> first(0, (std::size_t)n - 1);
+            const int f0 = (int)first(engs[r]);
+            chosen[r].push_back(f0);
+            is_chosen[r][f0] = 1;
+        }
+        d2.ensure((size_t)R * n);
+        double* hd2 = hpp.ensure<double>((size_t)R * n);
+        for (size_t e = 0; e < (size_t)R * n; ++e) hd2[e] = std::numeric_limits<double>::infinity();
+        CK(cudaMemcpyAsync(d2.p, hd2, sizeof(double) * R * n, cudaMemcpyHostToDevice, st));
+        for (int p = 1; p < c; ++p) {
+            PPLast lasts{};
+            for (int r = 0; r < 8; ++r) lasts.v[r] = chosen[r < R ? r : 0].back();
+            switch (R) {
+                case 1: launch_pp_multi<1>(lasts); break;
+                case 2: launch_pp_multi<2>(lasts); break;
+                case 3: launch_pp_multi<3>(lasts); break;
+                case 4: launch_pp_multi<4>(lasts); break;
+                case 5: launch_pp_multi<5>(lasts); break;
+                case 6: launch_pp_multi<6>(lasts); break;
+                case 7: launch_pp_multi<7>(lasts); break;
+                default: launch_pp_multi<8>(lasts); break;
+            }
+            CK(cudaMemcpyAsync(hd2, d2.p, sizeof(double) * R * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            for (int r = 0; r < R; ++r) {  // kmeans.cpp:192-221, restart by restart
+                const double* h = hd2 + (size_t)r * n;
+                double total = 0.0;
+                for (int j = 0; j < n; ++j) total += h[j];
+                int pick = n;
+                if (total > 0.0) {
+                    std::uniform_real_distribution<double> u(0.0, total);
+                    double rr = u(engs[r]);
+                    for (int j = 0; j < n; ++j) {
+                        rr -= h[j];
+                        if (rr <= 0.0 && !is_chosen[r][j]) {
+                            pick = j;
+                            break;
+                        }
+                    }
+                }
+                if (pick == n)
+                    for (int j = 0; j < n; ++j)
+                        if (!is_chosen[r][j]) {
+                            pick = j;
+                            break;
+                        }
+                chosen[r].push_back(pick);
+                is_chosen[r][pick] = 1;
+            }
+        }
+        return chosen;
+    }
+
     void gather(const std::vector<int>& idx, double* C) {
         gidx.ensure(c);
         CK(cudaMemcpyAsync(gidx.p, idx.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
@@ -1055,9 +1138,13 @@ struct KMeansEngine {
         cudaEvent_t ready;
         CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
         CK(cudaEventRecord(ready, st));  // M is complete on the caller's stream
-        // G = MᵀM on the caller's stream, overlapping the lanes' seeding and
-        // Lloyd steps; the refinements wait for it (gram_ev)
-        if (want_gram) compute_gram();
+        // G = MᵀM on its own stream, overlapping the seeding and the Lloyd
+        // steps; the refinements wait for it (gram_ev)
+        if (want_gram) {
+            if (!gram_st) CK(cudaStreamCreateWithFlags(&gram_st, cudaStreamNonBlocking));
+            CK(cudaStreamWaitEvent(gram_st, ready, 0));
+            compute_gram(gram_st);
+        }
         while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
             CK(cudaStreamCreateWithFlags(&lanes.back()->e.st, cudaStreamNonBlocking));
@@ -1105,6 +1192,16 @@ struct KMeansEngine {
             }
             truth[0] = std::mt19937_64(seed);
             truth_known[0] = 1;
+        }
+        // the first ≤ 8 restarts seed side by side from their speculated states
+        // (one pass over the columns per pick for all of them)
+        std::vector<std::vector<int>> joint_chosen;
+        std::vector<std::mt19937_64> joint_eng;
+        if (n_restarts > 1 && env_int("RESPCA_PP_JOINT", 1) != 0) {
+            const auto tj = HClock::now();
+            joint_eng.assign(spec.begin(), spec.begin() + (size_t)std::min<uint64_t>(n_restarts, 8));
+            joint_chosen = pp_joint(joint_eng);
+            if (stats) stats->t_pp += since(tj);
         }
         std::mutex mu;
         std::condition_variable cv;
@@ -1154,7 +1251,13 @@ struct KMeansEngine {
                     // against the true one (redone from it on a mismatch)
                     const auto tp = HClock::now();
                     std::mt19937_64 eng = spec[r];
-                    std::vector<int> chosen = e.pp_init(eng);
+                    std::vector<int> chosen;
+                    if (r < joint_chosen.size()) {
+                        eng = joint_eng[r];
+                        chosen = joint_chosen[r];
+                    } else {
+                        chosen = e.pp_init(eng);
+                    }
                     std::mt19937_64 start;
                     {
                         std::unique_lock<std::mutex> lk(mu);
