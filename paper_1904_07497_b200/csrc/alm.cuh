@@ -429,9 +429,11 @@ __global__ void __launch_bounds__(256) k_group_sum(
     const T* __restrict__ X, const T* __restrict__ S, const T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members, const Ctl* __restrict__ ctl,
     double* __restrict__ out0, double* __restrict__ out1, int use_parity, int scale_by_count,
-    int64_t d, int rowblocks) {
-    const int g = blockIdx.x / rowblocks;
-    const int rb = blockIdx.x - g * rowblocks;
+    int64_t d, int rowblocks, const int* __restrict__ gorder = nullptr) {
+    // gorder: groups largest first (the longest member walks start first)
+    const int gi = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - gi * rowblocks;
+    const int g = gorder ? __ldg(gorder + gi) : gi;
     const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
     if (i0 >= d) return;
     double* __restrict__ out = (use_parity && ctl->parity) ? out1 : out0;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(256) k_group_sum(
 #pragma unroll
     for (int r = 0; r < R; ++r) acc[r] = 0.0;
     int t = beg;
-    constexpr int U = 4;
+    constexpr int U = MODE == 1 ? 8 : 4;
     for (; t + U <= end; t += U) {
         Vec<T, R> xv[U], sv[U], tv[U];
 #pragma unroll
@@ -474,6 +476,46 @@ __global__ void __launch_bounds__(256) k_group_sum(
     const double inv = scale_by_count ? 1.0 / (double)(end - beg) : 1.0;
 #pragma unroll
     for (int r = 0; r < R; ++r) out[(int64_t)g * d + i0 + r] = scale_by_count ? acc[r] * inv : acc[r];
+}
+
+// means_of (kmeans.cpp:66-82): out[i,g] = (Σ_{j∈g, ascending} m[i,j]) · (1/n_g).
+// Each row's sum is a sequential chain over the group's members, so the only
+// parallelism is over rows (and groups): a thread owns one row and keeps U
+// member columns in flight (their indices staged in shared memory one batch
+// ahead), so even the largest group — whose chains bound the kernel — streams
+// at d·U·8 bytes in flight.  gorder: groups largest first.
+constexpr int MS_U = 32, MS_T = 64;
+template <typename T>
+__global__ void __launch_bounds__(MS_T, 8) k_means_sum(const T* __restrict__ M, const int* __restrict__ goff,
+                                                       const int* __restrict__ members,
+                                                       const int* __restrict__ gorder, double* __restrict__ out,
+                                                       int64_t d, int rowblocks, int scale = 1) {
+    __shared__ int sidx[2][MS_U];
+    const int gi = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - gi * rowblocks;
+    const int g = gorder ? __ldg(gorder + gi) : gi;
+    const int64_t i = (int64_t)rb * MS_T + threadIdx.x;
+    const bool row = i < d;
+    const int beg = __ldg(goff + g), end = __ldg(goff + g + 1);
+    double acc = 0.0;
+    if (threadIdx.x < MS_U) sidx[0][threadIdx.x] = beg + (int)threadIdx.x < end ? __ldg(members + beg + threadIdx.x) : 0;
+    __syncthreads();
+    int b = 0;
+    for (int t = beg; t < end; t += MS_U, b ^= 1) {
+        double x[MS_U];
+#pragma unroll
+        for (int u = 0; u < MS_U; ++u)
+            x[u] = (row && t + u < end) ? (double)__ldg(M + (int64_t)sidx[b][u] * d + i) : 0.0;
+        if (threadIdx.x < MS_U) {  // the next batch's indices
+            const int q = t + MS_U + (int)threadIdx.x;
+            sidx[b ^ 1][threadIdx.x] = q < end ? __ldg(members + q) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < MS_U; ++u)
+            if (t + u < end) acc += x[u];  // ascending member order (kmeans.cpp:73)
+        __syncthreads();
+    }
+    if (row) out[(int64_t)g * d + i] = scale ? acc * (1.0 / (double)(end - beg)) : acc;  // kmeans.cpp:78
 }
 
 // ---------------------------------------------------------------------------

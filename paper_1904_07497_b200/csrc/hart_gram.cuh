@@ -199,27 +199,46 @@ RESPCA_DEV double gam_n(double m) {  // γ_m = m·u/(1 − m·u), bounded with s
     return m * kU * 1.01;
 }
 
-// initial scalars from S⁰ and the start centroids C = means_of (kmeans.cpp:66-82)
-__global__ void k_gram_scal(const double* __restrict__ S, const double* __restrict__ xn,
-                            const int* __restrict__ goff, const int* __restrict__ members, int n, int c,
-                            double gamG, GramScal* __restrict__ out) {
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+// initial scalars from S⁰ and the start centroids C = means_of (kmeans.cpp:66-82);
+// one block per centroid (the bounds below hold for any summation order)
+__global__ void __launch_bounds__(256) k_gram_scal(const double* __restrict__ S, const double* __restrict__ xn,
+                                                   const int* __restrict__ goff, const int* __restrict__ members,
+                                                   int n, int c, double gamG, GramScal* __restrict__ out) {
+    __shared__ double ra[32], rq[32];
+    const int k = blockIdx.x;
     if (k >= c) return;
     const int p0 = goff[k], p1 = goff[k + 1];
     const double nk = (double)(p1 - p0);
     double A = 0.0, Q = 0.0;
-    for (int p = p0; p < p1; ++p) {
-        const int m = members[p];
-        A = __dadd_ru(A, xn[m]);
-        Q += S[(int64_t)k * n + m];
+    for (int p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+        const int m = __ldg(members + p);
+        A = __dadd_ru(A, __ldg(xn + m));
+        Q += __ldcg(S + (int64_t)k * n + m);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        A = __dadd_ru(A, __shfl_xor_sync(0xffffffffu, A, o));
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if (lane == 0) {
+        ra[warp] = A;
+        rq[warp] = Q;
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    A = 0.0;
+    Q = 0.0;
+    for (int w = 0; w < nw; ++w) {
+        A = __dadd_ru(A, ra[w]);
+        Q += rq[w];
     }
     const double gn = gam_n(nk);
     GramScal s;
     s.A = A;
     s.Q = Q;
-    // Ŝ⁰ = Σ_m Ĝ[m][j]: recursive-sum error γ_nk·Σ|Ĝ| plus the Ĝ errors
+    // Ŝ⁰ = Σ_m Ĝ[m][j] (any order): summation error γ_nk·Σ|Ĝ| plus the Ĝ errors
     s.ES = __dmul_ru(__dadd_ru(__dmul_ru(gn, 1.0 + gamG), gamG), __dmul_ru(A, 1.01));
-    // Q̂⁰ = Σ_m Ŝ⁰_k[m]: Σ_m xn_m·ES + γ_nk·Σ_m xn_m (A + ES)
+    // Q̂⁰ = Σ_m Ŝ⁰_k[m] (any order): Σ_m xn_m·ES + γ_nk·Σ_m xn_m (A + ES)
     s.EQ = __dmul_ru(__dadd_ru(__dmul_ru(A, s.ES), __dmul_ru(gn, __dmul_ru(A, __dadd_ru(A, s.ES)))), 1.01);
     // start centroid = fl(fl(Σ x_m) · fl(1/n_k)): ‖c − μ‖ ≤ γ_nk·A/n_k·(1+3u) + 2.01u·‖μ‖
     const double mn = __dsqrt_ru(fmax(__ddiv_ru(__dadd_ru(Q, s.EQ), nk * nk), 0.0));

@@ -351,15 +351,19 @@ struct KMeansEngine {
         upload_groups();
         launch_group_mean(Cout);
     }
+    DBuf<int> gord;
     void launch_group_mean(double* Cout) {
-        const bool r2 = (d % 2 == 0);
-        const int rb = ceil_div(d, 256 * (r2 ? 2 : 1));
-        if (r2)
-            k_group_sum<T, 2, 1><<<rb * c, 256, 0, st>>>(M, nullptr, nullptr, goff.p, members.p,
-                                                       nullptr, Cout, nullptr, 0, 1, d, rb);
-        else
-            k_group_sum<T, 1, 1><<<rb * c, 256, 0, st>>>(M, nullptr, nullptr, goff.p, members.p,
-                                                       nullptr, Cout, nullptr, 0, 1, d, rb);
+        // groups largest first: the largest group's member walks bound the kernel
+        std::vector<int> ord(c);
+        for (int k = 0; k < c; ++k) ord[k] = k;
+        if ((int)groups.counts.size() == c)
+            std::stable_sort(ord.begin(), ord.end(),
+                             [&](int x, int y) { return groups.counts[x] > groups.counts[y]; });
+        gord.ensure(c);
+        // pageable source: staged by the runtime before the call returns
+        CK(cudaMemcpyAsync(gord.p, ord.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
+        const int rb = ceil_div(d, MS_T);
+        k_means_sum<T><<<rb * c, MS_T, 0, st>>>(M, goff.p, members.p, gord.p, Cout, d, rb);
         ln.add();
     }
 
@@ -611,8 +615,17 @@ struct KMeansEngine {
         gram_reserve();
         if (gram_ev) CK(cudaStreamWaitEvent(st, gram_ev, 0));
         const double gamG = gram_gamma();
-        k_gram_s0<<<dim3(ceil_div(n, 256), c), 256, 0, st>>>(gram, goff.p, members.p, n, gS.p);
-        k_gram_scal<<<ceil_div(c, 128), 128, 0, st>>>(gS.p, gram_xn, goff.p, members.p, n, c, gamG, gsc.p);
+        {  // S⁰_k[j] = Σ_{m∈k} Ĝ[m][j]: the member-walk kernel of means_of over G's columns
+            std::vector<int> ord(c);
+            for (int k = 0; k < c; ++k) ord[k] = k;
+            std::stable_sort(ord.begin(), ord.end(),
+                             [&](int x, int y) { return groups.counts[x] > groups.counts[y]; });
+            gord.ensure(c);
+            CK(cudaMemcpyAsync(gord.p, ord.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
+            const int rb = ceil_div(n, MS_T);
+            k_means_sum<double><<<rb * c, MS_T, 0, st>>>(gram, goff.p, members.p, gord.p, gS.p, n, rb, 0);
+        }
+        k_gram_scal<<<c, 256, 0, st>>>(gS.p, gram_xn, goff.p, members.p, n, c, gamG, gsc.p);
         GramArgs a{};
         a.G = gram;
         a.xx = gram_xx;
