@@ -432,15 +432,6 @@ RESPCA_DEV uint32_t gcl_size() {
 }
 constexpr int GRAM_MAXCL = 16;
 
-// A move's new per-centroid state for both sides (what every CTA's replica
-// takes over once the move is elected), as 8-byte words for DSMEM copies.
-struct GramSpec {
-    GramScal s[2];
-    GramCoef cf[2];
-    double cnt[2];  // new counts (exact small integers)
-};
-constexpr int GRAM_SPEC_WORDS = sizeof(GramSpec) / 8;
-
 RESPCA_DEV void gcl_st_i32(uint32_t a, int v) {
     asm volatile("st.shared::cluster.b32 [%0], %1;\n" ::"r"(a), "r"(v) : "memory");
 }
@@ -452,17 +443,16 @@ RESPCA_DEV void gcl_st_f64(uint32_t a, double v) {
 // One thread-block cluster per restart.  Every CTA keeps a replica of the
 // per-centroid state.  A window of GRAM_WARPS·CL columns is decided by all
 // warps of the cluster (CTA r, warp w → column cursor + GRAM_WARPS·r + w); each
-// warp pushes its verdict into every CTA's shared memory, so after the one
-// cluster barrier per window every warp finds the first column that is not
-// provably "no move" from local shared memory.  A warp that finds a provable
-// move also computes the move's new per-centroid state (both sides)
-// speculatively; if its column is elected, every CTA copies it (DSMEM) into
-// its replica.  The move's O(n) update is applied during the next window, off
-// the critical path:
-//   * each deciding warp applies it to its own column's Ŝ_from, Ŝ_to in
-//     registers (one Ĝ element) before deciding, and writes them back;
+// CTA pushes its first candidate (verdict + the move's inputs: Ŝ_from[j],
+// Ŝ_to[j], Ĝ_jj and the norm bounds) into every CTA's shared memory, so after
+// the one cluster barrier per window every warp finds the elected move in local
+// shared memory, and two threads of every CTA update the replica (identical
+// inputs → identical replicas).  The move's O(n) update is applied during the
+// next window, off the critical path:
+//   * each window's Ŝ block is staged with the pending move applied (and the
+//     two changed entries written back);
 //   * each CTA applies it to its slice of the other columns while its warps
-//     decide (loads first, stores after).
+//     decide (loads first, stores before the decide).
 template <typename T, int KPL>
 __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
@@ -476,11 +466,12 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     __shared__ int s_wfrom[GRAM_WARPS];
     __shared__ double s_wg[GRAM_WARPS][2];            // Ĝ_jj, ‖x_j‖ bound of the window's columns
     __shared__ int s_loc[2][GRAM_WARPS];              // this CTA's verdicts: status | to << 2 | from << 17
-    __shared__ __align__(16) GramSpec s_spec[2][GRAM_WARPS];  // this CTA's speculative move states
+    constexpr int MVW = 5;  // a move's inputs: Ŝ_from[j], Ŝ_to[j], Ĝ_jj, ‖x_j‖ upper / lower bound
+    __shared__ double s_sv[2][GRAM_WARPS][MVW];       // this CTA's candidates' move inputs
     __shared__ int s_first[2][GRAM_MAXCL][2];         // every CTA's first candidate: verdict, warp
-    __shared__ __align__(16) GramSpec s_fspec[2][GRAM_MAXCL];  // ... and its move state
+    __shared__ double s_fsv[2][GRAM_MAXCL][MVW];      // ... and its move inputs
     __shared__ int s_xres;                            // exact fallback verdict (CTA 0)
-    __shared__ __align__(16) GramSpec s_xspec;
+    __shared__ double s_xsv[MVW];                     // ... and the move's inputs
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int rank = (int)gcl_rank(), CL = (int)gcl_size();
     const int W = GRAM_WARPS * CL;
@@ -510,19 +501,6 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             const unsigned long long t = clock64();
             tph[slot] += t - tmk;
             tmk = t;
-        }
-    };
-    // the speculative state of a move found by this warp at column j (lanes 0, 1)
-    auto speculate = [&](GramSpec* out, int j, int f, int t, double sf, double stv, double gmm, double xnm) {
-        if (lane < 2) {
-            const double xlm = __ldg(a.xl + j);
-            GramScal S = sc[lane ? t : f];
-            GramCoef C = cf[lane ? t : f];
-            int ck = cnt[lane ? t : f];
-            gram_side(lane, S, C, ck, lane ? stv : sf, gmm, xnm, xlm, gamG);
-            out->s[lane] = S;
-            out->cf[lane] = C;
-            out->cnt[lane] = (double)ck;
         }
     };
     int nlog = 0, replayed = 0, pass = 0, par = 0;
@@ -648,7 +626,13 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                             if (q == (from >> 5)) vf = __shfl_sync(0xffffffffu, sv[q], from & 31);
                             if (q == (to >> 5)) vt = __shfl_sync(0xffffffffu, sv[q], to & 31);
                         }
-                        speculate(&s_spec[par][warp], j, from, to, vf, vt, gjj, xnj);
+                        if (lane == 0) {
+                            s_sv[par][warp][0] = vf;
+                            s_sv[par][warp][1] = vt;
+                            s_sv[par][warp][2] = gjj;
+                            s_sv[par][warp][3] = xnj;
+                            s_sv[par][warp][4] = __ldg(a.xl + j);
+                        }
                     }
                 }
             }
@@ -674,10 +658,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         gcl_st_i32(gcl_map(&s_first[par][rank][0], (uint32_t)lane), bal ? fv : 0);
                         gcl_st_i32(gcl_map(&s_first[par][rank][1], (uint32_t)lane), fw);
                     }
-                    if ((fv & 3) == 1 && lane < GRAM_SPEC_WORDS) {
-                        const double word = reinterpret_cast<const double*>(&s_spec[par][fw])[lane];
-                        for (int r = 0; r < CL; ++r)
-                            gcl_st_f64(gcl_map(reinterpret_cast<double*>(&s_fspec[par][rank]) + lane, (uint32_t)r), word);
+                    if ((fv & 3) == 1 && lane < MVW) {
+                        const double word = s_sv[par][fw][lane];
+                        for (int r = 0; r < CL; ++r) gcl_st_f64(gcl_map(&s_fsv[par][rank][lane], (uint32_t)r), word);
                     }
                 }
             }
@@ -706,10 +689,10 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             cursor = jj + 1;
             const int mfrom = w >> 17;
             int mst = w & 3, mto = (w >> 2) & 0x7fff;
-            uint32_t spec_src = 0;  // the elected move's state: local copy, or CTA 0's after a fallback
-            const double* spec_loc = nullptr;
+            double mvin[MVW];  // the elected move's inputs (pushed by its CTA, or CTA 0's after a fallback)
             if (mst == 1) {
-                spec_loc = reinterpret_cast<const double*>(&s_fspec[par][pr]);
+#pragma unroll
+                for (int q = 0; q < MVW; ++q) mvin[q] = s_fsv[par][pr][q];
             } else {
                 // ---- near-tie (CTA 0): the reference's own chain on the
                 //      reference's centroids (logged moves replayed, kmeans.cpp:128-129)
@@ -749,10 +732,12 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         int t2 = -1;
                         const int s2 = gram_decide<KPL>(mfrom, c, cf, cnt, lo, hi, mid, t2);
                         if (lane == 0) s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;  // exact: 2 only for NaN
-                        if (s2 == 1) {
-                            const double sf = __ldcg(a.S + (int64_t)mfrom * n + jj);
-                            const double stv = __ldcg(a.S + (int64_t)t2 * n + jj);
-                            speculate(&s_xspec, jj, mfrom, t2, sf, stv, __ldg(a.xx + jj), __ldg(a.xn + jj));
+                        if (s2 == 1 && lane == 0) {
+                            s_xsv[0] = __ldcg(a.S + (int64_t)mfrom * n + jj);
+                            s_xsv[1] = __ldcg(a.S + (int64_t)t2 * n + jj);
+                            s_xsv[2] = __ldg(a.xx + jj);
+                            s_xsv[3] = __ldg(a.xn + jj);
+                            s_xsv[4] = __ldg(a.xl + jj);
                         }
                     }
                 }
@@ -762,38 +747,31 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 const int xr = gcl_ld_i32(gcl_map(&s_xres, 0));
                 mst = xr & 3;
                 mto = xr >> 2;
-                spec_src = gcl_map(&s_xspec, 0);
+                if (mst == 1)
+#pragma unroll
+                    for (int q = 0; q < MVW; ++q) mvin[q] = gcl_ld_f64(gcl_map(&s_xsv[q], 0));
                 lap(1);
             }
             if (mst == 1) {
-                // pending for the next window: the log (CTA 0) and the replicas
-                // take the elected state now (warp 0), the Ŝ update later
-                if (warp == 0) {
+                // pending for the next window: the log (CTA 0); the replicas take the
+                // move's per-centroid state now (two threads per CTA, identical
+                // inputs → identical replicas), the Ŝ update later
+                {
                     const int f = mfrom, t = mto;
-                    if (lane == 0 && rank == 0) {  // the log holds the counts before the move
-                        int* lg = a.log + 5 * (int64_t)nlog;
-                        lg[0] = jj;
-                        lg[1] = f;
-                        lg[2] = t;
-                        lg[3] = cnt[f];
-                        lg[4] = cnt[t];
-                        __stcg(a.labels + jj, t);
+                    int* lg = a.log + 5 * (int64_t)nlog;
+                    if (tid == 0) {  // the log holds the counts before the move
+                        if (rank == 0) {
+                            lg[0] = jj;
+                            lg[1] = f;
+                            lg[2] = t;
+                            lg[3] = cnt[f];
+                            __stcg(a.labels + jj, t);
+                        }
+                        gram_side(0, sc[f], cf[f], cnt[f], mvin[0], mvin[2], mvin[3], mvin[4], gamG);
                     }
-                    double wv = 0.0;
-                    if (lane < GRAM_SPEC_WORDS) wv = spec_loc ? spec_loc[lane] : gcl_ld_w(spec_src + 8u * (uint32_t)lane);
-                    __syncwarp();
-                    if (lane < GRAM_SPEC_WORDS) {
-                        GramSpec* loc = &s_xspec;  // staging: reuse is safe (see below)
-                        (void)loc;
-                        // scatter the words into the replica
-                        const int side = lane < 5 ? 0 : lane < 10 ? 1 : lane < 17 ? 0 : lane < 24 ? 1 : lane - 24;
-                        const int k = side ? t : f;
-                        double* dst;
-                        if (lane < 10) dst = reinterpret_cast<double*>(&sc[k]) + (lane < 5 ? lane : lane - 5);
-                        else if (lane < 24) dst = reinterpret_cast<double*>(&cf[k]) + (lane < 17 ? lane - 10 : lane - 17);
-                        else dst = nullptr;
-                        if (dst) *dst = wv;
-                        else cnt[k] = (int)wv;
+                    if (tid == 32) {
+                        if (rank == 0) lg[4] = cnt[t];
+                        gram_side(1, sc[t], cf[t], cnt[t], mvin[1], mvin[2], mvin[3], mvin[4], gamG);
                     }
                 }
                 lap(7);
