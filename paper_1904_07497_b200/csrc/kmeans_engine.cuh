@@ -201,7 +201,7 @@ struct KMeansEngine {
         tcCb.ensure((size_t)TC_N * d_pad);
         tcerr.ensure(1);
         CK(cudaMemsetAsync(tcerr.p, 0, sizeof(int), st));
-        k_tc_prep_centroids<<<TC_N, 256, 0, st>>>(C, d, c, d_pad, tcCb.p, cc.p);
+        k_tc_prep_centroids<<<TC_N, 1024, 0, st>>>(C, d, c, d_pad, tcCb.p, cc.p);
         const int tiles = ceil_div(n, TC_M);
         const int64_t total_kb = d_pad / TC_KB;
         // two CTAs fit per SM (smem ~100 KB): one wave of <= 2·148 CTAs
@@ -252,7 +252,7 @@ struct KMeansEngine {
         tcCb.ensure((size_t)TC_N * dpad);
         tcerr.ensure(1);
         CK(cudaMemsetAsync(tcerr.p, 0, sizeof(int), st));
-        k_tc_prep_centroids<<<TC_N, 256, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p);
+        k_tc_prep_centroids<<<TC_N, 1024, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p);
         if (tma_key_a != (const void*)Lbp || tma_key_n != n || tma_key_dpad != dpad) {
             mapA = make_map(Lbp, (uint64_t)dpad, (uint64_t)n, TC_M);
             mapB = make_map(tcCb.p, (uint64_t)dpad, (uint64_t)TC_N, TC_N);
@@ -264,6 +264,7 @@ struct KMeansEngine {
         const int64_t total_kb = dpad / TC_KB;
         int ns = (int)std::max<int64_t>(1, std::min<int64_t>(total_kb / 4, (2 * 148) / tiles));
         ns = std::max(1, std::min(ns, 16));
+        if (const char* e = std::getenv("RESPCA_TMA_NS")) ns = std::max(1, std::min(16, std::atoi(e)));
         const int kbps = (int)((total_kb + ns - 1) / ns);
         part.ensure((size_t)ns * n * c);
         xxp.ensure((size_t)ns * n);

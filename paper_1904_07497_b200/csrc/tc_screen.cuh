@@ -100,16 +100,28 @@ RESPCA_DEV uint32_t sw128(int row, int chunk) {
 }
 
 // centroids → BF16 K-major [TC_N][d_pad] (rows ≥ c zero) and ‖c_k‖² (FP64 FMA)
-__global__ void k_tc_prep_centroids(const double* __restrict__ C, int64_t d, int c,
-                                    int64_t d_pad, __nv_bfloat16* __restrict__ Cb,
-                                    double* __restrict__ cc) {
+__global__ void __launch_bounds__(1024) k_tc_prep_centroids(const double* __restrict__ C, int64_t d, int c,
+                                                             int64_t d_pad, __nv_bfloat16* __restrict__ Cb,
+                                                             double* __restrict__ cc) {
     __shared__ double red[32];
     const int k = blockIdx.x;  // 0..TC_N-1
     double s = 0.0;
-    for (int64_t i = threadIdx.x; i < d_pad; i += blockDim.x) {
-        const double v = (k < c && i < d) ? C[(int64_t)k * d + i] : 0.0;
-        Cb[(int64_t)k * d_pad + i] = __double2bfloat16(v);
-        s = __fma_rn(v, v, s);
+    // 1024 threads, 4 loads in flight each: one latency round per 4096 rows
+    for (int64_t i0 = threadIdx.x; i0 < d_pad; i0 += 4 * (int64_t)blockDim.x) {
+        double v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            v[u] = (k < c && i < d) ? __ldg(C + (int64_t)k * d + i) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            if (i < d_pad) {
+                Cb[(int64_t)k * d_pad + i] = __double2bfloat16(v[u]);
+                s = __fma_rn(v[u], v[u], s);
+            }
+        }
     }
     double v[1] = {s};
     block_sum<1>(v, red);
