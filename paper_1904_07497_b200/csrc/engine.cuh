@@ -62,10 +62,7 @@ struct DBuf {
     U* ensure(size_t count) {
         if (count == 0) count = 1;
         if (count > cap) {
-            if (p && owned) {
-                if (std::getenv("RESPCA_TRACE")) std::fprintf(stderr, "[respca] DBuf regrow %zu -> %zu x %zu B\n", cap, count, sizeof(U));
-                cudaFree(p);
-            }
+            if (p && owned) cudaFree(p);
             p = nullptr;
             cap = 0;
             owned = true;
@@ -141,7 +138,6 @@ struct HBuf {
         size_t bytes = count * sizeof(U);
         if (bytes == 0) bytes = 8;
         if (bytes > cap) {
-            if (p && std::getenv("RESPCA_TRACE")) std::fprintf(stderr, "[respca] HBuf regrow %zu -> %zu B\n", cap, bytes);
             if (p) cudaFreeHost(p);
             p = nullptr;
             CK(cudaMallocHost(&p, bytes));

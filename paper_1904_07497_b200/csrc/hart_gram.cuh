@@ -168,28 +168,6 @@ __global__ void k_gram_diag(const double* __restrict__ G, int n, double gamG, do
     xl[j] = __dsqrt_rd(fmax(__dmul_rd(v, __dsub_rd(1.0, 2.0 * gamG)), 0.0));
 }
 
-// S_k[j] = Σ_{m∈k} Ĝ[m][j] (members in ascending order), thread per (j, k)
-__global__ void k_gram_s0(const double* __restrict__ G, const int* __restrict__ goff,
-                          const int* __restrict__ members, int n, double* __restrict__ S) {
-    const int j = blockIdx.x * blockDim.x + threadIdx.x, k = blockIdx.y;
-    if (j >= n) return;
-    const int p0 = __ldg(goff + k), p1 = __ldg(goff + k + 1);
-    double s = 0.0;
-    int p = p0;
-    for (; p + 4 <= p1; p += 4) {
-        const double g0 = __ldcg(G + (int64_t)__ldg(members + p) * n + j);
-        const double g1 = __ldcg(G + (int64_t)__ldg(members + p + 1) * n + j);
-        const double g2 = __ldcg(G + (int64_t)__ldg(members + p + 2) * n + j);
-        const double g3 = __ldcg(G + (int64_t)__ldg(members + p + 3) * n + j);
-        s += g0;
-        s += g1;
-        s += g2;
-        s += g3;
-    }
-    for (; p < p1; ++p) s += __ldcg(G + (int64_t)__ldg(members + p) * n + j);
-    S[(int64_t)k * n + j] = s;
-}
-
 // per-centroid state of the Gram refinement
 struct GramScal {
     double Q, A, ES, EQ, Dl;  // Q̂_k, Σ‖x_m‖ (upper), S error / ‖x_j‖, Q error, ‖c_k − μ_k‖

@@ -1155,13 +1155,24 @@ struct KMeansEngine {
         // G = MᵀM on its own stream, overlapping the seeding and the Lloyd
         // steps; the refinements wait for it (gram_ev)
         if (want_gram) {
-            if (!gram_st) CK(cudaStreamCreateWithFlags(&gram_st, cudaStreamNonBlocking));
+            if (!gram_st) {
+                // lowest priority: G fills the SMs the lanes' seeding and Lloyd
+                // steps (the critical path) leave idle
+                int lo = 0, hi = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CK(cudaStreamCreateWithPriority(&gram_st, cudaStreamNonBlocking,
+                                                env_int("RESPCA_GRAM_LOWPRIO", 1) ? lo : hi));
+            }
             CK(cudaStreamWaitEvent(gram_st, ready, 0));
             compute_gram(gram_st);
         }
         while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
-            CK(cudaStreamCreateWithFlags(&lanes.back()->e.st, cudaStreamNonBlocking));
+            {
+                int lo = 0, hi = 0;
+                CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+                CK(cudaStreamCreateWithPriority(&lanes.back()->e.st, cudaStreamNonBlocking, hi));
+            }
         }
         for (int l = 0; l < L; ++l) {
             Lane& ln_ = *lanes[l];
