@@ -217,7 +217,11 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
                                                      const int* __restrict__ ver, int64_t d,
                                                      int n, int c, int chunks_per_split,
                                                      double* __restrict__ part,
-                                                     double* __restrict__ xxp) {
+                                                     double* __restrict__ xxp,
+                                                     const int* __restrict__ kmap = nullptr,
+                                                     int csub = 0) {
+    // kmap: screen only the centroids kmap[0..csub) (the rest of `part` is
+    // kept); k below runs over that subset, kmap[k] is the centroid
     constexpr int NW = 8, WJ = NW / WK;
     constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8, KI = 32;
     constexpr int AS = 36;  // row stride (elements) of both smem tiles
@@ -234,6 +238,8 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
     int64_t iend = ibeg + (int64_t)chunks_per_split * KI;
     if (iend > d) iend = d;
     const int nch = ibeg < iend ? (int)((iend - ibeg + KI - 1) / KI) : 0;
+    const int nk = kmap ? csub : c;  // centroids screened by this launch
+    auto cid = [&](int k) { return kmap ? __ldg(kmap + k) : k; };
     // 16-byte copies need 16-byte aligned global rows: true when d is a
     // multiple of 16/sizeof(T); otherwise fall back to element copies.
     const bool vec_ok = (d % EPV) == 0;
@@ -256,8 +262,9 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
                 const int k = k0 + row;
                 const int64_t i = i0 + v * 2;
                 int bytes = 0;
-                if (k < c && i < iend) bytes = (int)(8 * ((iend - i) < 2 ? (iend - i) : 2));
-                const double* ck = C + ((int64_t)(ver && k < c ? ver[k] : 0) * c + k) * d;
+                if (k < nk && i < iend) bytes = (int)(8 * ((iend - i) < 2 ? (iend - i) : 2));
+                const int kc = k < nk ? cid(k) : 0;
+                const double* ck = C + ((int64_t)(ver && k < nk ? ver[kc] : 0) * c + kc) * d;
                 cp_async16(bdst + row * AS + v * 2, bytes ? ck + i : C, bytes);
             }
         } else {
@@ -273,8 +280,9 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
                 const int row = e / KI, ii = e - row * KI;
                 const int k = k0 + row;
                 const int64_t i = i0 + ii;
-                const bool p = k < c && i < iend;
-                const double* ck = C + ((int64_t)(ver && k < c ? ver[k] : 0) * c + k) * d;
+                const bool p = k < nk && i < iend;
+                const int kc = k < nk ? cid(k) : 0;
+                const double* ck = C + ((int64_t)(ver && k < nk ? ver[kc] : 0) * c + kc) * d;
                 cp_async8(bdst + row * AS + ii, p ? ck + i : C, p);
             }
         }
@@ -338,8 +346,8 @@ __global__ void __launch_bounds__(256, 2) k_dist_dmma(const T* __restrict__ M,
 #pragma unroll
         for (int y = 0; y < NK; ++y) {
             const int k = k0 + (wk * NK + y) * 8 + 2 * t4;
-            if (k < c) dst[k] = acc[x][y][0];
-            if (k + 1 < c) dst[k + 1] = acc[x][y][1];
+            if (k < nk) dst[cid(k)] = acc[x][y][0];
+            if (k + 1 < nk) dst[cid(k + 1)] = acc[x][y][1];
         }
     }
     if (wk == 0) {
@@ -740,6 +748,14 @@ __global__ void __launch_bounds__(64) k_pp_d2(const T* __restrict__ M, int64_t d
         const double old = d2[j];
         d2[j] = (s < old) ? s : old;
     }
+}
+
+// dst[:, list[y]] = src[:, list[y]] for the listed columns (d-long)
+__global__ void k_copy_cols(const double* __restrict__ src, double* __restrict__ dst, int64_t d,
+                            const int* __restrict__ list) {
+    const int64_t k = __ldg(list + blockIdx.y);
+    for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x); i < d; i += (int64_t)gridDim.x * blockDim.x)
+        dst[k * d + i] = src[k * d + i];
 }
 
 // k-means++ distance update of R restarts seeded side by side: one pass over

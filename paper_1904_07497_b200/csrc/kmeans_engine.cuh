@@ -149,14 +149,50 @@ struct KMeansEngine {
     int tile_k() const { return tk_tile(); }
 
     template <int WK, int MJ, int NK>
-    void launch_dmma(const T* Mp, int nn, const double* C, const int* ver, dim3 grid, int cps) {
+    void launch_dmma(const T* Mp, int nn, const double* C, const int* ver, dim3 grid, int cps,
+                     const int* kmap = nullptr, int csub = 0) {
         constexpr int NW = 8, WJ = NW / WK;
         constexpr int TJ = WJ * MJ * 8, TK = WK * NK * 8;
         static_assert(TJ == 128, "tile");
         const size_t sm = sizeof(T) * 2 * TJ * 36 + sizeof(double) * 2 * TK * 36;
         auto kf = k_dist_dmma<T, WK, MJ, NK>;
         smem_at_least((const void*)kf, (size_t)(sm));
-        kf<<<grid, 256, sm, st>>>(Mp, C, ver, d, nn, c, cps, part.p, xxp.p);
+        kf<<<grid, 256, sm, st>>>(Mp, C, ver, d, nn, c, cps, part.p, xxp.p, kmap, csub);
+    }
+    static int tk_for(int cc_) { return cc_ > 32 ? 64 : (cc_ > 16 ? 32 : (cc_ > 8 ? 16 : 8)); }
+    // the Lloyd screen of only the centroids in `sub` (their values changed since
+    // the last screen of these columns; the other partials in `part` stay valid:
+    // unchanged member sets give bit-identical means and deterministic partials)
+    DBuf<int> kmap;
+    void screen_subset(const double* C, const std::vector<int>& sub) {
+        if ((int)sub.size() == c || scr_n != n || tc_mode) {
+            screen(C);
+            return;
+        }
+        if (sub.empty()) return;
+        const int cs = (int)sub.size();
+        kmap.ensure(c);
+        CK(cudaMemcpyAsync(kmap.p, sub.data(), sizeof(int) * cs, cudaMemcpyHostToDevice, st));
+        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p, nullptr, c);
+        // the split count of the full screen (the partial layout must not change)
+        const int tiles = ceil_div(n, tile_j()) * ceil_div(c, tile_k());
+        const int chunks = ceil_div(d, 32);
+        int ns = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
+        ns = std::min(ns, 64);
+        if (ns != scr_split) {
+            screen(C);
+            return;
+        }
+        const int cps = ceil_div(chunks, ns);
+        const int tk = tk_for(cs);
+        dim3 grid(ceil_div(n, tile_j()), ceil_div(cs, tk), ns);
+        switch (tk) {
+            case 64: launch_dmma<2, 4, 4>(M, n, C, nullptr, grid, cps, kmap.p, cs); break;
+            case 32: launch_dmma<1, 2, 4>(M, n, C, nullptr, grid, cps, kmap.p, cs); break;
+            case 16: launch_dmma<1, 2, 2>(M, n, C, nullptr, grid, cps, kmap.p, cs); break;
+            default: launch_dmma<1, 2, 1>(M, n, C, nullptr, grid, cps, kmap.p, cs); break;
+        }
+        ln.add(2);
     }
 
     // ---- screened distances --------------------------------------------
@@ -304,9 +340,10 @@ struct KMeansEngine {
     }
 
     // assign_nearest (kmeans.cpp:21-37) → labels (device)
-    void assign(const double* C, int* labels) {
+    void assign(const double* C, int* labels, const std::vector<int>* changed = nullptr) {
         CK(cudaMemsetAsync(kctl.p, 0, sizeof(Ctl), st));
-        screen(C);
+        if (changed) screen_subset(C, *changed);
+        else screen(C);
         decide(C, nullptr, nullptr, 0, labels, kctl.p);
         Ctl h;
         CK(cudaMemcpyAsync(&h, kctl.p, sizeof(Ctl), cudaMemcpyDeviceToHost, st));
@@ -352,19 +389,41 @@ struct KMeansEngine {
         upload_groups();
         launch_group_mean(Cout);
     }
+    // means_of of only the groups in `changed` (their member sets changed); the
+    // other columns of Cout are copied from Cprev (same member set → same bits)
+    DBuf<int> kcopy;
+    void means_subset(double* Cout, const double* Cprev, const std::vector<int>& changed) {
+        groups.build(h_labels.data(), n, c);
+        upload_groups();
+        std::vector<char> is(c, 0);
+        for (int k : changed) is[k] = 1;
+        std::vector<int> keep;
+        for (int k = 0; k < c; ++k)
+            if (!is[k]) keep.push_back(k);
+        if (!keep.empty()) {
+            kcopy.ensure(c);
+            CK(cudaMemcpyAsync(kcopy.p, keep.data(), sizeof(int) * keep.size(), cudaMemcpyHostToDevice, st));
+            k_copy_cols<<<dim3(ceil_div(d, 256 * 4), (unsigned)keep.size()), 256, 0, st>>>(Cprev, Cout, d,
+                                                                                        kcopy.p);
+            ln.add();
+        }
+        if (!changed.empty()) launch_group_mean(Cout, &changed);
+    }
     DBuf<int> gord;
-    void launch_group_mean(double* Cout) {
+    void launch_group_mean(double* Cout, const std::vector<int>* only = nullptr) {
         // groups largest first: the largest group's member walks bound the kernel
-        std::vector<int> ord(c);
-        for (int k = 0; k < c; ++k) ord[k] = k;
+        std::vector<int> ord;
+        if (only) ord = *only;
+        else
+            for (int k = 0; k < c; ++k) ord.push_back(k);
         if ((int)groups.counts.size() == c)
             std::stable_sort(ord.begin(), ord.end(),
                              [&](int x, int y) { return groups.counts[x] > groups.counts[y]; });
         gord.ensure(c);
         // pageable source: staged by the runtime before the call returns
-        CK(cudaMemcpyAsync(gord.p, ord.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
+        CK(cudaMemcpyAsync(gord.p, ord.data(), sizeof(int) * ord.size(), cudaMemcpyHostToDevice, st));
         const int rb = ceil_div(d, MS_T);
-        k_means_sum<T><<<rb * c, MS_T, 0, st>>>(M, goff.p, members.p, gord.p, Cout, d, rb);
+        k_means_sum<T><<<rb * (int)ord.size(), MS_T, 0, st>>>(M, goff.p, members.p, gord.p, Cout, d, rb);
         ln.add();
     }
 
@@ -409,15 +468,34 @@ struct KMeansEngine {
         double* nxt = nextC.p;
         const auto t_lloyd0 = HClock::now();
         double lph[5] = {0, 0, 0, 0, 0};
+        // incremental steps: a centroid whose group kept its member set keeps
+        // its bits (means_of sums the same columns in the same order), so the
+        // next means and the next screen only touch the groups that changed
+        std::vector<int> prevL, chg;
+        bool have_chg = false;  // chg = groups changed between the last two assignments
+        const bool incr = env_int("RESPCA_LLOYD_INCR", 1) != 0;
         for (; it < max_iters; ++it) {
             const auto ts0 = HClock::now();
-            assign(cur, labels);
+            assign(cur, labels, (incr && have_chg && it >= 2) ? &chg : nullptr);
             const double ta = since(ts0);
             fetch_labels(labels);
             const double tf = since(ts0);
             repair_if_needed(cur, labels);
             const double tr = since(ts0);
-            means(nxt);
+            if (incr && it >= 1 && (int)prevL.size() == n) {
+                std::vector<char> f(c, 0);
+                for (int j = 0; j < n; ++j)
+                    if (prevL[j] != h_labels[j]) f[prevL[j]] = f[h_labels[j]] = 1;
+                chg.clear();
+                for (int k = 0; k < c; ++k)
+                    if (f[k]) chg.push_back(k);
+                have_chg = true;
+                means_subset(nxt, cur, chg);
+            } else {
+                have_chg = false;
+                means(nxt);
+            }
+            prevL = h_labels;
             const double tm = since(ts0);
             if (stats) stats->lloyd_steps++;
             const bool stop = stop_test(nxt, cur, tol);
