@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     int nlog = 0, replayed = 0, pass = 0, par = 0;
     // the pending move (uniform over the cluster)
     int pj = -1, pf = 0, pt = 0;
+    double pmv[5] = {0, 0, 0, 0, 0};  // its inputs (MVW words)
     for (;;) {
         int improved = 0;
         int cursor = 0;
@@ -507,11 +508,12 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             }
             {
                 const int jb = cursor + GRAM_WARPS * rank;
-                constexpr int SPT = (KPL * 32 * GRAM_WARPS + GRAM_THREADS - 1) / GRAM_THREADS;
+                constexpr int SW = GRAM_THREADS - 32;  // staging threads (the last warp updates the replica)
+                constexpr int SPT = (KPL * 32 * GRAM_WARPS + SW - 1) / SW;
                 double v[SPT], g[SPT];
 #pragma unroll
                 for (int u = 0; u < SPT; ++u) {  // all loads first
-                    const int e = tid + u * GRAM_THREADS;
+                    const int e = tid < SW ? tid + u * SW : 1 << 30;
                     const int k = e / GRAM_WARPS, jc = jb + (e - k * GRAM_WARPS);
                     v[u] = 0.0;
                     g[u] = 0.0;
@@ -520,9 +522,16 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                         if (mv && (k == pf || k == pt)) g[u] = __ldcg(a.G + (int64_t)pj * n + jc);
                     }
                 }
+                // the replicas take the pending move's per-centroid state while the
+                // staging loads are in flight (two threads; identical inputs in
+                // every CTA → identical replicas; read only after the barrier below)
+                if (mv && warp == GRAM_WARPS - 1 && lane < 2) {  // the last warp stages nothing
+                    const int k = lane ? pt : pf;
+                    gram_side(lane, sc[k], cf[k], cnt[k], lane ? pmv[1] : pmv[0], pmv[2], pmv[3], pmv[4], gamG);
+                }
 #pragma unroll
                 for (int u = 0; u < SPT; ++u) {
-                    const int e = tid + u * GRAM_THREADS;
+                    const int e = tid < SW ? tid + u * SW : 1 << 30;
                     const int k = e / GRAM_WARPS, jl = e - k * GRAM_WARPS, jc = jb + jl;
                     if (k < c) {
                         double x = v[u];
@@ -734,24 +743,17 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 // pending for the next window: the log (CTA 0); the replicas take the
                 // move's per-centroid state now (two threads per CTA, identical
                 // inputs → identical replicas), the Ŝ update later
-                {
-                    const int f = mfrom, t = mto;
+                if (tid == 0 && rank == 0) {  // the log holds the counts before the move
                     int* lg = a.log + 5 * (int64_t)nlog;
-                    if (tid == 0) {  // the log holds the counts before the move
-                        if (rank == 0) {
-                            lg[0] = jj;
-                            lg[1] = f;
-                            lg[2] = t;
-                            lg[3] = cnt[f];
-                            __stcg(a.labels + jj, t);
-                        }
-                        gram_side(0, sc[f], cf[f], cnt[f], mvin[0], mvin[2], mvin[3], mvin[4], gamG);
-                    }
-                    if (tid == 32) {
-                        if (rank == 0) lg[4] = cnt[t];
-                        gram_side(1, sc[t], cf[t], cnt[t], mvin[1], mvin[2], mvin[3], mvin[4], gamG);
-                    }
+                    lg[0] = jj;
+                    lg[1] = mfrom;
+                    lg[2] = mto;
+                    lg[3] = cnt[mfrom];
+                    lg[4] = cnt[mto];
+                    __stcg(a.labels + jj, mto);
                 }
+#pragma unroll
+                for (int q = 0; q < MVW; ++q) pmv[q] = mvin[q];
                 lap(7);
                 pj = jj;
                 pf = mfrom;
@@ -764,7 +766,12 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
         ++pass;
         if (!improved || pass >= a.max_pass) break;
     }
-    // the last move's label was written when it was elected; its Ŝ update is not needed
+    // the last move's label was written when it was elected; its counts go to
+    // the output (its scalars and Ŝ update are no longer needed)
+    if (pj >= 0) {
+        if (tid == 0) --cnt[pf];
+        if (tid == 32) ++cnt[pt];
+    }
     __syncthreads();
     if (rank == 0) {
         for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];

@@ -634,24 +634,34 @@ struct KMeansEngine {
     bool gram_path() const { return gram != nullptr && c >= 2 && c <= kGramMaxC && !hart_ws_on(); }
     double gram_gamma() const { return (2.2 * (double)d + 4.0) * kU; }
     // G = MᵀM on the FP64 tensor cores + its diagonal bounds; the event marks completion
-    void compute_gram(cudaStream_t gs = nullptr) {
-        if (!gs) gs = st;
+    // G's storage and pointers (lent to the restart lanes before G is computed;
+    // its consumers wait on gram_ev)
+    void alloc_gram() {
         gG.ensure((size_t)n * n);
         gxx.ensure(n);
         gxn.ensure(n);
         gxl.ensure(n);
+        if (!gram_ev) CK(cudaEventCreateWithFlags(&gram_ev, cudaEventDisableTiming));
+        gram = gG.p;
+        gram_xx = gxx.p;
+        gram_xn = gxn.p;
+        gram_xl = gxl.p;
+    }
+    void compute_gram(cudaStream_t gs = nullptr) {
+        if (!gs) gs = st;
+        alloc_gram();
         const long long nb = ceil_div(n, GR_T);
         const long long tiles = nb * (nb + 1) / 2;
         const size_t sm = gram_smem<T>();
         smem_at_least((const void*)k_gram<T>, (size_t)(sm));
         cudaEvent_t e0 = nullptr, e1 = nullptr;
-        if (trace_on()) {
+        if (trace_on() && gs == st) {
             CK(cudaEventCreate(&e0));
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, gs));
         }
         k_gram<T><<<(unsigned)tiles, 256, sm, gs>>>(M, d, n, gG.p);
-        if (trace_on()) {
+        if (trace_on() && gs == st) {
             CK(cudaEventRecord(e1, gs));
             CK(cudaEventSynchronize(e1));
             float ms = 0.f;
@@ -692,6 +702,11 @@ struct KMeansEngine {
     void hartigan_gram(double* C, int* labels) {
         upload_groups();
         gram_reserve();
+        if (trace_on() && gram_ev) {
+            const auto tw = HClock::now();
+            CK(cudaEventSynchronize(gram_ev));
+            std::fprintf(stderr, "[respca] hartigan(gram): waited %.4fs for G\n", since(tw));
+        }
         if (gram_ev) CK(cudaStreamWaitEvent(st, gram_ev, 0));
         const double gamG = gram_gamma();
         {  // S⁰_k[j] = Σ_{m∈k} Ĝ[m][j]: the member-walk kernel of means_of over G's columns
@@ -1232,18 +1247,20 @@ struct KMeansEngine {
         CK(cudaEventRecord(ready, st));  // M is complete on the caller's stream
         // G = MᵀM on its own stream, overlapping the seeding and the Lloyd
         // steps; the refinements wait for it (gram_ev)
-        if (want_gram) {
+        // G = MᵀM on its own stream, overlapping the seedings and the Lloyd steps
+        // (RESPCA_GRAM_AFTER_PP=1: after the seedings; measured equal or slower)
+        const int gram_when = env_int("RESPCA_GRAM_AFTER_PP", 0);
+        auto launch_gram = [&](cudaEvent_t after) {
             if (!gram_st) {
-                // lowest priority: G fills the SMs the lanes' seeding and Lloyd
-                // steps (the critical path) leave idle
                 int lo = 0, hi = 0;
                 CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-                CK(cudaStreamCreateWithPriority(&gram_st, cudaStreamNonBlocking,
-                                                env_int("RESPCA_GRAM_LOWPRIO", 1) ? lo : hi));
+                CK(cudaStreamCreateWithPriority(&gram_st, cudaStreamNonBlocking, lo));
             }
-            CK(cudaStreamWaitEvent(gram_st, ready, 0));
+            CK(cudaStreamWaitEvent(gram_st, after, 0));
             compute_gram(gram_st);
-        }
+        };
+        if (want_gram) alloc_gram();  // pointers lent to the lanes below
+        if (want_gram && !gram_when) launch_gram(ready);
         while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
             {
@@ -1305,6 +1322,13 @@ struct KMeansEngine {
             joint_eng.assign(spec.begin(), spec.begin() + (size_t)std::min<uint64_t>(n_restarts, 8));
             joint_chosen = pp_joint(joint_eng);
             if (stats) stats->t_pp += since(tj);
+        }
+        if (want_gram && gram_when) {
+            cudaEvent_t seeded;
+            CK(cudaEventCreateWithFlags(&seeded, cudaEventDisableTiming));
+            CK(cudaEventRecord(seeded, st));
+            launch_gram(seeded);
+            CK(cudaEventDestroy(seeded));
         }
         std::mutex mu;
         std::condition_variable cv;

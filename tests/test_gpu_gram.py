@@ -91,6 +91,16 @@ def test_gram_exact_fallback_bitwise(cl):
     assert fallbacks(r.stderr) > 100, r.stderr[-2000:]
 
 
+@pytest.mark.parametrize("env", [{"RESPCA_LLOYD_INCR": "0"}, {"RESPCA_PP_JOINT": "0", "RESPCA_KM_LANES": "3"},
+                                 {"RESPCA_KM_LANES": "3"}])
+def test_init_switches_bitwise(env):
+    """Full Lloyd steps instead of incremental ones, restarts seeded one by
+    one, and restarts side by side (lanes): the same results."""
+    r = run(env)
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK ") == 6, r.stdout
+
+
 def test_per_pass_refinement_bitwise():
     r = run({"RESPCA_HART_GRAM": "0"})
     assert r.returncode == 0, r.stdout + r.stderr[-4000:]
