@@ -124,11 +124,14 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
     double* __restrict__ partials, int64_t d, int rowblocks,
     // optional BF16 copy of L′ in the K-major [n][dpad] layout the tcgen05
     // screen loads by TMA (nullptr: not written)
-    __nv_bfloat16* __restrict__ Lb, int64_t dpad) {
+    __nv_bfloat16* __restrict__ Lb, int64_t dpad,
+    // groups largest first (nullptr: in index order); partials stay per blockIdx
+    const int* __restrict__ gorder = nullptr) {
     __shared__ double red[32 * 5];
     if (ctl->done) return;  // loop already finished (bench launches ahead)
-    const int g = blockIdx.x / rowblocks;
-    const int rb = blockIdx.x - g * rowblocks;
+    const int gi = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - gi * rowblocks;
+    const int g = gorder ? __ldg(gorder + gi) : gi;
     const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
     const bool active = i0 < d;
 

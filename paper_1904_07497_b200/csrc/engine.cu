@@ -299,6 +299,10 @@ struct Alm : AlmBase {
     // (U 4: 79%, U 2 with 2 blocks/SM: 87%, U 12/16 spill).
     // With the BF16 L′ side output (lb_on) U 2 / 2 blocks per SM is best (876 vs
     // 826 iterations/s for U 8 / 1 block, which then spills).
+    int passf_lpt = [] {  // RESPCA_PASSF_LPT=1: groups largest first (measured 0.8 % slower at C3)
+        const char* e = std::getenv("RESPCA_PASSF_LPT");
+        return e ? std::atoi(e) : 0;
+    }();
     int passf_variant_env = [] {
         const char* e = std::getenv("RESPCA_PASSF");
         return e ? std::atoi(e) : -1;
@@ -309,7 +313,7 @@ struct Alm : AlmBase {
         k_pass_f<T, RR, U, MB><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
                                                     G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
                                                     partials.p, d, rowblocks, lb_on ? Lb.p : nullptr,
-                                                    dpad);
+                                                    dpad, passf_lpt ? km.gsize_ord.p : nullptr);
     }
     void launch_pass_f() {
         if (l21) {  // ℓ2,1: F1 only (the S/Θ half runs after the column norms)

@@ -356,7 +356,18 @@ struct KMeansEngine {
         CK(cudaMemcpyAsync(h_labels.data(), labels, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     }
+    // groups by size, largest first (group-walk kernels schedule the longest
+    // member walks first, so no single large group forms the tail)
+    DBuf<int> gsize_ord;
+    std::vector<int> h_gsize_ord;
     void upload_groups() {
+        h_gsize_ord.resize(c);
+        for (int k = 0; k < c; ++k) h_gsize_ord[k] = k;
+        if ((int)groups.counts.size() == c)
+            std::stable_sort(h_gsize_ord.begin(), h_gsize_ord.end(),
+                             [&](int x, int y) { return groups.counts[x] > groups.counts[y]; });
+        gsize_ord.ensure(c);
+        CK(cudaMemcpyAsync(gsize_ord.p, h_gsize_ord.data(), sizeof(int) * c, cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(goff.p, groups.goff.data(), sizeof(int) * (c + 1),
                            cudaMemcpyHostToDevice, st));
         CK(cudaMemcpyAsync(members.p, groups.members.data(), sizeof(int) * n,
