@@ -19,6 +19,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "km.cuh"  // cp.async helpers
 
 namespace respca_dev {
 
@@ -236,6 +237,110 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
             Cw[(int64_t)g * d + i0 + r] = cacc[r] * inv;
             Gn[(int64_t)g * d + i0 + r] = gacc[r];
         }
+    }
+    double v[5] = {pf, pl, ps, p1, psc};
+    block_sum<5>(v, red);
+    if (threadIdx.x == 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
+}
+
+// ---------------------------------------------------------------------------
+// Pass F for few groups (c·⌈d/512⌉ CTAs would not fill the GPU, e.g. c = 1):
+// the same per-element work and member-order sums as k_pass_f, one thread per
+// row, 64-thread CTAs, and each thread streams its row of the next U members'
+// X, S, Θ, L through a private cp.async ring in shared memory — the member
+// walk (sequential per row: the reference's summation order) keeps U·4
+// elements in flight per thread instead of the few a register batch holds.
+// ---------------------------------------------------------------------------
+constexpr int PFR_T = 64;  // default CTA rows
+template <typename T, int U, int NT = PFR_T>
+__global__ void __launch_bounds__(NT) k_pass_f_ring(
+    const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members, const double* G0, const double* G1,
+    double* Gn0, double* Gn1, double* __restrict__ Cw, const double* __restrict__ mean_w,
+    const Ctl* __restrict__ ctl, double* __restrict__ partials, int64_t d, int rowblocks,
+    __nv_bfloat16* __restrict__ Lb, int64_t dpad) {
+    __shared__ double red[32 * 5];
+    extern __shared__ __align__(16) unsigned char pfr_sm[];
+    auto ring = reinterpret_cast<T(*)[4][NT]>(pfr_sm);  // [stage][X, S, Θ, L][thread]
+    if (ctl->done) return;
+    const int g = blockIdx.x / rowblocks;
+    const int rb = blockIdx.x - g * rowblocks;
+    const int tid = threadIdx.x;
+    const int64_t i = (int64_t)rb * NT + tid;
+    const bool active = i < d;
+    const int par = ctl->parity;
+    const double* Gc = par ? G1 : G0;
+    double* Gn = par ? Gn0 : Gn1;
+    const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
+    const double mw = mean_w[g];
+    const int beg = goff[g], end = goff[g + 1];
+    const double ng = (double)(end - beg);
+    const double mscale = own_w / ng + mw;
+    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
+    if (active) {
+        const double Gi = Gc[(int64_t)g * d + i], mt = Gi * mscale;
+        double cacc = 0.0, gacc = 0.0;
+        auto issue = [&](int t) {
+            const int slot = (t - beg) % U;
+            const bool ok = t < end;
+            const int64_t off = ok ? (int64_t)__ldg(members + t) * d + i : 0;
+            if (sizeof(T) == 8) {
+                cp_async8(&ring[slot][0][tid], X + off, ok);
+                cp_async8(&ring[slot][1][tid], S + off, ok);
+                cp_async8(&ring[slot][2][tid], Th + off, ok);
+                cp_async8(&ring[slot][3][tid], L + off, ok);
+            } else {
+                cp_async4(&ring[slot][0][tid], X + off, ok);
+                cp_async4(&ring[slot][1][tid], S + off, ok);
+                cp_async4(&ring[slot][2][tid], Th + off, ok);
+                cp_async4(&ring[slot][3][tid], L + off, ok);
+            }
+            cp_commit();
+        };
+        for (int t = beg; t < beg + U - 1; ++t) issue(t);
+        for (int t = beg; t < end; ++t) {
+            issue(t + U - 1);  // refills the slot member t−1 used
+            cp_wait<U - 1>();
+            const int slot = (t - beg) % U;
+            const double x = (double)ring[slot][0][tid], s = (double)ring[slot][1][tid];
+            const double th = (double)ring[slot][2][tid], lold = (double)ring[slot][3][tid];
+            const int64_t off = (int64_t)__ldg(members + t) * d + i;
+            // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
+            const double q = th / rho;
+            const double dv = (x - s) + q;
+            const double ln = own_w * dv + mw * Gi;
+            cacc += ln;
+            const double xl = x - ln;
+            const double b = xl + q;
+            const double mag = fabs(b) - thr;
+            const double sn = mag > 0.0 ? copysign(mag, b) : 0.0;
+            const double rr = xl - sn;
+            const double tn = th + rho * rr;
+            gacc += (x - sn) + tn / rho_n;
+            pf += rr * rr;
+            const double dl = ln - lold;
+            pl += dl * dl;
+            const double ds = sn - s;
+            ps += ds * ds;
+            p1 += fabs(sn);
+            const double dm = ln - mt;
+            psc += dm * dm;
+            if (sizeof(T) == 8) {
+                __stcs(reinterpret_cast<double*>(L) + off, ln);
+                __stcs(reinterpret_cast<double*>(S) + off, sn);
+                __stcs(reinterpret_cast<double*>(Th) + off, tn);
+            } else {
+                __stcs(reinterpret_cast<float*>(L) + off, (float)ln);
+                __stcs(reinterpret_cast<float*>(S) + off, (float)sn);
+                __stcs(reinterpret_cast<float*>(Th) + off, (float)tn);
+            }
+            if (Lb) Lb[(int64_t)__ldg(members + t) * dpad + i] = __double2bfloat16(ln);
+        }
+        cp_wait<0>();
+        Cw[(int64_t)g * d + i] = cacc * (1.0 / ng);  // kmeans.cpp:78-79
+        Gn[(int64_t)g * d + i] = gacc;
     }
     double v[5] = {pf, pl, ps, p1, psc};
     block_sum<5>(v, red);

@@ -93,6 +93,25 @@ struct Alm : AlmBase {
     double lambda = 0.0;
     uint64_t budget = 0;
     int R = 1, rowblocks = 0, nbF = 0;
+    int nbP = 0;          // Pass F partials (CTAs) of the fast path
+    bool pf_ring = false;  // Pass F as k_pass_f_ring (few groups)
+    int ring_cfg() const {  // RESPCA_RING_CFG (tuning); measured: C3-c1 best 4, C5 best 0
+        const char* e = std::getenv("RESPCA_RING_CFG");
+        return e ? std::atoi(e) : (d <= 16384 ? 4 : 0);
+    }
+    int ring_nt() const {
+        switch (ring_cfg()) {
+            case 1: return 64;
+            case 2: return 128;
+            case 3: return 256;
+            case 4: return 128;
+            default: return 64;
+        }
+    }
+    int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
+        const char* e = std::getenv("RESPCA_PASSF_RING");
+        return e ? std::atoi(e) : 1;
+    }();
 
     DBuf<T> X, L, S, Th;
     DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm, bn;
@@ -220,7 +239,10 @@ struct Alm : AlmBase {
             CK(cudaMemsetAsync(Lb.p, 0, sizeof(__nv_bfloat16) * (size_t)n * dpad, st));  // K padding stays 0
         }
         nbF = rowblocks * c;
-        partials.ensure((size_t)nbF * 5);
+        // few groups: the ring variant of Pass F (64-row CTAs) fills the GPU
+        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && nbF < 2 * 148 && passf_ring_env != 0;
+        nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
+        partials.ensure((size_t)std::max(nbF, nbP) * 5);
         Ctl h{};
         h.rho = cfg.rho0;
         const double rn = cfg.rho0 * cfg.kappa;
@@ -329,6 +351,25 @@ struct Alm : AlmBase {
             ln.add();
             return;
         }
+        if (pf_ring) {
+            double* G1 = G.p + (size_t)d * c;
+            auto go = [&](auto kf, int nt, int u) {
+                const size_t sm = (size_t)u * 4 * nt * sizeof(T);
+                CK(cudaFuncSetAttribute((const void*)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+                const int rbr = ceil_div(d, nt);
+                kf<<<rbr * c, nt, sm, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p, G.p, G1, G.p, G1, Cw.p,
+                                            mean_w.p, ctl.p, partials.p, d, rbr, lb_on ? Lb.p : nullptr, dpad);
+            };
+            switch (ring_cfg()) {
+                case 1: go(k_pass_f_ring<T, 32, 64>, 64, 32); break;
+                case 2: go(k_pass_f_ring<T, 16, 128>, 128, 16); break;
+                case 3: go(k_pass_f_ring<T, 16, 256>, 256, 16); break;
+                case 4: go(k_pass_f_ring<T, 32, 128>, 128, 32); break;
+                default: go(k_pass_f_ring<T, 16, 64>, 64, 16); break;
+            }
+            ln.add();
+            return;
+        }
         if (R == 2) {
             const int passf_variant = passf_variant_env >= 0 ? passf_variant_env : (lb_on ? 2 : 4);
             switch (passf_variant) {
@@ -371,7 +412,7 @@ struct Alm : AlmBase {
         ln.add(3);
     }
     void launch_finalize(bool cond) {
-        k_finalize<<<1, 1024, 0, st>>>(ctl.p, partials.p, nbF, km.goff.p, mean_w.p, c, rep.p,
+        k_finalize<<<1, 1024, 0, st>>>(ctl.p, partials.p, l21 ? nbF : nbP, km.goff.p, mean_w.p, c, rep.p,
                                        cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
         ln.add();
     }

@@ -117,7 +117,11 @@ class Workload:
 
     def make(self, with_truth: bool = False, out: np.ndarray | None = None):
         if self.kind == "video":
-            return video(frames=self.n, seed=self.seed, with_truth=with_truth)
+            v = video(frames=self.n, seed=self.seed, with_truth=with_truth)
+            if out is not None and not with_truth:  # callers that pass `out` read it
+                out[...] = v
+                return out
+            return v
         return rpca(self.d, self.n, self.r, self.sigma, self.p, seed=self.seed,
                     with_truth=with_truth, out=out)
 
