@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
 // elements in flight per thread instead of the few a register batch holds.
 // ---------------------------------------------------------------------------
 constexpr int PFR_T = 64;  // default CTA rows
-template <typename T, int U, int NT = PFR_T>
+template <typename T, int U, int NT = PFR_T, int B = 1>
 __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members, const double* G0, const double* G1,
@@ -299,44 +299,66 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
             }
             cp_commit();
         };
-        for (int t = beg; t < beg + U - 1; ++t) issue(t);
-        for (int t = beg; t < end; ++t) {
-            issue(t + U - 1);  // refills the slot member t−1 used
-            cp_wait<U - 1>();
-            const int slot = (t - beg) % U;
-            const double x = (double)ring[slot][0][tid], s = (double)ring[slot][1][tid];
-            const double th = (double)ring[slot][2][tid], lold = (double)ring[slot][3][tid];
-            const int64_t off = (int64_t)__ldg(members + t) * d + i;
-            // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
-            const double q = th / rho;
-            const double dv = (x - s) + q;
-            const double ln = own_w * dv + mw * Gi;
-            cacc += ln;
-            const double xl = x - ln;
-            const double b = xl + q;
-            const double mag = fabs(b) - thr;
-            const double sn = mag > 0.0 ? copysign(mag, b) : 0.0;
-            const double rr = xl - sn;
-            const double tn = th + rho * rr;
-            gacc += (x - sn) + tn / rho_n;
-            pf += rr * rr;
-            const double dl = ln - lold;
-            pl += dl * dl;
-            const double ds = sn - s;
-            ps += ds * ds;
-            p1 += fabs(sn);
-            const double dm = ln - mt;
-            psc += dm * dm;
-            if (sizeof(T) == 8) {
-                __stcs(reinterpret_cast<double*>(L) + off, ln);
-                __stcs(reinterpret_cast<double*>(S) + off, sn);
-                __stcs(reinterpret_cast<double*>(Th) + off, tn);
-            } else {
-                __stcs(reinterpret_cast<float*>(L) + off, (float)ln);
-                __stcs(reinterpret_cast<float*>(S) + off, (float)sn);
-                __stcs(reinterpret_cast<float*>(Th) + off, (float)tn);
+        // batches of B members: their element chains are independent (ILP),
+        // the sums take them in member order afterwards
+        static_assert(U % B == 0 && U >= 2 * B, "ring");
+        for (int t = beg; t < beg + U; ++t) issue(t);
+        for (int t0 = beg; t0 < end; t0 += B) {
+            cp_wait<U - B>();
+            double ln[B], sm[B], xs[B], ss[B], ts[B], lo[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                const int slot = (t0 + u - beg) % U;
+                xs[u] = (double)ring[slot][0][tid];
+                ss[u] = (double)ring[slot][1][tid];
+                ts[u] = (double)ring[slot][2][tid];
+                lo[u] = (double)ring[slot][3][tid];
             }
-            if (Lb) Lb[(int64_t)__ldg(members + t) * dpad + i] = __double2bfloat16(ln);
+            // every thread's reads of the B slots are done before they refill
+#pragma unroll
+            for (int u = 0; u < B; ++u) issue(t0 + U + u);
+            double sn[B], tn[B], rr[B];
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
+                const double x = xs[u], s = ss[u], th = ts[u];
+                const double q = th / rho;
+                const double dv = (x - s) + q;
+                ln[u] = own_w * dv + mw * Gi;
+                const double xl = x - ln[u];
+                const double b = xl + q;
+                const double mag = fabs(b) - thr;
+                sn[u] = mag > 0.0 ? copysign(mag, b) : 0.0;
+                rr[u] = xl - sn[u];
+                tn[u] = th + rho * rr[u];
+                sm[u] = (x - sn[u]) + tn[u] / rho_n;
+            }
+#pragma unroll
+            for (int u = 0; u < B; ++u) {
+                if (t0 + u >= end) break;
+                cacc += ln[u];
+                gacc += sm[u];
+                pf += rr[u] * rr[u];
+                const double dl = ln[u] - lo[u];
+                pl += dl * dl;
+                const double ds = sn[u] - ss[u];
+                ps += ds * ds;
+                p1 += fabs(sn[u]);
+                const double dm = ln[u] - mt;
+                psc += dm * dm;
+                const int col = __ldg(members + t0 + u);
+                const int64_t off = (int64_t)col * d + i;
+                if (sizeof(T) == 8) {
+                    __stcs(reinterpret_cast<double*>(L) + off, ln[u]);
+                    __stcs(reinterpret_cast<double*>(S) + off, sn[u]);
+                    __stcs(reinterpret_cast<double*>(Th) + off, tn[u]);
+                } else {
+                    __stcs(reinterpret_cast<float*>(L) + off, (float)ln[u]);
+                    __stcs(reinterpret_cast<float*>(S) + off, (float)sn[u]);
+                    __stcs(reinterpret_cast<float*>(Th) + off, (float)tn[u]);
+                }
+                if (Lb) Lb[(int64_t)col * dpad + i] = __double2bfloat16(ln[u]);
+            }
         }
         cp_wait<0>();
         Cw[(int64_t)g * d + i] = cacc * (1.0 / ng);  // kmeans.cpp:78-79

@@ -95,18 +95,13 @@ struct Alm : AlmBase {
     int R = 1, rowblocks = 0, nbF = 0;
     int nbP = 0;          // Pass F partials (CTAs) of the fast path
     bool pf_ring = false;  // Pass F as k_pass_f_ring (few groups)
-    int ring_cfg() const {  // RESPCA_RING_CFG (tuning); measured: C3-c1 best 4, C5 best 0
+    int ring_cfg() const {  // RESPCA_RING_CFG (tuning): default 5 = 4-deep ring, 2-member batches
         const char* e = std::getenv("RESPCA_RING_CFG");
-        return e ? std::atoi(e) : (d <= 16384 ? 4 : 0);
+        return e ? std::atoi(e) : 5;  // C5: 75.6 % of HBM peak; C3-c1 2.77 ms
     }
     int ring_nt() const {
-        switch (ring_cfg()) {
-            case 1: return 64;
-            case 2: return 128;
-            case 3: return 256;
-            case 4: return 128;
-            default: return 64;
-        }
+        const int r = ring_cfg();
+        return (r == 3 || r == 4) ? 128 : 64;
     }
     int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
         const char* e = std::getenv("RESPCA_PASSF_RING");
@@ -361,11 +356,14 @@ struct Alm : AlmBase {
                                             mean_w.p, ctl.p, partials.p, d, rbr, lb_on ? Lb.p : nullptr, dpad);
             };
             switch (ring_cfg()) {
-                case 1: go(k_pass_f_ring<T, 32, 64>, 64, 32); break;
-                case 2: go(k_pass_f_ring<T, 16, 128>, 128, 16); break;
-                case 3: go(k_pass_f_ring<T, 16, 256>, 256, 16); break;
-                case 4: go(k_pass_f_ring<T, 32, 128>, 128, 32); break;
-                default: go(k_pass_f_ring<T, 16, 64>, 64, 16); break;
+                case 1: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
+                case 2: go(k_pass_f_ring<T, 16, 64, 4>, 64, 16); break;
+                case 3: go(k_pass_f_ring<T, 8, 128, 4>, 128, 8); break;
+                case 4: go(k_pass_f_ring<T, 16, 128, 4>, 128, 16); break;
+                case 5: go(k_pass_f_ring<T, 4, 64, 2>, 64, 4); break;
+                case 6: go(k_pass_f_ring<T, 8, 64, 2>, 64, 8); break;
+                case 7: go(k_pass_f_ring<T, 4, 64, 1>, 64, 4); break;
+                default: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
             }
             ln.add();
             return;
