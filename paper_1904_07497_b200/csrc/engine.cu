@@ -129,6 +129,10 @@ struct Alm : AlmBase {
         return !(e && (e[0] == '0' || e[0] == '1'));
     }();
     bool lb_on = false;
+    // the BF16 screens (κ ≈ 2⁻⁸·(‖x‖+‖c‖)²) decide nothing when the clusters
+    // are tight relative to the data norm (e.g. near-identical video frames):
+    // then the FP64 DMMA screen runs instead (set per solve from kmeans(X))
+    bool tc_useless = false;
     int64_t dpad = 0;
     DBuf<__nv_bfloat16> Lb;
 
@@ -211,6 +215,7 @@ struct Alm : AlmBase {
 
     void setup_state() {
         const int64_t N = d * n;
+        tc_useless = false;
         lambda = cfg.has_lambda ? cfg.lambda : std::sqrt((double)std::max<int64_t>(d, n));
         budget = cfg.has_fixed_iters ? cfg.fixed_iters : cfg.max_iter;
         CK(cudaMemcpyAsync(L.p, X.p, sizeof(T) * N, cudaMemcpyDeviceToDevice, st));
@@ -235,7 +240,10 @@ struct Alm : AlmBase {
         }
         nbF = rowblocks * c;
         // few groups: the ring variant of Pass F (64-row CTAs) fills the GPU
-        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && nbF < 2 * 148 && passf_ring_env != 0;
+        // (also for fp32 storage, where it beats the register-batched kernel: C4
+        // 0.74 -> 0.56 ms, C3-f32 0.83 -> 0.81 ms; fp64 C3 keeps k_pass_f: 1.03 vs 1.14 ms)
+        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0 &&
+                  (nbF < 2 * 148 || passf_ring_env == 2 || sizeof(T) == 4);
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
         partials.ensure((size_t)std::max(nbF, nbP) * 5);
         Ctl h{};
@@ -273,8 +281,13 @@ struct Alm : AlmBase {
             km.h_labels.assign(n, 0);
         } else {
             const uint64_t restarts = std::max<uint64_t>(cfg.km_n_restarts, 5);
-            km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, nullptr,
+            double inertia = 0.0;
+            km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, &inertia,
                       nullptr);
+            // mean squared distance to the own centroid vs the scale (‖x‖+‖c‖)² ≈ 4‖x‖²
+            // of the BF16 bound: below 1/32 its intervals straddle every decision
+            tc_useless = !(inertia >= xnorm * xnorm * 4.0 / 32.0);
+            if (tc_useless && lb_on) lb_on = false;
             tr("kmeans");
             km.fetch_labels(labels.p);
         }
@@ -388,7 +401,7 @@ struct Alm : AlmBase {
     void launch_pass_a() {
         if (c <= 1) return;
         if (lb_on) km.screen_tma(Lb.p, dpad, Cw.p);         // tcgen05, operands by TMA from Pass F's BF16 L′
-        else if (use_tc && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05, fp64 → bf16 producers
+        else if (use_tc && !tc_useless && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05, fp64 → bf16 producers
         else km.screen(Cw.p);                               // FP64 DMMA screen
         km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);
         k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
@@ -422,7 +435,7 @@ struct Alm : AlmBase {
     bool cap_valid = false;
     void capture_if_needed() {
         const uint64_t key[12] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
-                                  (uint64_t)use_tc, (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
+                                  (uint64_t)(use_tc && !tc_useless), (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
                                   (uint64_t)passf_variant_env, (uint64_t)dpad, g_alloc_gen.load()};
         if (cap_valid && std::equal(key, key + 12, cap_key)) return;
         cap_valid = false;

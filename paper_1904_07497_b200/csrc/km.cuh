@@ -654,6 +654,78 @@ __global__ void __launch_bounds__(128) k_exact_cols(const T* __restrict__ M,
     }
 }
 
+// The same exact chains, warp-transposed for long lists (many undecidable
+// columns, e.g. near-identical video frames): lane = listed column, each lane
+// runs KC centroids' chains (ascending i, the reference's order) on 32×32
+// column tiles and KC×32 centroid tiles streamed through a cp.async ring.
+// Grid: (warp groups of 32 listed columns, centroid chunks of KC).
+template <typename T, int KC>
+__global__ void __launch_bounds__(64) k_exact_cols_tile(const T* __restrict__ M, const double* __restrict__ C,
+                                                        int64_t d, int c, const int* __restrict__ list,
+                                                        const unsigned* __restrict__ count,
+                                                        double* __restrict__ out) {
+    constexpr int PD = 4, W = 2;
+    extern __shared__ __align__(16) unsigned char ex_sm[];
+    auto tile = reinterpret_cast<T(*)[PD][32][33]>(ex_sm);                                // [W][PD][32][33]
+    auto ctile = reinterpret_cast<double(*)[PD][KC][32]>(ex_sm + sizeof(T) * W * PD * 32 * 33);  // [W][PD][KC][32]
+    const unsigned cnt = *count;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const unsigned e0 = (blockIdx.x * W + w) * 32u;
+    if (e0 >= cnt) return;
+    const int k0 = blockIdx.y * KC;
+    const int64_t ntile = (d + 31) / 32;
+    // lane's column (list entry e0 + lane; past the end: repeat entry e0, not stored)
+    const bool mine = e0 + lane < cnt;
+    int cols[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) cols[q] = __ldg(list + (e0 + q < cnt ? e0 + q : e0));
+    auto issue = [&](int64_t t) {
+        const int slot = (int)(t % PD);
+        const int64_t i = t * 32 + lane;
+        const bool okr = i < d;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const T* src = okr ? M + (int64_t)cols[q] * d + i : M;
+            if (sizeof(T) == 8) cp_async8(&tile[w][slot][q][lane], src, okr);
+            else cp_async4(&tile[w][slot][q][lane], src, okr);
+        }
+#pragma unroll
+        for (int k = 0; k < KC; ++k) {
+            const bool ok = okr && k0 + k < c;
+            cp_async8(&ctile[w][slot][k][lane], ok ? C + (int64_t)(k0 + k) * d + i : C, ok);
+        }
+        cp_commit();
+    };
+    for (int64_t t = 0; t < PD - 1; ++t) {
+        if (t < ntile) issue(t);
+        else cp_commit();
+    }
+    double s[KC];
+#pragma unroll
+    for (int k = 0; k < KC; ++k) s[k] = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + PD - 1 < ntile) issue(t + PD - 1);
+        else cp_commit();
+        cp_wait<PD - 1>();
+        __syncwarp();
+        const int slot = (int)(t % PD);
+        const int lim = (int)((d - t * 32) < 32 ? (d - t * 32) : 32);
+        for (int r = 0; r < lim; ++r) {
+            const double x = (double)tile[w][slot][lane][r];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const double tt = x - ctile[w][slot][k][r];  // kmeans.cpp:15-16
+                s[k] += tt * tt;
+            }
+        }
+        __syncwarp();
+    }
+    if (mine)
+#pragma unroll
+        for (int k = 0; k < KC; ++k)
+            if (k0 + k < c) out[(int64_t)(e0 + lane) * c + k0 + k] = s[k];
+}
+
 // Re-decide the listed (ambiguous) columns with exact distances.
 __global__ void __launch_bounds__(256) k_redecide(const double* __restrict__ exact, int c,
                                                   const int* __restrict__ list,

@@ -326,12 +326,27 @@ struct KMeansEngine {
         return s;
     }
 
+    // long chains over few centroids: the warp-transposed exact kernel
+    bool exact_tiled() const {
+        const int e = env_int("RESPCA_EXACT_TILED", -1);
+        if (e >= 0) return e != 0;
+        return c <= 16 && d >= 4096;
+    }
     // decide (+ exact fallback for ambiguous columns); returns #ambiguous
     void decide(const double* C, const int* old_labels, const int* cnts, int mode, int* out_labels,
                 Ctl* ctl) {
         k_decide<<<ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(screen_view(), n, c, old_labels,
                                                                  cnts, mode, out_labels, amb.p,
                                                                  ctl, trace_on() ? 1 : 0);
+        if (exact_tiled()) {
+            // the list length is known only on the device: a grid for all n
+            // columns, warps past the count return at once
+            constexpr int KC = 4;
+            const size_t sm = sizeof(T) * 2 * 4 * 32 * 33 + sizeof(double) * 2 * 4 * KC * 32;
+            smem_at_least((const void*)k_exact_cols_tile<T, KC>, sm);
+            k_exact_cols_tile<T, KC><<<dim3(ceil_div(n, 64), ceil_div(c, KC)), 64, sm, st>>>(
+                M, C, d, c, amb.p, &ctl->ambiguous, exact.p);
+        } else
         k_exact_cols<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous,
                                                              exact.p);
         k_redecide<<<std::min(ceil_div((int64_t)n * 32, 256), 4 * 148), 256, 0, st>>>(
