@@ -106,3 +106,38 @@ def test_per_pass_refinement_bitwise():
     assert r.returncode == 0, r.stdout + r.stderr[-4000:]
     assert r.stdout.count(" OK ") == 6, r.stdout
     assert "hartigan(gram" not in r.stderr
+
+
+SHAPES = r"""
+import sys, numpy as np
+sys.path.insert(0, 'tests'); sys.path.insert(0, '.')
+from oracle import oracle as O
+from paper_1904_07497_b200 import respca as R
+from paper_1904_07497_b200.respca import KMeansConfig
+from helpers import bitwise
+orc = O.port()
+rng = np.random.default_rng(11)
+bad = 0
+# odd d / n (scalar copies, partial tiles), every KPL width (c ≤ 32, 64, 128, 256)
+for d, n, c, seed in ((37, 517, 7, 1), (300, 1025, 33, 2), (64, 900, 70, 3), (21, 1300, 129, 4),
+                      (16, 1500, 256, 5), (3, 40, 2, 6)):
+    m = np.asfortranarray(rng.normal(0, 1, (d, n)) + (rng.random((d, n)) < 0.1) * rng.uniform(-20, 20, (d, n)))
+    a = R.kmeans(m, KMeansConfig(c=c, seed=seed, n_restarts=2))
+    lab, cen, inertia, it = orc.kmeans(m, c, 100, 2, seed, 1e-6)
+    ok = (a.assignment == lab).all() and bitwise(a.centroids, cen) and a.inertia == inertia and a.iters_run == it
+    print("SHAPE", d, n, c, "OK" if ok else "BAD", flush=True)
+    bad += not ok
+sys.exit(1 if bad else 0)
+"""
+
+
+@pytest.mark.parametrize("cl", ["1", "8"])
+def test_gram_shapes_bitwise(cl):
+    """Odd row/column counts, partial Gram tiles and every lanes-per-centroid
+    width of the refinement kernel (c up to its 256 limit)."""
+    env = dict(os.environ, RESPCA_TRACE="1", RESPCA_GRAM_CL=cl)
+    r = subprocess.run([sys.executable, "-c", SHAPES], cwd=ROOT, env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK") == 6, r.stdout
+    assert r.stderr.count("hartigan(gram, CL=") >= 6, r.stderr[-2000:]
