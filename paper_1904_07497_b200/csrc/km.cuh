@@ -880,12 +880,34 @@ __global__ void __launch_bounds__(64) k_pp_d2_multi(const T* __restrict__ M, int
         __syncwarp();
         const int slot = (int)(t % PD);
         const int lim = (int)((d - t * 32) < 32 ? (d - t * 32) : 32);
-        for (int q = 0; q < lim; ++q) {
-            const double x = (double)tile[w][slot][lane][q];
+        if (lim == 32) {
+            // full tile: rows in batches of 8 (the shared-memory loads of a batch
+            // issue together; each chain still adds in ascending row order)
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double tt = x - (double)lastv[w][slot][r][q];
-                s[r] += tt * tt;
+            for (int q0 = 0; q0 < 32; q0 += 8) {
+                double x[8], lv[R][8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = (double)tile[w][slot][lane][q0 + u];
+#pragma unroll
+                for (int r = 0; r < R; ++r)
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) lv[r][u] = (double)lastv[w][slot][r][q0 + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const double tt = x[u] - lv[r][u];
+                        s[r] += tt * tt;
+                    }
+            }
+        } else {
+            for (int q = 0; q < lim; ++q) {
+                const double x = (double)tile[w][slot][lane][q];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const double tt = x - (double)lastv[w][slot][r][q];
+                    s[r] += tt * tt;
+                }
             }
         }
         __syncwarp();
