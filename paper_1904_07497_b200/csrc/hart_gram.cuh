@@ -50,7 +50,7 @@ size_t gram_smem() {
 
 template <typename T>
 __global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_t d, int n,
-                                                 double* __restrict__ G) {
+                                                 double* __restrict__ G, long long ntiles) {
     extern __shared__ __align__(16) unsigned char sm[];
     T* As = reinterpret_cast<T*>(sm);        // [ST][128][AS]  columns i0.. (rows of A)
     T* Bs = As + GR_ST * GR_T * GR_AS;       // [ST][128][AS]  columns j0..
@@ -58,8 +58,10 @@ __global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t4 = lane & 3;
     const int wr = warp >> 2, wc = warp & 3;
-    // triangular tile index → (bi ≥ bj)
-    const long long tix = blockIdx.x;
+    // a grid smaller than the tile count loops over tiles (G can then share
+    // the GPU with the restarts' seeding and Lloyd steps)
+    for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    __syncthreads();  // the previous tile's stages are free
     int bi = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
     while ((long long)(bi + 1) * (bi + 2) / 2 <= tix) ++bi;
     while ((long long)bi * (bi + 1) / 2 > tix) --bi;
@@ -155,6 +157,7 @@ __global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_
                     __stcg(G + (int64_t)r * n + q, acc[x][y][z]);
                 }
             }
+    }
 }
 
 // diagonal: xx = Ĝ_jj, xn ≥ ‖x_j‖ ≥ xl (|Ĝ_jj − ‖x_j‖²| ≤ γ_G‖x_j‖²)

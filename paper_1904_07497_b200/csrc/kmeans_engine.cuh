@@ -686,7 +686,9 @@ struct KMeansEngine {
             CK(cudaEventCreate(&e1));
             CK(cudaEventRecord(e0, gs));
         }
-        k_gram<T><<<(unsigned)tiles, 256, sm, gs>>>(M, d, n, gG.p);
+        const int gctas = env_int("RESPCA_GRAM_CTAS", 0);  // 0: one CTA per tile
+        k_gram<T><<<(unsigned)(gctas > 0 ? std::min<long long>(gctas, tiles) : tiles), 256, sm, gs>>>(M, d, n, gG.p,
+                                                                                                     tiles);
         if (trace_on() && gs == st) {
             CK(cudaEventRecord(e1, gs));
             CK(cudaEventSynchronize(e1));
