@@ -254,21 +254,23 @@ __global__ void __launch_bounds__(256, MINB) k_pass_f(
 // elements in flight per thread instead of the few a register batch holds.
 // ---------------------------------------------------------------------------
 constexpr int PFR_T = 64;  // default CTA rows
-template <typename T, int U, int NT = PFR_T, int B = 1>
+template <typename T, int U, int NT = PFR_T, int B = 1, int RW = 1>
 __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members, const double* G0, const double* G1,
     double* Gn0, double* Gn1, double* __restrict__ Cw, const double* __restrict__ mean_w,
     const Ctl* __restrict__ ctl, double* __restrict__ partials, int64_t d, int rowblocks,
     __nv_bfloat16* __restrict__ Lb, int64_t dpad) {
+    // RW rows per thread (RW = 2 needs d even): one 2·sizeof(T)-byte copy per
+    // array and member, so a warp moves 32·RW·sizeof(T) contiguous bytes
     __shared__ double red[32 * 5];
     extern __shared__ __align__(16) unsigned char pfr_sm[];
-    auto ring = reinterpret_cast<T(*)[4][NT]>(pfr_sm);  // [stage][X, S, Θ, L][thread]
+    auto ring = reinterpret_cast<T(*)[4][NT * RW]>(pfr_sm);  // [stage][X, S, Θ, L][row]
     if (ctl->done) return;
     const int g = blockIdx.x / rowblocks;
     const int rb = blockIdx.x - g * rowblocks;
     const int tid = threadIdx.x;
-    const int64_t i = (int64_t)rb * NT + tid;
+    const int64_t i = ((int64_t)rb * NT + tid) * RW;
     const bool active = i < d;
     const int par = ctl->parity;
     const double* Gc = par ? G1 : G0;
@@ -280,23 +282,27 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const double mscale = own_w / ng + mw;
     double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
     if (active) {
-        const double Gi = Gc[(int64_t)g * d + i], mt = Gi * mscale;
-        double cacc = 0.0, gacc = 0.0;
+        double Gi[RW], mt[RW], cacc[RW], gacc[RW];
+#pragma unroll
+        for (int w = 0; w < RW; ++w) {
+            Gi[w] = Gc[(int64_t)g * d + i + w];
+            mt[w] = Gi[w] * mscale;
+            cacc[w] = 0.0;
+            gacc[w] = 0.0;
+        }
+        auto cp = [&](T* dst, const T* src, bool ok) {
+            if (RW * sizeof(T) == 16) cp_async16(dst, ok ? src : X, ok ? 16 : 0);
+            else if (RW * sizeof(T) == 8) cp_async8(dst, ok ? src : X, ok);
+            else cp_async4(dst, ok ? src : X, ok);
+        };
         auto issue = [&](int t) {
             const int slot = (t - beg) % U;
             const bool ok = t < end;
             const int64_t off = ok ? (int64_t)__ldg(members + t) * d + i : 0;
-            if (sizeof(T) == 8) {
-                cp_async8(&ring[slot][0][tid], X + off, ok);
-                cp_async8(&ring[slot][1][tid], S + off, ok);
-                cp_async8(&ring[slot][2][tid], Th + off, ok);
-                cp_async8(&ring[slot][3][tid], L + off, ok);
-            } else {
-                cp_async4(&ring[slot][0][tid], X + off, ok);
-                cp_async4(&ring[slot][1][tid], S + off, ok);
-                cp_async4(&ring[slot][2][tid], Th + off, ok);
-                cp_async4(&ring[slot][3][tid], L + off, ok);
-            }
+            cp(&ring[slot][0][tid * RW], X + off, ok);
+            cp(&ring[slot][1][tid * RW], S + off, ok);
+            cp(&ring[slot][2][tid * RW], Th + off, ok);
+            cp(&ring[slot][3][tid * RW], L + off, ok);
             cp_commit();
         };
         // batches of B members: their element chains are independent (ILP),
@@ -305,64 +311,86 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
         for (int t = beg; t < beg + U; ++t) issue(t);
         for (int t0 = beg; t0 < end; t0 += B) {
             cp_wait<U - B>();
-            double ln[B], sm[B], xs[B], ss[B], ts[B], lo[B];
+            double xs[B][RW], ss[B][RW], ts[B][RW], lo[B][RW];
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 const int slot = (t0 + u - beg) % U;
-                xs[u] = (double)ring[slot][0][tid];
-                ss[u] = (double)ring[slot][1][tid];
-                ts[u] = (double)ring[slot][2][tid];
-                lo[u] = (double)ring[slot][3][tid];
+#pragma unroll
+                for (int w = 0; w < RW; ++w) {
+                    xs[u][w] = (double)ring[slot][0][tid * RW + w];
+                    ss[u][w] = (double)ring[slot][1][tid * RW + w];
+                    ts[u][w] = (double)ring[slot][2][tid * RW + w];
+                    lo[u][w] = (double)ring[slot][3][tid * RW + w];
+                }
             }
-            // every thread's reads of the B slots are done before they refill
+            // this thread's reads of the B slots are done before they refill
 #pragma unroll
             for (int u = 0; u < B; ++u) issue(t0 + U + u);
-            double sn[B], tn[B], rr[B];
+            double ln[B][RW], sn[B][RW], tn[B][RW], rr[B][RW], sm[B][RW];
 #pragma unroll
-            for (int u = 0; u < B; ++u) {
-                // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
-                const double x = xs[u], s = ss[u], th = ts[u];
-                const double q = th / rho;
-                const double dv = (x - s) + q;
-                ln[u] = own_w * dv + mw * Gi;
-                const double xl = x - ln[u];
-                const double b = xl + q;
-                const double mag = fabs(b) - thr;
-                sn[u] = mag > 0.0 ? copysign(mag, b) : 0.0;
-                rr[u] = xl - sn[u];
-                tn[u] = th + rho * rr[u];
-                sm[u] = (x - sn[u]) + tn[u] / rho_n;
-            }
+            for (int u = 0; u < B; ++u)
+#pragma unroll
+                for (int w = 0; w < RW; ++w) {
+                    // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
+                    const double x = xs[u][w], s = ss[u][w], th = ts[u][w];
+                    const double q = th / rho;
+                    const double dv = (x - s) + q;
+                    ln[u][w] = own_w * dv + mw * Gi[w];
+                    const double xl = x - ln[u][w];
+                    const double b = xl + q;
+                    const double mag = fabs(b) - thr;
+                    sn[u][w] = mag > 0.0 ? copysign(mag, b) : 0.0;
+                    rr[u][w] = xl - sn[u][w];
+                    tn[u][w] = th + rho * rr[u][w];
+                    sm[u][w] = (x - sn[u][w]) + tn[u][w] / rho_n;
+                }
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 if (t0 + u >= end) break;
-                cacc += ln[u];
-                gacc += sm[u];
-                pf += rr[u] * rr[u];
-                const double dl = ln[u] - lo[u];
-                pl += dl * dl;
-                const double ds = sn[u] - ss[u];
-                ps += ds * ds;
-                p1 += fabs(sn[u]);
-                const double dm = ln[u] - mt;
-                psc += dm * dm;
                 const int col = __ldg(members + t0 + u);
                 const int64_t off = (int64_t)col * d + i;
-                if (sizeof(T) == 8) {
-                    __stcs(reinterpret_cast<double*>(L) + off, ln[u]);
-                    __stcs(reinterpret_cast<double*>(S) + off, sn[u]);
-                    __stcs(reinterpret_cast<double*>(Th) + off, tn[u]);
-                } else {
-                    __stcs(reinterpret_cast<float*>(L) + off, (float)ln[u]);
-                    __stcs(reinterpret_cast<float*>(S) + off, (float)sn[u]);
-                    __stcs(reinterpret_cast<float*>(Th) + off, (float)tn[u]);
+#pragma unroll
+                for (int w = 0; w < RW; ++w) {
+                    cacc[w] += ln[u][w];
+                    gacc[w] += sm[u][w];
+                    pf += rr[u][w] * rr[u][w];
+                    const double dl = ln[u][w] - lo[u][w];
+                    pl += dl * dl;
+                    const double ds = sn[u][w] - ss[u][w];
+                    ps += ds * ds;
+                    p1 += fabs(sn[u][w]);
+                    const double dm = ln[u][w] - mt[w];
+                    psc += dm * dm;
                 }
-                if (Lb) Lb[(int64_t)col * dpad + i] = __double2bfloat16(ln[u]);
+                double a_l[RW], a_s[RW], a_t[RW];
+#pragma unroll
+                for (int w = 0; w < RW; ++w) {
+                    a_l[w] = ln[u][w];
+                    a_s[w] = sn[u][w];
+                    a_t[w] = tn[u][w];
+                }
+                Vec<T, RW>::store(L + off, a_l);
+                Vec<T, RW>::store(S + off, a_s);
+                Vec<T, RW>::store(Th + off, a_t);
+                if (Lb) {
+                    __nv_bfloat16* lb = Lb + (int64_t)col * dpad + i;
+                    if (RW == 2) {
+                        __nv_bfloat162 b2;
+                        b2.x = __double2bfloat16(ln[u][0]);
+                        b2.y = __double2bfloat16(ln[u][RW - 1]);
+                        *reinterpret_cast<__nv_bfloat162*>(lb) = b2;
+                    } else {
+                        lb[0] = __double2bfloat16(ln[u][0]);
+                    }
+                }
             }
         }
         cp_wait<0>();
-        Cw[(int64_t)g * d + i] = cacc * (1.0 / ng);  // kmeans.cpp:78-79
-        Gn[(int64_t)g * d + i] = gacc;
+#pragma unroll
+        for (int w = 0; w < RW; ++w) {
+            Cw[(int64_t)g * d + i + w] = cacc[w] * (1.0 / ng);  // kmeans.cpp:78-79
+            Gn[(int64_t)g * d + i + w] = gacc[w];
+        }
     }
     double v[5] = {pf, pl, ps, p1, psc};
     block_sum<5>(v, red);

@@ -95,13 +95,16 @@ struct Alm : AlmBase {
     int R = 1, rowblocks = 0, nbF = 0;
     int nbP = 0;          // Pass F partials (CTAs) of the fast path
     bool pf_ring = false;  // Pass F as k_pass_f_ring (few groups)
-    int ring_cfg() const {  // RESPCA_RING_CFG (tuning): default 5 = 4-deep ring, 2-member batches
+    int ring_cfg() const {  // RESPCA_RING_CFG (tuning)
         const char* e = std::getenv("RESPCA_RING_CFG");
-        return e ? std::atoi(e) : 5;  // C5: 75.6 % of HBM peak; C3-c1 2.77 ms
+        if (e) return std::atoi(e);
+        // fp64: 4-deep ring, 2-member batches, a row per thread (C5 0.755 of the HBM
+        // peak); fp32 storage: two rows per thread, 128-thread CTAs (C3-f32 0.71, C4 0.79)
+        return (sizeof(T) == 4 && d % 2 == 0) ? 10 : 5;
     }
-    int ring_nt() const {
+    int ring_nt() const {  // rows per CTA of the ring variant
         const int r = ring_cfg();
-        return (r == 3 || r == 4) ? 128 : 64;
+        return r == 10 ? 256 : (r == 8 || r == 9) ? 128 : (r == 3 || r == 4) ? 128 : 64;
     }
     int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
         const char* e = std::getenv("RESPCA_PASSF_RING");
@@ -361,10 +364,10 @@ struct Alm : AlmBase {
         }
         if (pf_ring) {
             double* G1 = G.p + (size_t)d * c;
-            auto go = [&](auto kf, int nt, int u) {
-                const size_t sm = (size_t)u * 4 * nt * sizeof(T);
+            auto go = [&](auto kf, int nt, int u, int rw = 1) {
+                const size_t sm = (size_t)u * 4 * nt * rw * sizeof(T);
                 CK(cudaFuncSetAttribute((const void*)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-                const int rbr = ceil_div(d, nt);
+                const int rbr = ceil_div(d, (int64_t)nt * rw);
                 kf<<<rbr * c, nt, sm, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p, G.p, G1, G.p, G1, Cw.p,
                                             mean_w.p, ctl.p, partials.p, d, rbr, lb_on ? Lb.p : nullptr, dpad);
             };
@@ -376,6 +379,9 @@ struct Alm : AlmBase {
                 case 5: go(k_pass_f_ring<T, 4, 64, 2>, 64, 4); break;
                 case 6: go(k_pass_f_ring<T, 8, 64, 2>, 64, 8); break;
                 case 7: go(k_pass_f_ring<T, 4, 64, 1>, 64, 4); break;
+                case 8: go(k_pass_f_ring<T, 4, 64, 2, 2>, 64, 4, 2); break;
+                case 9: go(k_pass_f_ring<T, 8, 64, 2, 2>, 64, 8, 2); break;
+                case 10: go(k_pass_f_ring<T, 4, 128, 2, 2>, 128, 4, 2); break;
                 default: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
             }
             ln.add();
