@@ -245,8 +245,10 @@ struct Alm : AlmBase {
         // few groups: the ring variant of Pass F (64-row CTAs) fills the GPU
         // (also for fp32 storage, where it beats the register-batched kernel: C4
         // 0.74 -> 0.56 ms, C3-f32 0.83 -> 0.81 ms; fp64 C3 keeps k_pass_f: 1.03 vs 1.14 ms)
+        // (and for small matrices, ≤ 256 MB each: C2 0.068 -> 0.055 ms)
         pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0 &&
-                  (nbF < 2 * 148 || passf_ring_env == 2 || sizeof(T) == 4);
+                  (nbF < 2 * 148 || passf_ring_env == 2 || sizeof(T) == 4 ||
+                   (double)d * (double)n * sizeof(T) <= 256e6);
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
         partials.ensure((size_t)std::max(nbF, nbP) * 5);
         Ctl h{};
