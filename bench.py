@@ -387,7 +387,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
             "config": {**workload_config(w), "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),
-                         "kernel": "k_pass_f (fused L/S/Θ update + group sums + residuals)",
+                         "kernel": "k_pass_f_ring (Pass F: fused L/S/Θ update + group sums + residuals)",
                          "alg_bytes_per_launch": pf_bytes,
                          "alg_bytes_note": "7·N·s (X,S,Θ,L in; L,S,Θ out)" + (" + 2·N (BF16 L′ for the TMA-fed screen)" if lb_side else ""),
                          "avg_launch_ms": pf_avg,

@@ -98,13 +98,19 @@ struct Alm : AlmBase {
     int ring_cfg() const {  // RESPCA_RING_CFG (tuning)
         const char* e = std::getenv("RESPCA_RING_CFG");
         if (e) return std::atoi(e);
-        // fp64: 4-deep ring, 2-member batches, a row per thread (C5 0.755 of the HBM
-        // peak); fp32 storage: two rows per thread, 128-thread CTAs (C3-f32 0.71, C4 0.79)
-        return (sizeof(T) == 4 && d % 2 == 0) ? 10 : 5;
+        // measured on B200 (fraction of the HBM copy bandwidth):
+        //  few groups (c = 1): a row per thread, 4-deep ring, 2-member batches (C5 0.755)
+        //  fp32 storage: two rows per thread, 128-thread CTAs, 4-deep (C3-f32 0.71, C4 0.79)
+        //  fp64 up to 256 MB: the same (C2 0.685)
+        //  fp64 larger: two rows per thread, 256-thread CTAs, 8-deep, 4-member batches (C3 0.923)
+        if (d % 2 != 0 || c * ceil_div(d, 512) < 2 * 148) return 5;
+        if (sizeof(T) == 4 || (double)d * (double)n * sizeof(T) <= 256e6) return 10;
+        return 16;
     }
     int ring_nt() const {  // rows per CTA of the ring variant
         const int r = ring_cfg();
-        return r == 10 ? 256 : (r == 8 || r == 9) ? 128 : (r == 3 || r == 4) ? 128 : 64;
+        return (r == 12 || r == 16) ? 512 : (r == 10 || r == 11 || r == 13 || r == 14 || r == 17) ? 256
+               : (r == 8 || r == 9 || r == 15) ? 128 : (r == 3 || r == 4) ? 128 : 64;
     }
     int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
         const char* e = std::getenv("RESPCA_PASSF_RING");
@@ -242,13 +248,11 @@ struct Alm : AlmBase {
             CK(cudaMemsetAsync(Lb.p, 0, sizeof(__nv_bfloat16) * (size_t)n * dpad, st));  // K padding stays 0
         }
         nbF = rowblocks * c;
-        // few groups: the ring variant of Pass F (64-row CTAs) fills the GPU
-        // (also for fp32 storage, where it beats the register-batched kernel: C4
-        // 0.74 -> 0.56 ms, C3-f32 0.83 -> 0.81 ms; fp64 C3 keeps k_pass_f: 1.03 vs 1.14 ms)
-        // (and for small matrices, ≤ 256 MB each: C2 0.068 -> 0.055 ms)
-        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0 &&
-                  (nbF < 2 * 148 || passf_ring_env == 2 || sizeof(T) == 4 ||
-                   (double)d * (double)n * sizeof(T) <= 256e6);
+        // Pass F as k_pass_f_ring (a private cp.async ring per thread, ring_cfg()):
+        // every shape measured is faster with it than with the register-batched
+        // k_pass_f (C3 1.026 -> 0.974 ms, C5 24.8 -> 18.4, C4 0.74 -> 0.45);
+        // RESPCA_PASSF_RING=0 keeps k_pass_f
+        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0;
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
         partials.ensure((size_t)std::max(nbF, nbP) * 5);
         Ctl h{};
@@ -384,6 +388,13 @@ struct Alm : AlmBase {
                 case 8: go(k_pass_f_ring<T, 4, 64, 2, 2>, 64, 4, 2); break;
                 case 9: go(k_pass_f_ring<T, 8, 64, 2, 2>, 64, 8, 2); break;
                 case 10: go(k_pass_f_ring<T, 4, 128, 2, 2>, 128, 4, 2); break;
+                case 11: go(k_pass_f_ring<T, 8, 128, 2, 2>, 128, 8, 2); break;
+                case 12: go(k_pass_f_ring<T, 4, 256, 2, 2>, 256, 4, 2); break;
+                case 13: go(k_pass_f_ring<T, 6, 128, 2, 2>, 128, 6, 2); break;
+                case 14: go(k_pass_f_ring<T, 8, 128, 4, 2>, 128, 8, 2); break;
+                case 15: go(k_pass_f_ring<T, 8, 64, 4, 2>, 64, 8, 2); break;
+                case 16: go(k_pass_f_ring<T, 8, 256, 4, 2>, 256, 8, 2); break;
+                case 17: go(k_pass_f_ring<T, 12, 128, 4, 2>, 128, 12, 2); break;
                 default: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
             }
             ln.add();
