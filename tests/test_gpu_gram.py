@@ -66,7 +66,7 @@ def run(env_extra):
     return r
 
 
-@pytest.mark.parametrize("cl", ["1", "2", "4", "8"])
+@pytest.mark.parametrize("cl", ["1", "2", "4", "8", "16"])
 def test_gram_refinement_bitwise(cl):
     r = run({"RESPCA_GRAM_CL": cl})
     assert r.returncode == 0, r.stdout + r.stderr[-4000:]
