@@ -352,7 +352,7 @@ RESPCA_DEV int gram_decide(int from, int c, const GramCoef* cf, const int* cnt, 
     return 1;
 }
 
-constexpr int GRAM_THREADS = 512;
+constexpr int GRAM_THREADS = 256;
 constexpr int GRAM_WARPS = GRAM_THREADS / 32;
 
 // The move m: from → to (kmeans.cpp:122-135) on one side's scalars (side 0 =
