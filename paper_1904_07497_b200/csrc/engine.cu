@@ -95,22 +95,24 @@ struct Alm : AlmBase {
     int R = 1, rowblocks = 0, nbF = 0;
     int nbP = 0;          // Pass F partials (CTAs) of the fast path
     bool pf_ring = false;  // Pass F as k_pass_f_ring (few groups)
-    int ring_cfg() const {  // RESPCA_RING_CFG (tuning)
-        const char* e = std::getenv("RESPCA_RING_CFG");
-        if (e) return std::atoi(e);
+    int ring_cfg() const {  // RESPCA_RING_CFG = 5, 10 or 16 (tuning)
+        if (const char* e = std::getenv("RESPCA_RING_CFG")) {
+            const int r = std::atoi(e);
+            if (r == 5 || ((r == 10 || r == 16) && d % 2 == 0)) return r;
+        }
         // measured on B200 (fraction of the HBM copy bandwidth):
-        //  few groups (c = 1): a row per thread, 4-deep ring, 2-member batches (C5 0.755)
-        //  fp32 storage: two rows per thread, 128-thread CTAs, 4-deep (C3-f32 0.71, C4 0.79)
-        //  fp64 up to 256 MB: the same (C2 0.685)
-        //  fp64 larger: two rows per thread, 256-thread CTAs, 8-deep, 4-member batches (C3 0.923)
+        //  5: a row per thread, 4-deep ring, 2-member batches — few groups (C5 0.755)
+        //  10: two rows per thread, 128-thread CTAs, 4-deep — fp32 storage (C3-f32
+        //      0.71, C4 0.79) and fp64 up to 256 MB (C2 0.685)
+        //  16: two rows per thread, 256-thread CTAs, 8-deep, 4-member batches —
+        //      fp64 larger (C3 0.926)
         if (d % 2 != 0 || c * ceil_div(d, 512) < 2 * 148) return 5;
         if (sizeof(T) == 4 || (double)d * (double)n * sizeof(T) <= 256e6) return 10;
         return 16;
     }
     int ring_nt() const {  // rows per CTA of the ring variant
         const int r = ring_cfg();
-        return (r == 12 || r == 16) ? 512 : (r == 10 || r == 11 || r == 13 || r == 14 || r == 17) ? 256
-               : (r == 8 || r == 9 || r == 15) ? 128 : (r == 3 || r == 4) ? 128 : 64;
+        return r == 16 ? 512 : r == 10 ? 256 : 64;
     }
     int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
         const char* e = std::getenv("RESPCA_PASSF_RING");
@@ -377,25 +379,12 @@ struct Alm : AlmBase {
                 kf<<<rbr * c, nt, sm, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p, G.p, G1, G.p, G1, Cw.p,
                                             mean_w.p, ctl.p, partials.p, d, rbr, lb_on ? Lb.p : nullptr, dpad);
             };
+            // the three configurations ring_cfg() chooses from (RESPCA_RING_CFG: the
+            // tuning sweep's numbering, kept for reproducibility)
             switch (ring_cfg()) {
-                case 1: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
-                case 2: go(k_pass_f_ring<T, 16, 64, 4>, 64, 16); break;
-                case 3: go(k_pass_f_ring<T, 8, 128, 4>, 128, 8); break;
-                case 4: go(k_pass_f_ring<T, 16, 128, 4>, 128, 16); break;
-                case 5: go(k_pass_f_ring<T, 4, 64, 2>, 64, 4); break;
-                case 6: go(k_pass_f_ring<T, 8, 64, 2>, 64, 8); break;
-                case 7: go(k_pass_f_ring<T, 4, 64, 1>, 64, 4); break;
-                case 8: go(k_pass_f_ring<T, 4, 64, 2, 2>, 64, 4, 2); break;
-                case 9: go(k_pass_f_ring<T, 8, 64, 2, 2>, 64, 8, 2); break;
                 case 10: go(k_pass_f_ring<T, 4, 128, 2, 2>, 128, 4, 2); break;
-                case 11: go(k_pass_f_ring<T, 8, 128, 2, 2>, 128, 8, 2); break;
-                case 12: go(k_pass_f_ring<T, 4, 256, 2, 2>, 256, 4, 2); break;
-                case 13: go(k_pass_f_ring<T, 6, 128, 2, 2>, 128, 6, 2); break;
-                case 14: go(k_pass_f_ring<T, 8, 128, 4, 2>, 128, 8, 2); break;
-                case 15: go(k_pass_f_ring<T, 8, 64, 4, 2>, 64, 8, 2); break;
                 case 16: go(k_pass_f_ring<T, 8, 256, 4, 2>, 256, 8, 2); break;
-                case 17: go(k_pass_f_ring<T, 12, 128, 4, 2>, 128, 12, 2); break;
-                default: go(k_pass_f_ring<T, 8, 64, 4>, 64, 8); break;
+                default: go(k_pass_f_ring<T, 4, 64, 2>, 64, 4); break;
             }
             ln.add();
             return;
