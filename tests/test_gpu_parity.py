@@ -65,14 +65,16 @@ def test_solve_against_oracle_random(ctx, orc):
         assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
 
 
-def test_fp32_mode_tolerance(ctx, orc):
+@pytest.mark.parametrize("d,n,c", [(200, 300, 10), (201, 300, 10), (151, 120, 1)])
+def test_fp32_mode_tolerance(ctx, orc, d, n, c):
     """fp32 storage: ≤1e-4 relative Frobenius error of L and S against the
-    fp64 reference on the same (f32-rounded) input."""
+    fp64 reference on the same (f32-rounded) input (even d: Pass F with two rows
+    per thread; odd d and c = 1: one row per thread)."""
     from paper_1904_07497_b200 import synth
     from paper_1904_07497_b200.respca import SolverConfig
 
-    X = synth.rpca(200, 300, 10, 1.0 / np.sqrt(10), 0.1, seed=11).astype(np.float32)
-    cfg = SolverConfig(c=10, tol=1e-5)
+    X = synth.rpca(d, n, 10, 1.0 / np.sqrt(10), 0.1, seed=11).astype(np.float32)
+    cfg = SolverConfig(c=c, tol=1e-5)
     a = _solve(ctx, X, cfg, precision="f32")
     b = orc.solve(X.astype(np.float64), cfg)
     assert rel_fro(a.L, b.L) <= 1e-4
