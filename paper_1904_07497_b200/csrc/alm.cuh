@@ -700,6 +700,9 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
     if (threadIdx.x == 0) {
         Ctl& k = *ctl;
         const int t = k.iter;
+        // fast-path verdict of Pass A (k_decide's counts): a label change or a
+        // Hartigan move sends this iteration to the exact slow path
+        if (k.changed || k.moves) k.slow = 1;
         const double feas = sqrt(v[0]) / k.xnorm;  // solver.cpp:20, 30
         const double dl = sqrt(v[1]) / k.xnorm;
         const double ds = sqrt(v[2]) / k.xnorm;

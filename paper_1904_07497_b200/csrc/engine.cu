@@ -411,9 +411,7 @@ struct Alm : AlmBase {
         if (lb_on) km.screen_tma(Lb.p, dpad, Cw.p);         // tcgen05, operands by TMA from Pass F's BF16 L′
         else if (use_tc && !tc_useless && km.tc_ok()) km.screen_tc(Cw.p);  // tcgen05, fp64 → bf16 producers
         else km.screen(Cw.p);                               // FP64 DMMA screen
-        km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);
-        k_fast_verdict<<<1, 1, 0, st>>>(ctl.p);
-        ln.add();
+        km.decide(Cw.p, labels.p, km.counts.p, 1, labels_new.p, ctl.p);  // verdict: k_finalize
     }
     // ℓ2,1 second half: ‖B_j‖, S'/Θ'/G_{t+1}, the ℓ2,1 report term
     void launch_post() {
@@ -435,7 +433,7 @@ struct Alm : AlmBase {
                                        cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
         ln.add();
     }
-    int kernels_per_iter() const { return 1 + (c > 1 ? 6 : 0) + 1 + (l21 ? 3 : 0); }
+    int kernels_per_iter() const { return 1 + (c > 1 ? 5 : 0) + 1 + (l21 ? 3 : 0); }
 
     // the captured graphs bake in pointers and shapes: re-capture only when
     // one of them (or any device allocation) changed since the last capture

@@ -369,15 +369,29 @@ struct Screen {
     const double* cc;
     int nsplit, n, c;
     double kappa_d;
+    // split partials in split order; loads four at a time (the padding zeros
+    // leave the sums unchanged: they never start from −0)
     RESPCA_DEV double xx(int j) const {
         double s = 0.0;
-        for (int p = 0; p < nsplit; ++p) s += xxp[(int64_t)p * n + j];
+        for (int p0 = 0; p0 < nsplit; p0 += 4) {
+            double a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = p0 + u < nsplit ? xxp[(int64_t)(p0 + u) * n + j] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) s += a[u];
+        }
         return s;
     }
     RESPCA_DEV void get(int j, int k, double xxj, double nx, double& lo, double& hi,
                         double& mid) const {
         double dot = 0.0;
-        for (int p = 0; p < nsplit; ++p) dot += part[((int64_t)p * n + j) * c + k];
+        for (int p0 = 0; p0 < nsplit; p0 += 4) {
+            double a[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) a[u] = p0 + u < nsplit ? part[((int64_t)(p0 + u) * n + j) * c + k] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) dot += a[u];
+        }
         const double ck = cc[k];
         mid = (xxj + ck) - 2.0 * dot;
         const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid);
@@ -494,7 +508,7 @@ RESPCA_DEV int decide_column(int j, int c, int old_label, const int* __restrict_
 // Same decision with each lane's intervals (k = lane + 32q, q < KPL) computed
 // once into registers; the candidate's interval is broadcast by shuffle.
 template <int KPL>
-RESPCA_DEV int decide_column_cached(int c, int old_label, const int* __restrict__ counts,
+RESPCA_DEV int decide_column_cached(int c, int old_label, const int (&cq)[KPL],
                                     bool hart, const double (&lo)[KPL], const double (&hi)[KPL],
                                     const double (&mid)[KPL], int& new_label) {
     const int lane = threadIdx.x & 31;
@@ -540,7 +554,15 @@ RESPCA_DEV int decide_column_cached(int c, int old_label, const int* __restrict_
     if (bk != old_label) return ST_CHANGED;
     if (!hart) return ST_STABLE;
     const int from = bk;
-    const int cf = counts[from];
+    int cf = 0;  // counts[from], from the lane that holds it
+    {
+        const int q = from >> 5;
+        int t = 0;
+#pragma unroll
+        for (int qq = 0; qq < KPL; ++qq)
+            if (qq == q) t = cq[qq];
+        cf = __shfl_sync(0xffffffffu, t, from & 31);
+    }
     if (cf <= 1) return ST_STABLE;  // kmeans.cpp:105
     const double na = (double)cf;
     const double wa = na / (na - 1.0);
@@ -550,7 +572,7 @@ RESPCA_DEV int decide_column_cached(int c, int old_label, const int* __restrict_
     for (int q = 0; q < KPL; ++q) {
         const int k = lane + 32 * q;
         if (k >= c || k == from) continue;
-        const double nb = (double)counts[k];
+        const double nb = (double)cq[q];
         const double wb = nb / (nb + 1.0);
         surely_none &= !(wb * lo[q] - gain_hi < -1e-12);
         surely_move |= (wb * hi[q] - gain_lo) < -1e-12;
@@ -566,7 +588,7 @@ RESPCA_DEV int decide_column_cached(int c, int old_label, const int* __restrict_
 // 1 = ALM fast-path check (assignment + first Hartigan pass).
 // Output labels are written to new_labels; ambiguous columns are appended to
 // amb_list and keep their old label for now.
-__global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
+__global__ void __launch_bounds__(256, 4) k_decide(Screen sc, int n, int c,
                                                 const int* __restrict__ old_labels,
                                                 const int* __restrict__ counts, int mode,
                                                 int* __restrict__ new_labels,
@@ -574,13 +596,22 @@ __global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
                                                 int diag) {
     const int lane = threadIdx.x & 31;
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (j >= n || ctl->done) return;
+    if (j >= n) return;
+    // every load of the column is issued before the first use (the done flag,
+    // labels and group sizes included): one memory latency round per warp
+    const int done = *(volatile const int*)&ctl->done;
+    const int old = old_labels ? old_labels[j] : -1;
+    int cq[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int k = lane + 32 * q;
+        cq[q] = (counts && k < c) ? __ldg(counts + k) : 0;
+    }
     const double xxj = sc.xx(j);
     const double nx = sqrt(fabs(xxj));
     auto fn = [&](int jj, int k, double& lo, double& hi, double& mid) {
         sc.get(jj, k, xxj, nx, lo, hi, mid);
     };
-    const int old = old_labels ? old_labels[j] : -1;
     int nl = old;
     int st;
     if (c <= 128) {  // intervals computed once per lane (KPL = 4)
@@ -591,8 +622,10 @@ __global__ void __launch_bounds__(256) k_decide(Screen sc, int n, int c,
             if (k < c) fn(j, k, lo[q], hi[q], mid[q]);
             else lo[q] = hi[q] = mid[q] = INFINITY;
         }
-        st = decide_column_cached<4>(c, old, counts, mode == 1, lo, hi, mid, nl);
+        if (done) return;
+        st = decide_column_cached<4>(c, old, cq, mode == 1, lo, hi, mid, nl);
     } else {
+        if (done) return;
         st = decide_column(j, c, old, counts, mode == 1, fn, nl);
     }
     if (diag && mode == 1 && old >= 0 && counts[old] > 1) {
@@ -755,12 +788,6 @@ __global__ void __launch_bounds__(256) k_redecide(const double* __restrict__ exa
             if (st == ST_MOVE) atomicAdd(&ctl->moves, 1u);
         }
     }
-}
-
-// Fast-path verdict: any label change or Hartigan move → slow path.
-__global__ void k_fast_verdict(Ctl* __restrict__ ctl) {
-    if (ctl->done) return;
-    if (ctl->changed || ctl->moves) ctl->slow = 1;
 }
 
 // ---------------------------------------------------------------------------

@@ -287,8 +287,7 @@ struct KMeansEngine {
     void screen_tma(const __nv_bfloat16* Lbp, int64_t dpad, const double* C) {
         tcCb.ensure((size_t)TC_N * dpad);
         tcerr.ensure(1);
-        CK(cudaMemsetAsync(tcerr.p, 0, sizeof(int), st));
-        k_tc_prep_centroids<<<TC_N, 1024, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p);
+        k_tc_prep_centroids<<<TC_N, 1024, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p, tcerr.p);
         if (tma_key_a != (const void*)Lbp || tma_key_n != n || tma_key_dpad != dpad) {
             mapA = make_map(Lbp, (uint64_t)dpad, (uint64_t)n, TC_M);
             mapB = make_map(tcCb.p, (uint64_t)dpad, (uint64_t)TC_N, TC_N);

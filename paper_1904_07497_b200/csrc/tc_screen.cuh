@@ -102,9 +102,10 @@ RESPCA_DEV uint32_t sw128(int row, int chunk) {
 // centroids → BF16 K-major [TC_N][d_pad] (rows ≥ c zero) and ‖c_k‖² (FP64 FMA)
 __global__ void __launch_bounds__(1024) k_tc_prep_centroids(const double* __restrict__ C, int64_t d, int c,
                                                              int64_t d_pad, __nv_bfloat16* __restrict__ Cb,
-                                                             double* __restrict__ cc) {
+                                                             double* __restrict__ cc, int* __restrict__ err = nullptr) {
     __shared__ double red[32];
     const int k = blockIdx.x;  // 0..TC_N-1
+    if (err && k == 0 && threadIdx.x == 0) *err = 0;  // the screen's error flag, reset before it runs
     double s = 0.0;
     // 1024 threads, 4 loads in flight each: one latency round per 4096 rows
     for (int64_t i0 = threadIdx.x; i0 < d_pad; i0 += 4 * (int64_t)blockDim.x) {
