@@ -369,6 +369,7 @@ struct Screen {
     const double* cc;
     int nsplit, n, c;
     double kappa_d;
+    double abs_e = 0.0;  // absolute half-width term (TMA screen: FP32 underflow of ‖x‖² chunk sums)
     // split partials in split order; loads four at a time (the padding zeros
     // leave the sums unchanged: they never start from −0)
     RESPCA_DEV double xx(int j) const {
@@ -394,7 +395,7 @@ struct Screen {
         }
         const double ck = cc[k];
         mid = (xxj + ck) - 2.0 * dot;
-        const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid);
+        const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid) + abs_e;
         if (!isfinite(mid) || !isfinite(e)) {
             lo = -INFINITY;
             hi = INFINITY;

@@ -322,6 +322,7 @@ struct KMeansEngine {
         s.c = c;
         s.kappa_d = tc_mode ? tc_bf16_kappa((double)d) + kappa_screen() : kappa_screen();
         if (tma_mode) s.kappa_d = (s.kappa_d + tma_xx_kappa((double)d)) * 1.01;  // ‖x‖² from BF16 values
+        if (tma_mode) s.abs_e = tma_xx_abs((double)d) * 1.01;
         return s;
     }
 

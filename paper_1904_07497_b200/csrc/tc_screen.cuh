@@ -338,8 +338,13 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_screen_tc(
 constexpr int TM_THREADS = 6 * 32;
 
 __host__ __device__ inline double tma_xx_kappa(double d) {
-    return 0.00390625 + 7.62939453125e-06 + d * 1.2212453270876722e-16;
+    // bf16 rounding of x (2⁻⁸ + 2⁻¹⁷), FP32 stage sums of 64 squares
+    // (64·2⁻²⁴), the FP64 accumulation (d·1.1u)
+    return 0.00390625 + 7.62939453125e-06 + 3.814697265625e-06 + d * 1.2212453270876722e-16;
 }
+// squares below FP32's normal range lose bits in the stage sums: absolute
+// error ≤ 2⁻¹⁴⁹ per element (added to the screen's interval half-width)
+__host__ __device__ inline double tma_xx_abs(double d) { return d * 1.401298464324817e-45; }
 
 RESPCA_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
     asm volatile(
@@ -368,6 +373,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
     int64_t kb1 = kb0 + kblocks_per_split;
     if (kb1 > total_kb) kb1 = total_kb;
     const int nkb = kb1 > kb0 ? (int)(kb1 - kb0) : 0;
+    const int rot = nkb ? (int)(((int64_t)blockIdx.x * 5) % nkb) : 0;  // this tile's first K block (the sums are order-free: bounds cover any order)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < TC_STAGES; ++s) {
@@ -403,7 +409,10 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
                 }
                 const uint32_t a = smem_u32(stage_base + (size_t)s * TC_STAGE_BYTES);
                 mbar_expect_tx_cta(&full_bar[s], TC_A_BYTES + TC_B_BYTES);
-                const int kx = (int)((kb0 + it) * TC_KB);
+                // K blocks in a rotated order, different per column tile: the
+                // tiles of a split would otherwise all read the same centroid
+                // (B) block at the same time — one L2 hot spot serving 79 CTAs
+                const int kx = (int)((kb0 + (it + rot) % nkb) * TC_KB);
                 tma_load_2d(a, &mapA, kx, j0, &full_bar[s]);
                 tma_load_2d(a + TC_A_BYTES, &mapB, kx, 0, &full_bar[s]);
             }
@@ -452,20 +461,27 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
                 break;
             }
             const unsigned char* A = stage_base + (size_t)s * TC_STAGE_BYTES;
+            // the 64 squares of a stage summed in FP32 (a bf16 square is exact
+            // in FP32; 63 roundings ≤ 64·2⁻²⁴ relative, in tma_xx_kappa), then
+            // one conversion: F2F.F64.F32 per element throttled these warps
+            uint4 q[8];
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) q[ch] = *reinterpret_cast<const uint4*>(A + sw128(row, ch));
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty_bar[s]);  // the stage is in registers: release it
+            float f0 = 0.0f, f1 = 0.0f;  // two FP32 chains of 32 squares
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {
-                const uint4 q = *reinterpret_cast<const uint4*>(A + sw128(row, ch));
-                const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+                const uint32_t w[4] = {q[ch].x, q[ch].y, q[ch].z, q[ch].w};
 #pragma unroll
                 for (int h = 0; h < 4; ++h) {
-                    const double lo = (double)__uint_as_float(w[h] << 16);
-                    const double hi = (double)__uint_as_float(w[h] & 0xffff0000u);
-                    xx = __fma_rn(lo, lo, xx);
-                    xx = __fma_rn(hi, hi, xx);
+                    const float lo = __uint_as_float(w[h] << 16);
+                    const float hi = __uint_as_float(w[h] & 0xffff0000u);
+                    f0 = __fmaf_rn(lo, lo, f0);
+                    f1 = __fmaf_rn(hi, hi, f1);
                 }
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty_bar[s]);
+            xx += (double)f0 + (double)f1;
         }
     }
     __syncthreads();  // every stage issued
