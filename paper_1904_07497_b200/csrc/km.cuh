@@ -393,7 +393,10 @@ struct Screen {
 #pragma unroll
             for (int u = 0; u < 4; ++u) dot += a[u];
         }
-        const double ck = cc[k];
+        interval(xxj, nx, dot, cc[k], lo, hi, mid);
+    }
+    RESPCA_DEV void interval(double xxj, double nx, double dot, double ck, double& lo, double& hi,
+                             double& mid) const {
         mid = (xxj + ck) - 2.0 * dot;
         const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid) + abs_e;
         if (!isfinite(mid) || !isfinite(e)) {
@@ -652,6 +655,66 @@ __global__ void __launch_bounds__(256, 4) k_decide(Screen sc, int n, int c,
                 if (mrel < 0.1 / (double)(q == 0 ? 1 : (q == 1 ? 10 : (q == 2 ? 100 : (q == 3 ? 1000 : (q == 4 ? 10000 : 100000))))))
                     atomicAdd(&ctl->margin_hist[q], 1u);
     }
+    if (lane == 0) {
+        new_labels[j] = st == ST_AMBIG ? old : nl;
+        if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);
+        if (st == ST_MOVE) atomicAdd(&ctl->moves, 1u);
+        if (st == ST_AMBIG) {
+            const unsigned slot = atomicAdd(&ctl->ambiguous, 1u);
+            amb_list[slot] = j;
+        }
+    }
+}
+
+// k_decide for c ≤ 32·KPL centroids and ≤ 4 screen splits: every load of the
+// column (split partials, ‖x‖² partials, ‖c‖², labels, group sizes, the done
+// flag) is issued in one basic block — one memory latency round per warp —
+// and the intervals are Screen::get's arithmetic, term for term.
+template <int KPL>
+__global__ void __launch_bounds__(256, KPL == 2 ? 4 : 3) k_decide_fast(Screen sc, int n, int c,
+                                                        const int* __restrict__ old_labels,
+                                                        const int* __restrict__ counts, int mode,
+                                                        int* __restrict__ new_labels,
+                                                        int* __restrict__ amb_list, Ctl* __restrict__ ctl) {
+    const int lane = threadIdx.x & 31;
+    const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (j >= n) return;
+    const int ns = sc.nsplit;
+    const int done = *(volatile const int*)&ctl->done;
+    const int old = old_labels ? old_labels[j] : -1;
+    double xp[4], pa[KPL][4], ccq[KPL];
+    int cq[KPL];
+#pragma unroll
+    for (int p = 0; p < 4; ++p) xp[p] = p < ns ? __ldg(sc.xxp + (int64_t)p * n + j) : 0.0;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
+        const bool kk = k < c;
+        cq[q] = (counts && kk) ? __ldg(counts + k) : 0;
+        ccq[q] = kk ? __ldg(sc.cc + k) : 0.0;
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+            pa[q][p] = (kk && p < ns) ? __ldg(sc.part + ((int64_t)p * n + j) * c + k) : 0.0;
+    }
+    double xxj = 0.0;  // Screen::xx: splits in order (trailing zeros leave the sum unchanged)
+#pragma unroll
+    for (int p = 0; p < 4; ++p) xxj += xp[p];
+    const double nx = sqrt(fabs(xxj));
+    double lo[KPL], hi[KPL], mid[KPL];
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        if (lane + 32 * q < c) {
+            double dot = 0.0;
+#pragma unroll
+            for (int p = 0; p < 4; ++p) dot += pa[q][p];
+            sc.interval(xxj, nx, dot, ccq[q], lo[q], hi[q], mid[q]);
+        } else {
+            lo[q] = hi[q] = mid[q] = INFINITY;
+        }
+    }
+    if (done) return;
+    int nl = old;
+    const int st = decide_column_cached<KPL>(c, old, cq, mode == 1, lo, hi, mid, nl);
     if (lane == 0) {
         new_labels[j] = st == ST_AMBIG ? old : nl;
         if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);

@@ -333,11 +333,21 @@ struct KMeansEngine {
         return c <= 16 && d >= 4096;
     }
     // decide (+ exact fallback for ambiguous columns); returns #ambiguous
+    static bool decide_fast_env() {  // RESPCA_DECIDE_FAST=0: the general k_decide everywhere
+        static const bool v = env_int("RESPCA_DECIDE_FAST", 1) != 0;
+        return v;
+    }
     void decide(const double* C, const int* old_labels, const int* cnts, int mode, int* out_labels,
                 Ctl* ctl) {
-        k_decide<<<ceil_div((int64_t)n * 32, 256), 256, 0, st>>>(screen_view(), n, c, old_labels,
-                                                                 cnts, mode, out_labels, amb.p,
-                                                                 ctl, trace_on() ? 1 : 0);
+        const Screen sv = screen_view();
+        const unsigned nb = (unsigned)ceil_div((int64_t)n * 32, 256);
+        if (!trace_on() && sv.nsplit <= 4 && c <= 64 && decide_fast_env())
+            k_decide_fast<2><<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl);
+        else if (!trace_on() && sv.nsplit <= 4 && c <= 128 && decide_fast_env())
+            k_decide_fast<4><<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl);
+        else
+            k_decide<<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl,
+                                         trace_on() ? 1 : 0);
         if (exact_tiled()) {
             // the list length is known only on the device: a grid for all n
             // columns, warps past the count return at once
