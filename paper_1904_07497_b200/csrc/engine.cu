@@ -433,7 +433,7 @@ struct Alm : AlmBase {
                                        cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
         ln.add();
     }
-    int kernels_per_iter() const { return 1 + (c > 1 ? 5 : 0) + 1 + (l21 ? 3 : 0); }
+    int kernels_per_iter() const { return 1 + (c > 1 ? 2 + km.decide_kernels() : 0) + 1 + (l21 ? 3 : 0); }
 
     // the captured graphs bake in pointers and shapes: re-capture only when
     // one of them (or any device allocation) changed since the last capture

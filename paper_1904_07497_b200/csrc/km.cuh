@@ -854,6 +854,52 @@ __global__ void __launch_bounds__(256) k_redecide(const double* __restrict__ exa
     }
 }
 
+// k_exact_cols and k_redecide in one launch (short lists: one block per listed
+// column computes its exact chains, then its first warp re-decides it).  With
+// nothing ambiguous — the common iteration — this is one empty launch, not two.
+template <typename T>
+__global__ void __launch_bounds__(128) k_exact_redecide(const T* __restrict__ M, const double* __restrict__ C,
+                                                        int64_t d, int c, const int* __restrict__ list,
+                                                        const unsigned* __restrict__ count,
+                                                        double* __restrict__ exact,
+                                                        const int* __restrict__ old_labels,
+                                                        const int* __restrict__ counts, int mode,
+                                                        int* __restrict__ new_labels, Ctl* __restrict__ ctl) {
+    if (ctl->done) return;
+    const unsigned cnt = *count;
+    if (blockIdx.x == 0 && threadIdx.x == 0) ctl->exact_fallbacks += cnt;
+    const int lane = threadIdx.x & 31;
+    for (unsigned idx = blockIdx.x; idx < cnt; idx += gridDim.x) {
+        const int j = list[idx];
+        const T* x = M + (int64_t)j * d;
+        for (int k = threadIdx.x; k < c; k += blockDim.x) {  // k_exact_cols' chains
+            const double* cv = C + (int64_t)k * d;
+            double s = 0.0;
+            for (int64_t i = 0; i < d; ++i) {
+                const double t = (double)__ldg(x + i) - __ldg(cv + i);
+                s += t * t;
+            }
+            exact[(int64_t)idx * c + k] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x < 32) {  // k_redecide's decision
+            auto fn = [&](int, int k, double& lo, double& hi, double& mid) {
+                mid = exact[(int64_t)idx * c + k];
+                lo = hi = mid;
+            };
+            const int old = old_labels ? old_labels[j] : -1;
+            int nl = old;
+            const int st = decide_column(j, c, old, counts, mode == 1, fn, nl);
+            if (lane == 0) {
+                new_labels[j] = nl;
+                if (st == ST_CHANGED) atomicAdd(&ctl->changed, 1u);
+                if (st == ST_MOVE) atomicAdd(&ctl->moves, 1u);
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // k-means++ distance update (kmeans.cpp:188-191):
 //   d2[j] = std::min(d2[j], sq_dist(col_j, col_last))

@@ -333,6 +333,7 @@ struct KMeansEngine {
         return c <= 16 && d >= 4096;
     }
     // decide (+ exact fallback for ambiguous columns); returns #ambiguous
+    int decide_kernels() const { return exact_tiled() ? 3 : 2; }  // launches of decide()
     static bool decide_fast_env() {  // RESPCA_DECIDE_FAST=0: the general k_decide everywhere
         static const bool v = env_int("RESPCA_DECIDE_FAST", 1) != 0;
         return v;
@@ -356,12 +357,14 @@ struct KMeansEngine {
             smem_at_least((const void*)k_exact_cols_tile<T, KC>, sm);
             k_exact_cols_tile<T, KC><<<dim3(ceil_div(n, 64), ceil_div(c, KC)), 64, sm, st>>>(
                 M, C, d, c, amb.p, &ctl->ambiguous, exact.p);
-        } else
-        k_exact_cols<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous,
-                                                             exact.p);
-        k_redecide<<<std::min(ceil_div((int64_t)n * 32, 256), 4 * 148), 256, 0, st>>>(
-            exact.p, c, amb.p, &ctl->ambiguous, old_labels, cnts, mode, out_labels, ctl);
-        ln.add(3);
+            k_redecide<<<std::min(ceil_div((int64_t)n * 32, 256), 4 * 148), 256, 0, st>>>(
+                exact.p, c, amb.p, &ctl->ambiguous, old_labels, cnts, mode, out_labels, ctl);
+            ln.add(3);
+        } else {
+            k_exact_redecide<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous, exact.p,
+                                                                      old_labels, cnts, mode, out_labels, ctl);
+            ln.add(2);
+        }
     }
 
     // assign_nearest (kmeans.cpp:21-37) → labels (device)
