@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     __shared__ double red[32 * 5];
     extern __shared__ __align__(16) unsigned char pfr_sm[];
     auto ring = reinterpret_cast<T(*)[4][NT * RW]>(pfr_sm);  // [stage][X, S, Θ, L][row]
+    pdl_enter();
     if (ctl->done) return;
     const int g = blockIdx.x / rowblocks;
     const int rb = blockIdx.x - g * rowblocks;
@@ -687,6 +688,7 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
                                                    double* __restrict__ rep, int has_cond,
                                                    cudaGraphConditionalHandle cond) {
     __shared__ double red[32 * 5];
+    pdl_enter();
     if (ctl->done) {
         if (threadIdx.x == 0 && has_cond) cudaGraphSetConditional(cond, 0u);
         return;

@@ -12,6 +12,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #define RESPCA_DEV __device__ __forceinline__
 
 namespace respca_dev {
@@ -76,4 +79,41 @@ RESPCA_DEV double ld(const T* p) {
     return (double)__ldg(p);
 }
 
+// Programmatic dependent launch (PDL).  Kernels launched through pdl_launch
+// start with pdl_enter(): griddepcontrol.wait blocks until the previous
+// kernel on the stream has COMPLETED and its writes are visible (so every
+// read below it sees exactly what a plain launch would), then the kernel
+// allows its own dependent to be scheduled.  The gain is only the launch and
+// CTA rasterisation latency at each kernel boundary, hidden under the
+// predecessor's tail.  Without the launch attribute both instructions are
+// no-ops.  RESPCA_PDL=0 launches plainly.
+RESPCA_DEV void pdl_enter() {
+    asm volatile("griddepcontrol.wait;\n\tgriddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace respca_dev
+
+namespace respca_host {
+inline bool pdl_on() {
+    static const bool v = [] {
+        const char* e = std::getenv("RESPCA_PDL");
+        return e ? std::atoi(e) != 0 : true;
+    }();
+    return v;
+}
+template <class... P, class... A>
+inline cudaError_t pdl_launch(void (*kf)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              A&&... args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl_on() ? 1 : 0;
+    return cudaLaunchKernelEx(&lc, kf, std::forward<A>(args)...);
+}
+}  // namespace respca_host

@@ -429,8 +429,8 @@ struct Alm : AlmBase {
         ln.add(3);
     }
     void launch_finalize(bool cond) {
-        k_finalize<<<1, 1024, 0, st>>>(ctl.p, partials.p, l21 ? nbF : nbP, km.goff.p, mean_w.p, c, rep.p,
-                                       cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{});
+        CK(pdl_launch(k_finalize, dim3(1), dim3(1024), 0, st, ctl.p, partials.p, l21 ? nbF : nbP, km.goff.p,
+                      mean_w.p, c, rep.p, cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{}));
         ln.add();
     }
     int kernels_per_iter() const { return 1 + (c > 1 ? 2 + km.decide_kernels() : 0) + 1 + (l21 ? 3 : 0); }

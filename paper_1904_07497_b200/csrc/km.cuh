@@ -677,6 +677,7 @@ __global__ void __launch_bounds__(256, KPL == 2 ? 4 : 3) k_decide_fast(Screen sc
                                                         int* __restrict__ new_labels,
                                                         int* __restrict__ amb_list, Ctl* __restrict__ ctl) {
     const int lane = threadIdx.x & 31;
+    pdl_enter();
     const int j = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (j >= n) return;
     const int ns = sc.nsplit;
@@ -865,6 +866,7 @@ __global__ void __launch_bounds__(128) k_exact_redecide(const T* __restrict__ M,
                                                         const int* __restrict__ old_labels,
                                                         const int* __restrict__ counts, int mode,
                                                         int* __restrict__ new_labels, Ctl* __restrict__ ctl) {
+    pdl_enter();
     if (ctl->done) return;
     const unsigned cnt = *count;
     if (blockIdx.x == 0 && threadIdx.x == 0) ctl->exact_fallbacks += cnt;

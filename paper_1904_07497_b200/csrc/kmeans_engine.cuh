@@ -287,7 +287,7 @@ struct KMeansEngine {
     void screen_tma(const __nv_bfloat16* Lbp, int64_t dpad, const double* C) {
         tcCb.ensure((size_t)TC_N * dpad);
         tcerr.ensure(1);
-        k_tc_prep_centroids<<<TC_N, 1024, 0, st>>>(C, d, c, dpad, tcCb.p, cc.p, tcerr.p);
+        CK(pdl_launch(k_tc_prep_centroids, dim3(TC_N), dim3(1024), 0, st, C, d, c, dpad, tcCb.p, cc.p, tcerr.p));
         if (tma_key_a != (const void*)Lbp || tma_key_n != n || tma_key_dpad != dpad) {
             mapA = make_map(Lbp, (uint64_t)dpad, (uint64_t)n, TC_M);
             mapB = make_map(tcCb.p, (uint64_t)dpad, (uint64_t)TC_N, TC_N);
@@ -304,8 +304,8 @@ struct KMeansEngine {
         part.ensure((size_t)ns * n * c);
         xxp.ensure((size_t)ns * n);
         smem_at_least((const void*)k_screen_tma, (size_t)(TC_SMEM));
-        k_screen_tma<<<dim3(tiles, ns), TM_THREADS, TC_SMEM, st>>>(mapA, mapB, d, n, c, kbps, part.p, xxp.p,
-                                                                   tcerr.p);
+        CK(pdl_launch(k_screen_tma, dim3(tiles, ns), dim3(TM_THREADS), TC_SMEM, st, mapA, mapB, d, n, c, kbps,
+                      part.p, xxp.p, tcerr.p));
         ln.add(2);
         scr_n = n;
         scr_split = ns;
@@ -343,9 +343,11 @@ struct KMeansEngine {
         const Screen sv = screen_view();
         const unsigned nb = (unsigned)ceil_div((int64_t)n * 32, 256);
         if (!trace_on() && sv.nsplit <= 4 && c <= 64 && decide_fast_env())
-            k_decide_fast<2><<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl);
+            CK(pdl_launch(k_decide_fast<2>, dim3(nb), dim3(256), 0, st, sv, n, c, old_labels, cnts, mode,
+                          out_labels, amb.p, ctl));
         else if (!trace_on() && sv.nsplit <= 4 && c <= 128 && decide_fast_env())
-            k_decide_fast<4><<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl);
+            CK(pdl_launch(k_decide_fast<4>, dim3(nb), dim3(256), 0, st, sv, n, c, old_labels, cnts, mode,
+                          out_labels, amb.p, ctl));
         else
             k_decide<<<nb, 256, 0, st>>>(sv, n, c, old_labels, cnts, mode, out_labels, amb.p, ctl,
                                          trace_on() ? 1 : 0);
@@ -361,8 +363,8 @@ struct KMeansEngine {
                 exact.p, c, amb.p, &ctl->ambiguous, old_labels, cnts, mode, out_labels, ctl);
             ln.add(3);
         } else {
-            k_exact_redecide<T><<<std::min(n, 4 * 148), 128, 0, st>>>(M, C, d, c, amb.p, &ctl->ambiguous, exact.p,
-                                                                      old_labels, cnts, mode, out_labels, ctl);
+            CK(pdl_launch(k_exact_redecide<T>, dim3(std::min(n, 4 * 148)), dim3(128), 0, st, M, C, d, c, amb.p,
+                          &ctl->ambiguous, exact.p, old_labels, cnts, mode, out_labels, ctl));
             ln.add(2);
         }
     }

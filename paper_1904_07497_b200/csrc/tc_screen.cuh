@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(1024) k_tc_prep_centroids(const double* __rest
                                                              int64_t d_pad, __nv_bfloat16* __restrict__ Cb,
                                                              double* __restrict__ cc, int* __restrict__ err = nullptr) {
     __shared__ double red[32];
+    pdl_enter();
     const int k = blockIdx.x;  // 0..TC_N-1
     if (err && k == 0 && threadIdx.x == 0) *err = 0;  // the screen's error flag, reset before it runs
     double s = 0.0;
@@ -358,6 +359,7 @@ __global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
     const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t d,
     int n, int c, int kblocks_per_split, double* __restrict__ part, double* __restrict__ xxp,
     int* __restrict__ err) {
+    pdl_enter();
     extern __shared__ __align__(1024) unsigned char tsm_raw[];
     unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
     unsigned char* stage_base = tsm;
