@@ -94,12 +94,9 @@ RESPCA_DEV void pdl_enter() {
 }  // namespace respca_dev
 
 namespace respca_host {
-inline bool pdl_on() {
-    static const bool v = [] {
-        const char* e = std::getenv("RESPCA_PDL");
-        return e ? std::atoi(e) != 0 : true;
-    }();
-    return v;
+inline bool pdl_on() {  // read per launch: the captured graph's key includes it
+    const char* e = std::getenv("RESPCA_PDL");
+    return e ? std::atoi(e) != 0 : true;
 }
 template <class... P, class... A>
 inline cudaError_t pdl_launch(void (*kf)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

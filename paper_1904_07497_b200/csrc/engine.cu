@@ -437,13 +437,14 @@ struct Alm : AlmBase {
 
     // the captured graphs bake in pointers and shapes: re-capture only when
     // one of them (or any device allocation) changed since the last capture
-    uint64_t cap_key[12] = {};
+    uint64_t cap_key[13] = {};
     bool cap_valid = false;
     void capture_if_needed() {
-        const uint64_t key[12] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
+        const uint64_t key[13] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
                                   (uint64_t)(use_tc && !tc_useless), (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
-                                  (uint64_t)passf_variant_env, (uint64_t)dpad, g_alloc_gen.load()};
-        if (cap_valid && std::equal(key, key + 12, cap_key)) return;
+                                  (uint64_t)passf_variant_env, (uint64_t)dpad, g_alloc_gen.load(),
+                                  (uint64_t)pdl_on()};
+        if (cap_valid && std::equal(key, key + 13, cap_key)) return;
         cap_valid = false;
         try {
             capture();
@@ -457,7 +458,7 @@ struct Alm : AlmBase {
             cudaGetLastError();
             throw;
         }
-        std::copy(key, key + 12, cap_key);
+        std::copy(key, key + 13, cap_key);
         cap_valid = true;
     }
     void capture() {

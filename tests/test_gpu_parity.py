@@ -155,3 +155,15 @@ def test_l21_solve_bitwise(ctx, orc, seed, d, n, c):
         assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
         np.testing.assert_allclose(a.report.objective, b.objective, rtol=1e-9)
         np.testing.assert_allclose(a.report.feas, b.feas, rtol=1e-10)
+
+
+@pytest.mark.parametrize("pdl", ["0", "1"])
+def test_c1_bitwise_launch_modes(ctx, monkeypatch, pdl):
+    """Programmatic dependent launch on (default) or off for the Pass A chain
+    and k_finalize: every dependent kernel waits for its predecessor before
+    its first read, so the bits are the reference's either way."""
+    monkeypatch.setenv("RESPCA_PDL", pdl)
+    for name in ("C1", "C2"):
+        case = load(f"solve_{name}.json")
+        res = _solve(ctx, make_x(case), cfg_from(case["config"]))
+        assert_matches_golden(res, case)
