@@ -76,6 +76,8 @@ typedef struct {
     uint64_t slow_iters;    /* iterations whose p-update changed labels or moved a point */
     uint64_t hartigan_moves;/* total exact Hartigan moves (initial clustering + loop) */
     uint64_t exact_fallbacks;/* distance decisions resolved by exact sequential chains */
+    uint64_t stop_resolves; /* ALM stop tests decided on the reference's own sequential
+                               residual chains (the tree-sum interval straddled tol) */
 } respca_cu_report;
 
 void respca_cu_default_config(respca_cu_config* cfg);

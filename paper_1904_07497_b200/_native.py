@@ -41,7 +41,7 @@ class CReport(C.Structure):
         ("iters", u64), ("converged", C.c_int), ("lambda_", C.c_double),
         ("wall_time", C.c_double), ("init_ms", C.c_double), ("loop_ms", C.c_double),
         ("h2d_ms", C.c_double), ("d2h_ms", C.c_double), ("slow_iters", u64),
-        ("hartigan_moves", u64), ("exact_fallbacks", u64),
+        ("hartigan_moves", u64), ("exact_fallbacks", u64), ("stop_resolves", u64),
     ]
 
 

@@ -722,7 +722,28 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
         double mx = feas;  // std::max({feas, dl, ds})
         if (mx < dl) mx = dl;
         if (mx < ds) mx = ds;
-        if (!k.fixed && mx <= k.tol) k.converged = 1;
+        if (!k.fixed && !k.nonfinite) {  // solver.cpp:197
+            if (!k.guard) {
+                if (mx <= k.tol) k.converged = 1;
+            } else if (k.force_exact) {
+                k.stop_amb = 1;
+            } else {
+                // the reference's sums lie in [v·(1−ε), v·(1+ε)] (rounded outwards);
+                // correctly rounded sqrt and / are monotone, so its residuals lie in
+                // [sqrt(lo)/xn_hi, sqrt(hi)/xn_lo]
+                const double om = __dadd_rd(1.0, -k.sum_eps), op = __dadd_ru(1.0, k.sum_eps);
+                double lo = 0.0, hi = 0.0;
+#pragma unroll
+                for (int q = 0; q < 3; ++q) {
+                    const double a = sqrt(__dmul_rd(v[q], om)) / k.xn_hi;
+                    const double b = sqrt(__dmul_ru(v[q], op)) / k.xn_lo;
+                    lo = lo < a ? a : lo;
+                    hi = hi < b ? b : hi;
+                }
+                if (hi <= k.tol) k.converged = 1;
+                else if (!(lo > k.tol)) k.stop_amb = 1;  // decided on the chains (host)
+            }
+        }
         k.iter = t + 1;
         // advance ρ and the derived scalars to iteration t+1
         const double rho = k.rho_next;
@@ -733,7 +754,7 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
         k.own_w = rho / (two_lam + rho);
         k.thr = 1.0 / rho;
         k.parity ^= 1;
-        const int done = k.converged || k.slow || k.nonfinite || (t + 1 >= k.budget);
+        const int done = k.converged || k.slow || k.nonfinite || k.stop_amb || (t + 1 >= k.budget);
         k.done = done;
         s_done = done;
         if (has_cond) cudaGraphSetConditional(cond, done ? 0u : 1u);
@@ -743,6 +764,67 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
     for (int g = threadIdx.x; g < c; g += blockDim.x)  // solver.cpp:66-67
         mean_w[g] = two_lam / ((double)(goff[g + 1] - goff[g]) * (two_lam + rho));
     (void)s_done;
+}
+
+// ---------------------------------------------------------------------------
+// The reference's residual sums as its own sequential chains, for a stop test
+// the intervals of k_finalize could not decide (rare: the chain and the tree
+// sum differ by ~1e-16 relative in practice, the rigorous bound is ~N·u):
+//   chain 0: Σ_k ((x_k − l_k) − s_k)²   feas_residual   solver.cpp:23-31
+//   chain 1: Σ_k (l_k − lp_k)²          rel_diff(L)      solver.cpp:14-21
+//   chain 2: Σ_k (s_k − sp_k)²          rel_diff(S)
+//   chain 3: Σ_k x_k²                   frob_norm(X)     matrix.cpp:99-103
+// k in storage order (DenseMatrix::data()).  One CTA per chain: the terms are
+// independent, so warps 1..7 stage the next tile's terms in shared memory while
+// thread 0 adds the current tile's in order (the dependent adds are the cost:
+// ≈N·4 cycles).  skip_x: chain 3 is not needed (‖X‖ already exact).
+// ---------------------------------------------------------------------------
+constexpr int CH_TILE = 2048;
+template <typename T>
+__global__ void __launch_bounds__(256) k_exact_chains(const T* __restrict__ X, const T* __restrict__ L,
+                                                      const T* __restrict__ Lp, const T* __restrict__ S,
+                                                      const T* __restrict__ Sp, int64_t N, int skip_x,
+                                                      double* __restrict__ out) {
+    __shared__ double buf[2][CH_TILE];
+    const int q = blockIdx.x;
+    if (q == 3 && skip_x) return;
+    auto term = [&](int64_t k) -> double {
+        if (q == 0) {
+            const double r = (ld(X + k) - ld(L + k)) - ld(S + k);
+            return r * r;
+        }
+        if (q == 1) {
+            const double r = ld(L + k) - ld(Lp + k);
+            return r * r;
+        }
+        if (q == 2) {
+            const double r = ld(S + k) - ld(Sp + k);
+            return r * r;
+        }
+        const double v = ld(X + k);
+        return v * v;
+    };
+    auto fill = [&](int64_t tile, double* b) {
+        const int64_t base = tile * CH_TILE;
+        for (int e = (int)threadIdx.x - 32; e < CH_TILE; e += (int)blockDim.x - 32)
+            b[e] = base + e < N ? term(base + e) : 0.0;
+    };
+    const int64_t ntiles = (N + CH_TILE - 1) / CH_TILE;
+    if (threadIdx.x >= 32) fill(0, buf[0]);
+    __syncthreads();
+    double acc = 0.0;
+    for (int64_t t = 0; t < ntiles; ++t) {
+        if (threadIdx.x == 0) {
+            const double* b = buf[t & 1];
+            const int cnt = (int)((N - t * CH_TILE) < CH_TILE ? (N - t * CH_TILE) : CH_TILE);
+#pragma unroll 16
+            for (int e = 0; e < cnt; ++e) acc += b[e];
+        } else if (threadIdx.x >= 32 && t + 1 < ntiles) {
+            fill(t + 1, buf[(t + 1) & 1]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) out[q] = acc;
 }
 
 // mean_w for the current ρ (after the host rebuilt the member lists).

@@ -45,6 +45,18 @@ struct Ctl {
     int l21;          // sparse_norm = L21: the sparse term comes from `sparse_term`
     double sparse_term;
     unsigned long long exact_fallbacks;
+    // ALM stop guard (solver.cpp:197 on the sequential chains of solver.cpp:14-31
+    // and matrix.cpp:99-103): the three residual sums are tree sums here; the
+    // reference's chain of the same N non-negative terms lies within
+    // sum_eps·(tree sum) of it, so the reference's decision max(...) <= tol is
+    // known exactly unless tol falls inside the interval — then stop_amb sends
+    // the iteration to the host, which recomputes the chains in the
+    // reference's order (Alm::resolve_stop).
+    int guard;        // 1: decide on intervals (fp64 storage); 0: on the tree values
+    int force_exact;  // RESPCA_ALM_STOP_FORCE_EXACT=1: every stop test goes to the chains
+    int stop_amb;     // the stop test of the last finalized iteration was undecidable
+    double sum_eps;   // relative bound |chain − tree| ≤ sum_eps·tree (rounded up)
+    double xn_lo, xn_hi;  // bounds on the reference's ‖X‖ (= xnorm once it is the chain value)
 };
 
 RESPCA_DEV double warp_sum(double v) {

@@ -298,6 +298,7 @@ DecompositionResult b200::solve(const DenseMatrix& x, const SolverConfig& cfg,
     cfg.validate();  // solver.cpp:128-132 (finite / non-zero are checked on the device)
     if (cfg.c > x.cols()) throw std::invalid_argument("solve: c exceeds column count");
     const auto t0 = std::chrono::steady_clock::now();
+    // allocation only (>= 1 entry); the solver writes rep.iters entries, 0 for fixed_iters = 0
     const std::size_t budget = std::max<std::size_t>(cfg.fixed_iters.value_or(cfg.max_iter), 1);
     DecompositionResult out;
     out.L = DenseMatrix(x.rows(), x.cols());

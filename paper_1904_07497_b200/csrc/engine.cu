@@ -8,6 +8,7 @@
 // (no FMA contraction, solver.cpp / kmeans.cpp compiled for baseline x86-64).
 #include <cuda_profiler_api.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cmath>
@@ -128,7 +129,20 @@ struct Alm : AlmBase {
     KMeansEngine<T>& km;     // solve(): the context's engine (buffers reused)
     WhileGraph wg;
     PlainGraph rest;
-    double init_ms = 0.0, xnorm = 0.0;
+    double init_ms = 0.0, xnorm = 0.0, xsq_tree = 0.0;
+    // exact ALM stop (resolve_stop): the start of the loop it replays from, and
+    // ‖X‖ as the reference's chain once computed
+    Ctl ctl0{};
+    std::vector<int> labels0_h;
+    bool xnorm_chain_ok = false;
+    double xnorm_chain = 0.0;
+    uint64_t stop_resolves = 0;  // iterations whose stop test went to the chains
+    DBuf<T> Lp, Sp;
+    DBuf<double> chains;
+    int force_exact_env = [] {  // RESPCA_ALM_STOP_FORCE_EXACT=1: every stop test on the chains
+        const char* e = std::getenv("RESPCA_ALM_STOP_FORCE_EXACT");
+        return e && e[0] == '1' ? 1 : 0;
+    }();
     bool use_tc = [] {
         const char* e = std::getenv("RESPCA_TC_SCREEN");
         return !(e && e[0] == '0');
@@ -220,6 +234,7 @@ struct Alm : AlmBase {
         CK(cudaMemcpyAsync(h, nrm.p + 3 * 2048, sizeof(h), cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
         if (h[2] != 0.0) throw InvalidArg("solve: non-finite X");
+        xsq_tree = h[0];
         xnorm = std::sqrt(h[0]);
         if (xnorm == 0.0) throw InvalidArg("solve: all-zero X");
     }
@@ -272,6 +287,25 @@ struct Alm : AlmBase {
         h.fixed = cfg.has_fixed_iters ? 1 : 0;
         l21 = cfg.sparse_norm == RESPCA_L21;
         h.l21 = l21 ? 1 : 0;
+        h.done = budget == 0 ? 1 : 0;  // fixed_iters = 0: no iteration (solver.cpp:152, 157)
+        // stop guard: fp64 storage decides like the reference (fp32 storage has
+        // no reference chain to match)
+        h.guard = sizeof(T) == 8 ? 1 : 0;
+        h.force_exact = force_exact_env;
+        h.stop_amb = 0;
+        {
+            // recursive summation of N non-negative terms, any order: |sum − exact| ≤
+            // γ_{N−1}·exact (γ_m = m·u/(1 − m·u)); chain vs tree: ≤ 2γ/(1−γ) of the tree
+            const double u = std::ldexp(1.0, -53), m = (double)(N - 1);
+            const double gam = m * u / (1.0 - m * u);
+            h.sum_eps = 2.0 * gam / (1.0 - gam) * 1.0001;
+            const double e2 = h.sum_eps + 4.0 * u;  // covers this host rounding
+            h.xn_lo = std::sqrt(std::nextafter(xsq_tree * (1.0 - e2), 0.0));
+            h.xn_hi = std::sqrt(std::nextafter(xsq_tree * (1.0 + e2), HUGE_VAL));
+        }
+        xnorm_chain_ok = false;
+        stop_resolves = 0;
+        ctl0 = h;
         write_ctl(h);
     }
 
@@ -302,6 +336,7 @@ struct Alm : AlmBase {
             tr("kmeans");
             km.fetch_labels(labels.p);
         }
+        labels0_h = km.h_labels;
         km.bind(L.p, d, n, c);  // from here on the p-update clusters L
         km.groups.build(km.h_labels.data(), n, c);
         km.upload_groups();
@@ -505,12 +540,16 @@ struct Alm : AlmBase {
     // run the loop to completion (solver.cpp:157-201)
     uint64_t slow_iters = 0;
     void run_loop() {
+        if (budget == 0) return;  // solver.cpp:157: no iteration, L = X, S = 0
         for (;;) {
             const int it0 = read_ctl().iter;
             wg.launch(st);
             Ctl h = read_ctl();
             ln.add((uint64_t)kernels_per_iter() * (uint64_t)(h.iter - it0));
-            if (h.slow) {
+            if (h.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
+            if (h.stop_amb) {
+                resolve_stop(h);  // also runs the iteration's slow path, if any
+            } else if (h.slow) {
                 ++slow_iters;
                 slow_path(h);
                 capture_if_needed();  // the exact continuation may have grown a buffer
@@ -518,6 +557,127 @@ struct Alm : AlmBase {
             if (h.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
             if (h.done) break;
         }
+    }
+
+    // ---- the exact ALM stop ------------------------------------------------
+    // The stop test of iteration t was undecidable on the tree sums.  The
+    // reference decides it on its chains over L_{t+1} − L_t and S_{t+1} − S_t,
+    // but L_t, S_t were overwritten in place.  The solve is deterministic, so it
+    // is replayed from the state after kmeans(X) (fixed-iteration mode, every
+    // iteration — slow paths included — exactly as before) up to iteration t,
+    // L_t and S_t are copied aside, iteration t runs again, and k_exact_chains
+    // computes the reference's three chains (and ‖X‖'s once).  Costs one more
+    // loop up to t plus ≈4 cycles per element and chain; never happens on the
+    // BASELINE workloads without RESPCA_ALM_STOP_FORCE_EXACT=1.
+    void reset_to_start(int target) {
+        const int64_t N = d * n;
+        CK(cudaMemcpyAsync(L.p, X.p, sizeof(T) * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemsetAsync(S.p, 0, sizeof(T) * N, st));
+        CK(cudaMemsetAsync(Th.p, 0, sizeof(T) * N, st));
+        CK(cudaMemcpyAsync(labels.p, labels0_h.data(), sizeof(int) * n, cudaMemcpyHostToDevice, st));
+        km.h_labels = labels0_h;
+        km.groups.build(km.h_labels.data(), n, c);
+        km.upload_groups();
+        Ctl h = ctl0;
+        h.fixed = 1;
+        h.budget = target;
+        h.done = target == 0 ? 1 : 0;
+        write_ctl(h);
+        launch_group_D();
+        CK(cudaStreamSynchronize(st));
+    }
+    // fixed-mode iterations until ctl.iter == target (slow paths included)
+    void advance(int target) {
+        for (;;) {
+            Ctl h = read_ctl();
+            if (h.iter >= target) return;
+            if (!h.done) {
+                wg.launch(st);
+                ln.add((uint64_t)kernels_per_iter() * (uint64_t)(read_ctl().iter - h.iter));
+                h = read_ctl();
+            }
+            if (h.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
+            if (h.slow) {
+                slow_path(h);
+                capture_if_needed();
+            } else if (h.done && h.iter < target) {
+                throw RuntimeErr("respca: replay of the ALM loop stopped early");
+            }
+        }
+    }
+    void resolve_stop(Ctl& h) {
+        const int t = h.iter - 1;
+        const int64_t N = d * n;
+        const Stats s0 = stats;
+        const uint64_t slow0 = slow_iters;
+        // the report rows so far (some may hold chain values already)
+        std::vector<double> rows((size_t)t * 4 + 4);
+        if (t > 0) CK(cudaMemcpyAsync(rows.data(), rep.p, sizeof(double) * 4 * t, cudaMemcpyDeviceToHost, st));
+        Lp.ensure(N);
+        Sp.ensure(N);
+        chains.ensure(4);
+        capture_if_needed();
+        reset_to_start(t);
+        advance(t);
+        CK(cudaMemcpyAsync(Lp.p, L.p, sizeof(T) * N, cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(Sp.p, S.p, sizeof(T) * N, cudaMemcpyDeviceToDevice, st));
+        Ctl g = read_ctl();
+        g.budget = t + 1;
+        g.done = 0;
+        write_ctl(g);
+        wg.launch(st);
+        ln.add((uint64_t)kernels_per_iter());
+        g = read_ctl();
+        if (g.nonfinite) throw NonFinite("solve: non-finite value inside the ALM loop");
+        if (g.iter != t + 1) throw RuntimeErr("respca: replay of the ALM loop diverged");
+        const Stats s1 = stats;
+        const bool was_slow = g.slow != 0;
+        if (was_slow) {
+            slow_path(g);
+            capture_if_needed();
+            g = read_ctl();
+        }
+        const Stats s2 = stats;
+        k_exact_chains<T><<<4, 256, 0, st>>>(X.p, L.p, Lp.p, S.p, Sp.p, N, xnorm_chain_ok ? 1 : 0, chains.p);
+        ln.add();
+        double ch[4];
+        CK(cudaMemcpyAsync(ch, chains.p, sizeof(ch), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (!xnorm_chain_ok) {
+            xnorm_chain = std::sqrt(ch[3]);  // frob_norm, matrix.cpp:99-103
+            xnorm_chain_ok = true;
+        }
+        const double feas = std::sqrt(ch[0]) / xnorm_chain;  // solver.cpp:20, 30
+        const double dl = std::sqrt(ch[1]) / xnorm_chain;
+        const double ds = std::sqrt(ch[2]) / xnorm_chain;
+        // restore the earlier report rows, this row's residuals from the chains
+        if (t > 0) CK(cudaMemcpyAsync(rep.p, rows.data(), sizeof(double) * 4 * t, cudaMemcpyHostToDevice, st));
+        const double r3[3] = {feas, dl, ds};
+        CK(cudaMemcpyAsync(rep.p + (size_t)t * 4, r3, sizeof(r3), cudaMemcpyHostToDevice, st));
+        const bool conv = !ctl0.fixed && std::max({feas, dl, ds}) <= cfg.tol;  // solver.cpp:197
+        g.fixed = ctl0.fixed;
+        g.budget = ctl0.budget;
+        g.converged = conv ? 1 : 0;
+        g.stop_amb = 0;
+        g.slow = 0;
+        g.exact_fallbacks = h.exact_fallbacks;
+        std::copy(h.margin_hist, h.margin_hist + 6, g.margin_hist);
+        g.xnorm = xnorm_chain;  // from here on the report divides by the reference's ‖X‖
+        g.xn_lo = g.xn_hi = xnorm_chain;
+        g.done = conv || g.nonfinite || g.iter >= g.budget;
+        write_ctl(g);
+        CK(cudaStreamSynchronize(st));
+        stats = s0;
+        stats.hartigan_moves += s2.hartigan_moves - s1.hartigan_moves;
+        stats.exact_fallbacks += s2.exact_fallbacks - s1.exact_fallbacks;
+        stats.lloyd_steps += s2.lloyd_steps - s1.lloyd_steps;
+        stats.hartigan_passes += s2.hartigan_passes - s1.hartigan_passes;
+        slow_iters = slow0 + (was_slow ? 1 : 0);
+        ++stop_resolves;
+        if (trace_on())
+            std::fprintf(stderr, "[respca] stop test of iteration %d on the chains: max %.17g vs tol %.17g -> %s\n",
+                         t + 1, std::max({feas, dl, ds}), cfg.tol, conv ? "converged" : "continue");
+        h = g;
     }
 
     void download(T* Lo, T* So, uint64_t* lab, respca_cu_report* rep_out) {
@@ -561,6 +721,7 @@ struct Alm : AlmBase {
             rep_out->slow_iters = slow_iters;
             rep_out->hartigan_moves = stats.hartigan_moves;
             rep_out->exact_fallbacks = stats.exact_fallbacks + h.exact_fallbacks;
+            rep_out->stop_resolves = stop_resolves;
         }
     }
 

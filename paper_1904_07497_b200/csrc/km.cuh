@@ -370,6 +370,14 @@ struct Screen {
     int nsplit, n, c;
     double kappa_d;
     double abs_e = 0.0;  // absolute half-width term (TMA screen: FP32 underflow of ‖x‖² chunk sums)
+    // BF16 screens: operands below the FP32/BF16 normal range are subnormal or
+    // flushed (|error| ≤ 2⁻¹²⁶ per operand and product, not relative), so the
+    // half-width gets lin_e·(‖x‖ + ‖c‖) on top of abs_e
+    double lin_e = 0.0;
+    // tcgen05 screens: their error flag (an mbarrier wait timed out, the
+    // accumulators are not valid); set → every interval is unbounded, i.e. every
+    // decision goes to the exact chains
+    const int* err = nullptr;
     // split partials in split order; loads four at a time (the padding zeros
     // leave the sums unchanged: they never start from −0)
     RESPCA_DEV double xx(int j) const {
@@ -398,8 +406,9 @@ struct Screen {
     RESPCA_DEV void interval(double xxj, double nx, double dot, double ck, double& lo, double& hi,
                              double& mid) const {
         mid = (xxj + ck) - 2.0 * dot;
-        const double e = screen_err(kappa_d, nx, sqrt(fabs(ck)), mid) + abs_e;
-        if (!isfinite(mid) || !isfinite(e)) {
+        const double nc = sqrt(fabs(ck));
+        const double e = screen_err(kappa_d, nx, nc, mid) + abs_e + lin_e * (nx + nc);
+        if (!isfinite(mid) || !isfinite(e) || (err && __ldg(err) != 0)) {
             lo = -INFINITY;
             hi = INFINITY;
         } else {

@@ -288,6 +288,9 @@ struct KMeansEngine {
         tcCb.ensure((size_t)TC_N * dpad);
         tcerr.ensure(1);
         CK(pdl_launch(k_tc_prep_centroids, dim3(TC_N), dim3(1024), 0, st, C, d, c, dpad, tcCb.p, cc.p, tcerr.p));
+        // RESPCA_TC_FORCE_ERR=1 (tests): raise the screen's error flag as a timed-out
+        // mbarrier wait would — every decision must then come from the exact chains
+        if (env_int("RESPCA_TC_FORCE_ERR", 0)) CK(cudaMemsetAsync(tcerr.p, 0x7f, sizeof(int), st));
         if (tma_key_a != (const void*)Lbp || tma_key_n != n || tma_key_dpad != dpad) {
             mapA = make_map(Lbp, (uint64_t)dpad, (uint64_t)n, TC_M);
             mapB = make_map(tcCb.p, (uint64_t)dpad, (uint64_t)TC_N, TC_N);
@@ -323,6 +326,14 @@ struct KMeansEngine {
         s.kappa_d = tc_mode ? tc_bf16_kappa((double)d) + kappa_screen() : kappa_screen();
         if (tma_mode) s.kappa_d = (s.kappa_d + tma_xx_kappa((double)d)) * 1.01;  // ‖x‖² from BF16 values
         if (tma_mode) s.abs_e = tma_xx_abs((double)d) * 1.01;
+        if (tc_mode) {
+            // per operand |η| ≤ 2⁻¹²⁶ (BF16 subnormal or flushed): Σ|η|(|x_i| + |c_i|) + η² per dot,
+            // twice in the distance; products flushed below 2⁻¹²⁶: d·2⁻¹²⁶ per dot
+            const double t = std::ldexp(1.0, -126);
+            s.abs_e += 4.0 * (double)d * t * 1.01;
+            s.lin_e = 2.0 * std::sqrt((double)d) * t * 1.01;
+            s.err = tcerr.p;
+        }
         return s;
     }
 

@@ -100,6 +100,7 @@ class DecompositionResult:
     slow_iters: int = 0
     hartigan_moves: int = 0
     exact_fallbacks: int = 0
+    stop_resolves: int = 0  # stop tests decided on the reference's sequential residual chains
 
 
 @dataclass
@@ -150,7 +151,7 @@ def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
     xm = _mat(x, dt)
     d, n = xm.shape
     budget = cfg.fixed_iters if cfg.fixed_iters is not None else cfg.max_iter
-    budget = max(int(budget), 1)
+    budget = max(int(budget), 1)  # allocation only: the solver writes rep.iters (0 for fixed_iters=0)
     if out is not None:
         L, S = out
         for a in (L, S):
@@ -175,7 +176,7 @@ def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
     return DecompositionResult(L, S, lab, report, float(rep.wall_time), float(rep.lambda_),
                                float(rep.init_ms), float(rep.loop_ms), float(rep.h2d_ms),
                                float(rep.d2h_ms), int(rep.slow_iters), int(rep.hartigan_moves),
-                               int(rep.exact_fallbacks))
+                               int(rep.exact_fallbacks), int(rep.stop_resolves))
 
 
 def _result(L, S, lab, arrs, rep) -> DecompositionResult:
@@ -185,7 +186,7 @@ def _result(L, S, lab, arrs, rep) -> DecompositionResult:
     return DecompositionResult(L, S, lab, report, float(rep.wall_time), float(rep.lambda_),
                                float(rep.init_ms), float(rep.loop_ms), float(rep.h2d_ms),
                                float(rep.d2h_ms), int(rep.slow_iters), int(rep.hartigan_moves),
-                               int(rep.exact_fallbacks))
+                               int(rep.exact_fallbacks), int(rep.stop_resolves))
 
 
 def binary_info(path) -> tuple[int, int]:
@@ -210,7 +211,7 @@ def solve_file(x_path, cfg: Optional[SolverConfig] = None, l_path=None, s_path=N
     ctx = _ctx(ctx)
     d, n = binary_info(x_path)
     budget = cfg.fixed_iters if cfg.fixed_iters is not None else cfg.max_iter
-    budget = max(int(budget), 1)
+    budget = max(int(budget), 1)  # allocation only: the solver writes rep.iters (0 for fixed_iters=0)
     lab = np.empty(n, dtype=np.uint64)
     arrs = [np.zeros(budget) for _ in range(4)]
     rep = N.CReport()

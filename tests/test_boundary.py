@@ -76,7 +76,7 @@ def test_config_struct_layout_matches_header():
 #include "respca_cu.h"
 int main(void) {
   printf("%zu %zu %zu %zu %zu\n", sizeof(respca_cu_config), offsetof(respca_cu_config, fixed_iters),
-         sizeof(respca_cu_report), offsetof(respca_cu_report, exact_fallbacks),
+         sizeof(respca_cu_report), offsetof(respca_cu_report, stop_resolves),
          offsetof(respca_cu_config, km_tol));
   return 0;
 }'''
@@ -87,7 +87,7 @@ int main(void) {
         subprocess.run(["gcc", f"-I{ROOT / 'include'}", str(p), "-o", str(exe)], check=True)
         out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
     got = [C.sizeof(N.CConfig), N.CConfig.fixed_iters.offset, C.sizeof(N.CReport),
-           N.CReport.exact_fallbacks.offset, N.CConfig.km_tol.offset]
+           N.CReport.stop_resolves.offset, N.CConfig.km_tol.offset]
     assert [int(v) for v in out] == got
 
 

@@ -89,6 +89,31 @@ def test_port_vs_reference_random_solves(orc):
 
 
 @need_ref
+def test_port_vs_reference_stop_edges(orc):
+    """The edges tests/test_gpu_stop.py checks the device against: fixed_iters
+    = 0 (solver.cpp:152, 157) and tol exactly on / one ulp below the
+    reference's own max residual (solver.cpp:197, `<=`)."""
+    from paper_1904_07497_b200 import synth
+    from paper_1904_07497_b200.respca import SolverConfig
+
+    ref = O.reference()
+    X = synth.rpca(40, 60, 3, 1.0, 0.05, seed=21)
+    for c in (1, 3):
+        a = orc.solve(X, SolverConfig(c=c, fixed_iters=0))
+        _same_result(a, ref.solve(X, SolverConfig(c=c, fixed_iters=0)))
+        assert a.iters == 0 and bitwise(a.L, X) and not a.S.any()
+    X = synth.rpca(60, 80, 3, 1.0, 0.05, seed=3)
+    probe = ref.solve(X, SolverConfig(c=4, tol=1e-300, max_iter=30))
+    mx = np.maximum(np.maximum(probe.feas, probe.delta_l), probe.delta_s)
+    k = next(t for t in range(8, len(mx)) if mx[t] < mx[:t].min())
+    for tol, stops_at_k in ((float(mx[k]), True), (float(np.nextafter(mx[k], 0.0)), False)):
+        cfg = SolverConfig(c=4, tol=tol, max_iter=30)
+        r = ref.solve(X, cfg)
+        _same_result(orc.solve(X, cfg), r)
+        assert (r.iters == k + 1) == stops_at_k
+
+
+@need_ref
 def test_port_vs_reference_building_blocks(orc):
     ref = O.reference()
     rng = np.random.default_rng(1)
