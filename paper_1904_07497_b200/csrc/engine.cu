@@ -752,6 +752,10 @@ struct Alm : AlmBase {
         // to exactly the timed iterations
         const char* prof = std::getenv("RESPCA_PROFILE_TIMED");
         const bool profiling = prof && prof[0] == '1' && iters > 1;
+        // RESPCA_BENCH_EAGER=1: every kernel of the iteration launched on the
+        // stream (no graph), so launch tracers that do not see graph nodes list them
+        const char* eg = std::getenv("RESPCA_BENCH_EAGER");
+        const bool eager = eg && eg[0] == '1';
         if (profiling) CK(cudaProfilerStart());
         double fsum = 0.0, asum = 0.0;
         CK(cudaEventRecord(all.a, st));
@@ -762,7 +766,15 @@ struct Alm : AlmBase {
                 launch_pass_f();
                 CK(cudaEventRecord(evf[base + t].b, st));
                 CK(cudaEventRecord(eva[base + t].a, st));
-                rest.launch(st);
+                if (eager) {
+                    const uint64_t l0 = *ln.counter;
+                    launch_pass_a();
+                    launch_post();
+                    launch_finalize(false);
+                    *ln.counter = l0;
+                } else {
+                    rest.launch(st);
+                }
                 ln.add(kernels_per_iter() - 1);
                 CK(cudaEventRecord(eva[base + t].b, st));
             }

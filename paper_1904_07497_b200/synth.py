@@ -26,15 +26,25 @@ class _Video(C.Structure):
 
 
 _lib = None
+_lib_path = None
+
+
+def use_library(path) -> None:
+    """Load the generator from `path` instead of lib/libsynth.so — bench.py's
+    reference arm uses the copy oracle/Makefile builds (oracle/libinput.so) so
+    that arm loads no library of this package."""
+    global _lib, _lib_path
+    _lib, _lib_path = None, Path(path)
 
 
 def _L():
     global _lib
     if _lib is None:
-        if not LIB.exists():
+        path = _lib_path or LIB
+        if _lib_path is None and not LIB.exists():
             from .build import build_synth
             build_synth()
-        _lib = C.CDLL(str(LIB))
+        _lib = C.CDLL(str(path))
         _lib.synth_rpca.argtypes = [C.POINTER(_Rpca), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.synth_video.argtypes = [C.POINTER(_Video), C.c_void_p, C.c_void_p, C.c_void_p]
         _lib.synth_version.restype = C.c_char_p
