@@ -400,6 +400,251 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
         for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
 }
 
+template <typename T>
+RESPCA_DEV void store_vec16(T* p, const double* a);
+template <>
+RESPCA_DEV void store_vec16<double>(double* p, const double* a) {
+    __stcs(reinterpret_cast<double2*>(p), make_double2(a[0], a[1]));
+}
+template <>
+RESPCA_DEV void store_vec16<float>(float* p, const double* a) {
+    __stcs(reinterpret_cast<float4*>(p), make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]));
+}
+
+// ---------------------------------------------------------------------------
+// Pass F as streams: one CTA per (group g, block of rb rows) walks g's members
+// in ascending order, so each row's two running sums stay inside one CTA (no
+// cross-CTA hand-off), while the element work of a stage of mps members is
+// spread over all 256 threads (a thread owns K 16-byte chunks = K·VEC rows of
+// one member each) — what the one-thread-per-row walk of k_pass_f_ring lacks
+// when d is small relative to the GPU (C3-c1: 10⁴ rows for 148 SMs).
+//
+// rb is a runtime multiple of VEC (16-byte aligned segments since d % VEC == 0),
+// chosen by the host so that the c·⌈d/rb⌉ streams fill whole waves of the
+// resident CTAs (c = 1: one wave, every stream runs the whole time).
+//
+// Pipeline: NS stages of X, S, Θ, L [mps][rb] staged by cp.async, NS − 1 in
+// flight while one is computed.  A thread loads and later reads only its own
+// chunks of every stage (fixed chunk positions), so the stages need no
+// barrier.  The two summands of each element go to a double-buffered shared
+// array; after one __syncthreads per stage, warp 0 adds them in member order
+// (lane = row, RPL rows per lane) while the other warps go on to the next
+// stage.  Member indices are staged one stage ahead (a register prefetch
+// plus a per-thread shared slot), so no address waits on a global load.
+// ---------------------------------------------------------------------------
+template <typename T, int K, int NS, int RBMAX>
+struct StreamCfg {
+    static constexpr int VEC = 16 / (int)sizeof(T);
+    static constexpr int CPS = 256 * K;  // 16-byte chunks per stage (all arrays count once)
+    static constexpr int RPL = RBMAX / 32;
+    static constexpr int SMEM = NS * 4 * CPS * 16 + 2 * 2 * CPS * VEC * 8 + NS * CPS * 4;
+};
+
+RESPCA_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+RESPCA_DEV void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
+
+constexpr int PFS_THREADS = 288;  // 8 element warps + 1 chain warp
+template <typename T, int K, int NS, int RBMAX>
+__global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
+    const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
+    const int* __restrict__ goff, const int* __restrict__ members, const int* __restrict__ gorder,
+    const double* G0, const double* G1, double* Gn0, double* Gn1, double* __restrict__ Cw,
+    const double* __restrict__ mean_w, const Ctl* __restrict__ ctl, double* __restrict__ partials,
+    int64_t d, int rb_rows, int nrb, __nv_bfloat16* __restrict__ Lb, int64_t dpad, int ident) {
+    // ident: every group's members are consecutive columns (c = 1: the one group
+    // is 0..n−1), so a member index is gb + position and needs no load
+    using C = StreamCfg<T, K, NS, RBMAX>;
+    constexpr int VEC = C::VEC, CPS = C::CPS, RPL = C::RPL;
+    static_assert(RBMAX % 32 == 0 && RBMAX / VEC <= CPS, "stream tile");
+    // named barriers: FULL[b] (element warps → chain warp), EMPTY[b] (back)
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3;
+    extern __shared__ __align__(16) unsigned char pfs_sm[];
+    // stage s, array a, chunk k: 16 bytes at ((s·4 + a)·CPS + k)·16
+    unsigned char* stg = pfs_sm;
+    double* summ = reinterpret_cast<double*>(pfs_sm + NS * 4 * CPS * 16);  // [2 bufs][2][CPS·VEC]
+    int* scol = reinterpret_cast<int*>(pfs_sm + NS * 4 * CPS * 16 + 2 * 2 * CPS * VEC * 8);  // [NS][CPS]
+    __shared__ double red[32 * 5];
+    pdl_enter();
+    if (ctl->done) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gi = blockIdx.x / nrb;
+    const int rbi = blockIdx.x - gi * nrb;
+    const int g = gorder ? __ldg(gorder + gi) : gi;  // longest member walks first
+    const int lpc = rb_rows / VEC;                    // chunks per member segment
+    const int mps = CPS / lpc;                        // members per stage
+    const int64_t r0 = (int64_t)rbi * rb_rows;
+    const int par = ctl->parity;
+    const double* Gc = par ? G1 : G0;
+    double* Gn = par ? Gn0 : Gn1;
+    const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
+    const double mw = mean_w[g];
+    const int gb = __ldg(goff + g), ge = __ldg(goff + g + 1);
+    const int m = ge - gb;
+    const int nst = (m + mps - 1) / mps;
+    const double ng = (double)m;
+    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
+    if (warp < 8) {
+        // ================= element warps =================
+        const double mscale = own_w / ng + mw;
+        // this thread's chunks (the same positions in every stage)
+        int cmem[K], csub[K];
+        bool crow[K];
+        double Gi[K][VEC], mt[K][VEC];
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+            const int k = tid + 256 * j;
+            cmem[j] = k / lpc;
+            csub[j] = k - cmem[j] * lpc;
+            crow[j] = cmem[j] < mps && r0 + csub[j] * VEC < d;
+            const int64_t row = r0 + csub[j] * VEC;
+#pragma unroll
+            for (int v = 0; v < VEC; ++v) {
+                Gi[j][v] = crow[j] ? Gc[(int64_t)g * d + row + v] : 0.0;
+                mt[j][v] = Gi[j][v] * mscale;
+            }
+        }
+        // member index of chunk j in stage s (−1: none)
+        auto member_of = [&](int s, int j) -> int {
+            const int c_ = s * mps + cmem[j];
+            return (s < nst && crow[j] && c_ < m) ? (ident ? gb + c_ : __ldg(members + gb + c_)) : -1;
+        };
+        auto issue = [&](int s, const int (&col)[K]) {
+            if (s < nst) {
+#pragma unroll
+                for (int j = 0; j < K; ++j) {
+                    const int k = tid + 256 * j;
+                    const bool ok = col[j] >= 0;
+                    const int64_t off = ok ? (int64_t)col[j] * d + r0 + csub[j] * VEC : 0;
+                    const int nb = ok ? 16 : 0;
+                    unsigned char* base = stg + (size_t)(s % NS) * 4 * CPS * 16 + (size_t)k * 16;
+                    cp_async16(base, X + off, nb);
+                    cp_async16(base + CPS * 16, S + off, nb);
+                    cp_async16(base + 2 * CPS * 16, Th + off, nb);
+                    cp_async16(base + 3 * CPS * 16, L + off, nb);
+                    scol[(s % NS) * CPS + k] = col[j];
+                }
+            }
+            cp_commit();  // one group per stage, empty past the end
+        };
+        int nxt[K];
+#pragma unroll
+        for (int s = 0; s < NS - 1; ++s) {
+            int col[K];
+#pragma unroll
+            for (int j = 0; j < K; ++j) col[j] = member_of(s, j);
+            issue(s, col);
+        }
+#pragma unroll
+        for (int j = 0; j < K; ++j) nxt[j] = member_of(NS - 1, j);
+        for (int s = 0; s < nst; ++s) {
+            issue(s + NS - 1, nxt);
+#pragma unroll
+            for (int j = 0; j < K; ++j) nxt[j] = member_of(s + NS, j);  // consumed next stage
+            cp_wait<NS - 1>();  // this thread's chunks of stage s have landed
+            if (s >= 2) named_bar_sync(BAR_EMPTY + (s & 1), PFS_THREADS);  // chain of stage s − 2 done
+            double* sm_ = summ + (size_t)(s & 1) * 2 * CPS * VEC;
+#pragma unroll
+            for (int j = 0; j < K; ++j) {
+                if (cmem[j] >= mps) continue;  // a chunk past the stage's members (mps·lpc < CPS)
+                const int k = tid + 256 * j;
+                const unsigned char* base = stg + (size_t)(s % NS) * 4 * CPS * 16 + (size_t)k * 16;
+                const T* xs = reinterpret_cast<const T*>(base);
+                const T* ss = reinterpret_cast<const T*>(base + CPS * 16);
+                const T* ts = reinterpret_cast<const T*>(base + 2 * CPS * 16);
+                const T* ls = reinterpret_cast<const T*>(base + 3 * CPS * 16);
+                const int col = scol[(s % NS) * CPS + k];
+                const bool ok = col >= 0;
+                double lo_[VEC], so_[VEC], to_[VEC];
+#pragma unroll
+                for (int v = 0; v < VEC; ++v) {
+                    // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
+                    const double x = (double)xs[v], sv = (double)ss[v], th = (double)ts[v], lp = (double)ls[v];
+                    const double qq = th / rho;
+                    const double dv = (x - sv) + qq;
+                    const double ln = own_w * dv + mw * Gi[j][v];
+                    const double xl = x - ln;
+                    const double bb = xl + qq;
+                    const double mag = fabs(bb) - thr;
+                    const double sn = mag > 0.0 ? copysign(mag, bb) : 0.0;
+                    const double r = xl - sn;
+                    const double tn = th + rho * r;
+                    // summand layout [2][member][row of the block]
+                    const int e = cmem[j] * rb_rows + csub[j] * VEC + v;
+                    sm_[e] = ln;
+                    sm_[CPS * VEC + e] = (x - sn) + tn / rho_n;
+                    lo_[v] = ln;
+                    so_[v] = sn;
+                    to_[v] = tn;
+                    if (ok) {
+                        pf += r * r;
+                        const double dl = ln - lp;
+                        pl += dl * dl;
+                        const double ds = sn - sv;
+                        ps += ds * ds;
+                        p1 += fabs(sn);
+                        const double dm = ln - mt[j][v];
+                        psc += dm * dm;
+                    }
+                }
+                if (ok) {
+                    const int64_t off = (int64_t)col * d + r0 + csub[j] * VEC;
+                    store_vec16<T>(L + off, lo_);
+                    store_vec16<T>(S + off, so_);
+                    store_vec16<T>(Th + off, to_);
+                    if (Lb) {
+                        __nv_bfloat16* lb = Lb + (int64_t)col * dpad + r0 + csub[j] * VEC;
+#pragma unroll
+                        for (int v = 0; v < VEC; v += 2) {
+                            __nv_bfloat162 b2;
+                            b2.x = __double2bfloat16(lo_[v]);
+                            b2.y = __double2bfloat16(lo_[v + 1]);
+                            *reinterpret_cast<__nv_bfloat162*>(lb + v) = b2;
+                        }
+                    }
+                }
+            }
+            named_bar_arrive(BAR_FULL + (s & 1), PFS_THREADS);  // stage s's summands are in place
+        }
+        cp_wait<0>();
+    } else {
+        // ================= the chain warp: each row's two sums in member order =================
+        double a[RPL], b[RPL];
+        int rl[RPL];
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            a[q] = b[q] = 0.0;
+            rl[q] = (lane + 32 * q) < rb_rows ? lane + 32 * q : 0;
+        }
+        for (int s = 0; s < nst; ++s) {
+            named_bar_sync(BAR_FULL + (s & 1), PFS_THREADS);
+            const double* y0 = summ + (size_t)(s & 1) * 2 * CPS * VEC;
+            const double* y1 = y0 + CPS * VEC;
+            const int cnt = m - s * mps < mps ? m - s * mps : mps;
+#pragma unroll 4
+            for (int u = 0; u < cnt; ++u)
+#pragma unroll
+                for (int q = 0; q < RPL; ++q) {
+                    a[q] += y0[u * rb_rows + rl[q]];  // ascending member order (solver.cpp:64, kmeans.cpp:73)
+                    b[q] += y1[u * rb_rows + rl[q]];
+                }
+            if (s + 2 < nst) named_bar_arrive(BAR_EMPTY + (s & 1), PFS_THREADS);
+        }
+#pragma unroll
+        for (int q = 0; q < RPL; ++q) {
+            const int r_ = lane + 32 * q;
+            if (r_ < rb_rows && r0 + r_ < d) {
+                Cw[(int64_t)g * d + r0 + r_] = a[q] * (1.0 / ng);  // kmeans.cpp:78-79
+                Gn[(int64_t)g * d + r0 + r_] = b[q];
+            }
+        }
+    }
+    double pv[5] = {pf, pl, ps, p1, psc};
+    block_sum<5>(pv, red);
+    if (tid == 0)
+#pragma unroll
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = pv[q];
+}
+
 // ---------------------------------------------------------------------------
 // ℓ2,1 variant of the iteration (sparse_norm = L21, solver.cpp:90-102), split
 // around the column norms of B that the shrinkage needs:

@@ -96,6 +96,14 @@ struct Alm : AlmBase {
     int R = 1, rowblocks = 0, nbF = 0;
     int nbP = 0;          // Pass F partials (CTAs) of the fast path
     bool pf_ring = false;  // Pass F as k_pass_f_ring (few groups)
+    // Pass F as streams (k_pass_f_stream): RESPCA_PASSF_STREAM = 0 never, 1 always
+    // (where d allows 16-byte copies), default: c = 1; RESPCA_STREAM_RB = rows per stream
+    int passf_stream_env = [] {
+        const char* e = std::getenv("RESPCA_PASSF_STREAM");
+        return e ? std::atoi(e) : -1;
+    }();
+    bool pf_stream = false;
+    int stream_rb = 32, stream_nrb = 0;
     int ring_cfg() const {  // RESPCA_RING_CFG = 5, 10 or 16 (tuning)
         if (const char* e = std::getenv("RESPCA_RING_CFG")) {
             const int r = std::atoi(e);
@@ -271,6 +279,37 @@ struct Alm : AlmBase {
         // RESPCA_PASSF_RING=0 keeps k_pass_f
         pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0;
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
+        // c = 1 with d up to 2·10⁴ rows: one-thread-per-row walks cannot fill the GPU
+        // (measured Pass F fraction of HBM, ring → stream: C2-c1 0.06 → 0.40,
+        // C3-c1 0.31 → 0.65; C5 (d = 4·10⁴) stays on the ring, 0.74 vs 0.73)
+        pf_stream = !(cfg.sparse_norm == RESPCA_L21) && d % (16 / (int64_t)sizeof(T)) == 0 &&
+                    (passf_stream_env > 0 || (passf_stream_env < 0 && c == 1 && d <= 20000));
+        if (pf_stream) {
+            // rows per stream (a multiple of VEC, 16..RBMAX): the c·⌈d/rb⌉ streams
+            // should fill whole waves of the 2·148 resident CTAs — the fill
+            // (streams / (waves·slots)) decides, ties to the wider segment
+            const int vec = 16 / (int)sizeof(T), rbmax = sizeof(T) == 8 ? 128 : 256;
+            const int64_t slots = 2 * 148;
+            double best = -1.0;
+            for (int r = 16; r <= rbmax; r += vec) {
+                if (r / vec > 256) break;
+                const int64_t ns = (int64_t)c * ceil_div(d, (int64_t)r);
+                const int64_t waves = ceil_div(ns, slots);
+                const double fill = (double)ns / (double)(waves * slots);
+                // a stream needs enough rows for whole 128-byte lines (r·s ≥ 128)
+                const double score = fill - (r * (int)sizeof(T) < 256 ? 0.05 : 0.0);
+                if (score >= best) {
+                    best = score;
+                    stream_rb = r;
+                }
+            }
+            if (const char* e = std::getenv("RESPCA_STREAM_RB")) {
+                const int r = std::atoi(e);
+                if (r >= vec && r <= rbmax && r % vec == 0) stream_rb = r;
+            }
+            stream_nrb = (int)ceil_div(d, (int64_t)stream_rb);
+            nbP = c * stream_nrb;
+        }
         partials.ensure((size_t)std::max(nbF, nbP) * 5);
         Ctl h{};
         h.rho = cfg.rho0;
@@ -343,6 +382,18 @@ struct Alm : AlmBase {
         tr("groups");
     }
 
+    template <int K, int NS, int RBMAX>
+    void launch_stream() {
+        auto kf = k_pass_f_stream<T, K, NS, RBMAX>;
+        constexpr int sm = StreamCfg<T, K, NS, RBMAX>::SMEM;
+        CK(cudaFuncSetAttribute((const void*)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, sm));
+        double* G1 = G.p + (size_t)d * c;
+        kf<<<c * stream_nrb, PFS_THREADS, sm, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
+                                             c > 1 ? km.gsize_ord.p : nullptr, G.p, G1, G.p, G1, Cw.p,
+                                             mean_w.p, ctl.p, partials.p, d, stream_rb, stream_nrb,
+                                             lb_on ? Lb.p : nullptr, dpad, c == 1 ? 1 : 0);
+    }
+
     void launch_group_D() {  // G_t = Σ_{j∈g} ((x − s) + θ/ρ) into G[parity]
         if (R == 2)
             k_group_sum<T, 2, 0><<<nbF, 256, 0, st>>>(X.p, S.p, Th.p, km.goff.p, km.members.p,
@@ -402,6 +453,12 @@ struct Alm : AlmBase {
                 k_pass_f1<T, 1><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
                                                     G.p, G1, Cw.p, mean_w.p, ctl.p, partials.p, d,
                                                     rowblocks);
+            ln.add();
+            return;
+        }
+        if (pf_stream) {
+            if constexpr (sizeof(T) == 8) launch_stream<1, 5, 128>();
+            else launch_stream<1, 4, 256>();
             ln.add();
             return;
         }
@@ -477,7 +534,7 @@ struct Alm : AlmBase {
     void capture_if_needed() {
         const uint64_t key[13] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
                                   (uint64_t)(use_tc && !tc_useless), (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
-                                  (uint64_t)passf_variant_env, (uint64_t)dpad, g_alloc_gen.load(),
+                                  (uint64_t)passf_variant_env ^ ((uint64_t)pf_stream << 44) ^ ((uint64_t)stream_rb << 45), (uint64_t)dpad, g_alloc_gen.load(),
                                   (uint64_t)pdl_on()};
         if (cap_valid && std::equal(key, key + 13, cap_key)) return;
         cap_valid = false;
