@@ -163,6 +163,14 @@ int respca_cu_debug_screen_tc(respca_cu_ctx* ctx, const double* m, uint64_t d, u
                               const double* centroids, uint64_t c, double* approx_out,
                               double* err_out);
 
+/* Test hook for device memory checking (compute-sanitizer is unavailable on
+ * the GPU pool): with RESPCA_GUARD=1 in the environment every device
+ * allocation is poisoned with 0xFF bytes and followed by a 4 KiB guard;
+ * returns the number of guards found overwritten (guard mode never frees
+ * device memory, so every buffer ever allocated is checked), -1 when
+ * RESPCA_GUARD is off; `msg` (may be NULL) describes the first ones. */
+int respca_cu_debug_guards(char* msg, uint64_t cap);
+
 /* --- benchmark hooks (device-resident state, no host copies) ------------- */
 /* Upload X and run validation + the one-time initial clustering; leaves the
  * context ready to step the ALM loop.  init_ms receives the device time. */

@@ -58,7 +58,7 @@ EXPORTS = [
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
     "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
-    "respca_cu_debug_screen_tc", "respca_cu_binary_info", "respca_cu_solve_file",
+    "respca_cu_debug_screen_tc", "respca_cu_debug_guards", "respca_cu_binary_info", "respca_cu_solve_file",
     "respca_cu_outlier_scores", "respca_cu_synth_rpca",
 ]
 
@@ -110,6 +110,7 @@ def lib() -> C.CDLL:
             L.respca_cu_bench_steps.argtypes = [vp, u64, dptr, dptr, dptr, u64ptr]
             L.respca_cu_debug_screen.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             L.respca_cu_debug_screen_tc.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
+            L.respca_cu_debug_guards.argtypes = [C.c_char_p, u64]
             L.respca_cu_binary_info.argtypes = [C.c_char_p, u64ptr, u64ptr, C.c_char_p, C.c_size_t]
             L.respca_cu_solve_file.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(CConfig),
                                                C.c_char_p, C.c_char_p, u64ptr, u64, C.POINTER(CReport)]

@@ -114,137 +114,6 @@ struct Vec<float, 4> {
 // Traffic: reads X, S, Θ, L_t; writes L', S', Θ' — 7·d·n·sizeof(T).
 // L, S, Θ are updated in place (each element is owned by one thread).
 // ---------------------------------------------------------------------------
-template <typename T, int R, int U, int MINB = 1>
-__global__ void __launch_bounds__(256, MINB) k_pass_f(
-    const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
-    const int* __restrict__ goff, const int* __restrict__ members,
-    // G0/G1 and Gn0/Gn1 are the same two buffers: G_t is read from
-    // buf[parity], G_{t+1} written to buf[1 - parity] (never the same one)
-    const double* G0, const double* G1, double* Gn0, double* Gn1, double* __restrict__ Cw,
-    const double* __restrict__ mean_w, const Ctl* __restrict__ ctl,
-    double* __restrict__ partials, int64_t d, int rowblocks,
-    // optional BF16 copy of L′ in the K-major [n][dpad] layout the tcgen05
-    // screen loads by TMA (nullptr: not written)
-    __nv_bfloat16* __restrict__ Lb, int64_t dpad,
-    // groups largest first (nullptr: in index order); partials stay per blockIdx
-    const int* __restrict__ gorder = nullptr) {
-    __shared__ double red[32 * 5];
-    if (ctl->done) return;  // loop already finished (bench launches ahead)
-    const int gi = blockIdx.x / rowblocks;
-    const int rb = blockIdx.x - gi * rowblocks;
-    const int g = gorder ? __ldg(gorder + gi) : gi;
-    const int64_t i0 = ((int64_t)rb * blockDim.x + threadIdx.x) * R;
-    const bool active = i0 < d;
-
-    const int par = ctl->parity;
-    const double* Gc = par ? G1 : G0;
-    double* Gn = par ? Gn0 : Gn1;
-    const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
-    const double mw = mean_w[g];
-    const int beg = goff[g], end = goff[g + 1];
-    const double ng = (double)(end - beg);
-    const double mscale = own_w / ng + mw;  // exact-arithmetic mean of L' over g is G·mscale
-
-    double G[R], cacc[R], gacc[R], mt[R];
-    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
-    if (active) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            G[r] = Gc[(int64_t)g * d + i0 + r];
-            mt[r] = G[r] * mscale;
-            cacc[r] = 0.0;
-            gacc[r] = 0.0;
-        }
-
-        auto body = [&](const Vec<T, R>& xv, const Vec<T, R>& sv, const Vec<T, R>& tv,
-                        const Vec<T, R>& lv, int64_t off, int col) {
-            double lo[R], so[R], to[R];
-#pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const double x = xv.v[r], s = sv.v[r], th = tv.v[r];
-                const double q = th / rho;
-                const double dv = (x - s) + q;
-                const double ln = own_w * dv + mw * G[r];
-                cacc[r] += ln;
-                const double xl = x - ln;
-                const double b = xl + q;
-                const double mag = fabs(b) - thr;
-                const double sn = mag > 0.0 ? copysign(mag, b) : 0.0;
-                const double rr = xl - sn;
-                const double tn = th + rho * rr;
-                gacc[r] += (x - sn) + tn / rho_n;
-                pf += rr * rr;
-                const double dl = ln - lv.v[r];
-                pl += dl * dl;
-                const double ds = sn - s;
-                ps += ds * ds;
-                p1 += fabs(sn);
-                const double dm = ln - mt[r];
-                psc += dm * dm;
-                lo[r] = ln;
-                so[r] = sn;
-                to[r] = tn;
-            }
-            Vec<T, R>::store(L + off, lo);
-            Vec<T, R>::store(S + off, so);
-            Vec<T, R>::store(Th + off, to);
-            if (Lb) {
-                __nv_bfloat16* lb = Lb + (int64_t)col * dpad + i0;
-                if (R == 2) {
-                    __nv_bfloat162 b2;
-                    b2.x = __double2bfloat16(lo[0]);
-                    b2.y = __double2bfloat16(lo[R - 1]);
-                    *reinterpret_cast<__nv_bfloat162*>(lb) = b2;
-                } else {
-                    lb[0] = __double2bfloat16(lo[0]);
-                }
-            }
-        };
-
-        int t = beg;
-        for (; t + U <= end; t += U) {
-            Vec<T, R> xv[U], sv[U], tv[U], lv[U];
-            int64_t off[U];
-            int mj[U];
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                mj[u] = __ldg(members + t + u);
-                off[u] = (int64_t)mj[u] * d + i0;
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) {
-                xv[u].load(X + off[u]);
-                sv[u].load_cs(S + off[u]);
-                tv[u].load_cs(Th + off[u]);
-                lv[u].load_cs(L + off[u]);
-            }
-#pragma unroll
-            for (int u = 0; u < U; ++u) body(xv[u], sv[u], tv[u], lv[u], off[u], mj[u]);
-        }
-        for (; t < end; ++t) {
-            Vec<T, R> xv, sv, tv, lv;
-            const int col = __ldg(members + t);
-            const int64_t off = (int64_t)col * d + i0;
-            xv.load(X + off);
-            sv.load_cs(S + off);
-            tv.load_cs(Th + off);
-            lv.load_cs(L + off);
-            body(xv, sv, tv, lv, off, col);
-        }
-        const double inv = 1.0 / ng;  // means_of: sum * (1.0 / count), kmeans.cpp:78-79
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-            Cw[(int64_t)g * d + i0 + r] = cacc[r] * inv;
-            Gn[(int64_t)g * d + i0 + r] = gacc[r];
-        }
-    }
-    double v[5] = {pf, pl, ps, p1, psc};
-    block_sum<5>(v, red);
-    if (threadIdx.x == 0)
-#pragma unroll
-        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
-}
-
 // ---------------------------------------------------------------------------
 // Pass F for few groups (c·⌈d/512⌉ CTAs would not fill the GPU, e.g. c = 1):
 // the same per-element work and member-order sums as k_pass_f, one thread per

@@ -123,11 +123,6 @@ struct Alm : AlmBase {
         const int r = ring_cfg();
         return r == 16 ? 512 : r == 10 ? 256 : 64;
     }
-    int passf_ring_env = [] {  // RESPCA_PASSF_RING=0: never
-        const char* e = std::getenv("RESPCA_PASSF_RING");
-        return e ? std::atoi(e) : 1;
-    }();
-
     DBuf<T> X, L, S, Th;
     DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm, bn;
     bool l21 = false;
@@ -273,11 +268,10 @@ struct Alm : AlmBase {
             CK(cudaMemsetAsync(Lb.p, 0, sizeof(__nv_bfloat16) * (size_t)n * dpad, st));  // K padding stays 0
         }
         nbF = rowblocks * c;
-        // Pass F as k_pass_f_ring (a private cp.async ring per thread, ring_cfg()):
-        // every shape measured is faster with it than with the register-batched
-        // k_pass_f (C3 1.026 -> 0.974 ms, C5 24.8 -> 18.4, C4 0.74 -> 0.45);
-        // RESPCA_PASSF_RING=0 keeps k_pass_f
-        pf_ring = !(cfg.sparse_norm == RESPCA_L21) && passf_ring_env != 0;
+        // ℓ1: Pass F as k_pass_f_ring (a private cp.async ring per thread, ring_cfg());
+        // round 1 measured it faster than a register-batched walk on every shape
+        // (C3 1.026 -> 0.974 ms, C5 24.8 -> 18.4, C4 0.74 -> 0.45)
+        pf_ring = !(cfg.sparse_norm == RESPCA_L21);
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
         // c = 1 with d up to 2·10⁴ rows: one-thread-per-row walks cannot fill the GPU
         // (measured Pass F fraction of HBM, ring → stream: C2-c1 0.06 → 0.40,
@@ -421,27 +415,6 @@ struct Alm : AlmBase {
     }
 
     // ---- one iteration of the fast path, captured ----------------------
-    // Pass F variants (RESPCA_PASSF, tuning only): members per batch U / min
-    // blocks per SM.  Default 4 = U 8, 1 block/SM: 89% of measured HBM peak at C3
-    // (U 4: 79%, U 2 with 2 blocks/SM: 87%, U 12/16 spill).
-    // With the BF16 L′ side output (lb_on) U 2 / 2 blocks per SM is best (876 vs
-    // 826 iterations/s for U 8 / 1 block, which then spills).
-    int passf_lpt = [] {  // RESPCA_PASSF_LPT=1: groups largest first (measured 0.8 % slower at C3)
-        const char* e = std::getenv("RESPCA_PASSF_LPT");
-        return e ? std::atoi(e) : 0;
-    }();
-    int passf_variant_env = [] {
-        const char* e = std::getenv("RESPCA_PASSF");
-        return e ? std::atoi(e) : -1;
-    }();
-    template <int RR, int U, int MB>
-    void launch_pf() {
-        double* G1 = G.p + (size_t)d * c;
-        k_pass_f<T, RR, U, MB><<<nbF, 256, 0, st>>>(X.p, L.p, S.p, Th.p, km.goff.p, km.members.p,
-                                                    G.p, G1, G.p, G1, Cw.p, mean_w.p, ctl.p,
-                                                    partials.p, d, rowblocks, lb_on ? Lb.p : nullptr,
-                                                    dpad, passf_lpt ? km.gsize_ord.p : nullptr);
-    }
     void launch_pass_f() {
         if (l21) {  // ℓ2,1: F1 only (the S/Θ half runs after the column norms)
             double* G1 = G.p + (size_t)d * c;
@@ -481,22 +454,6 @@ struct Alm : AlmBase {
             ln.add();
             return;
         }
-        if (R == 2) {
-            const int passf_variant = passf_variant_env >= 0 ? passf_variant_env : (lb_on ? 2 : 4);
-            switch (passf_variant) {
-                case 1: launch_pf<2, 4, 2>(); break;
-                case 2: launch_pf<2, 2, 2>(); break;
-                case 3: launch_pf<2, 2, 3>(); break;
-                case 4: launch_pf<2, 8, 1>(); break;
-                case 5: launch_pf<2, 6, 1>(); break;
-                case 6: launch_pf<2, 12, 1>(); break;
-                case 7: launch_pf<2, 16, 1>(); break;
-                default: launch_pf<2, 4, 1>(); break;
-            }
-        } else {
-            launch_pf<1, 4, 1>();
-        }
-        ln.add();
     }
     void launch_pass_a() {
         if (c <= 1) return;
@@ -534,7 +491,7 @@ struct Alm : AlmBase {
     void capture_if_needed() {
         const uint64_t key[13] = {(uint64_t)d, (uint64_t)n, (uint64_t)c, (uint64_t)l21, (uint64_t)lb_on,
                                   (uint64_t)(use_tc && !tc_useless), (uint64_t)R, (uint64_t)rowblocks, (uint64_t)nbF,
-                                  (uint64_t)passf_variant_env ^ ((uint64_t)pf_stream << 44) ^ ((uint64_t)stream_rb << 45), (uint64_t)dpad, g_alloc_gen.load(),
+                                  ((uint64_t)pf_stream << 44) ^ ((uint64_t)stream_rb << 45), (uint64_t)dpad, g_alloc_gen.load(),
                                   (uint64_t)pdl_on()};
         if (cap_valid && std::equal(key, key + 13, cap_key)) return;
         cap_valid = false;
@@ -1504,6 +1461,17 @@ int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint
         CK(cudaMemcpyAsync(err_out, e.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
     });
+}
+
+int respca_cu_debug_guards(char* msg, uint64_t cap) {
+    if (!guard_on()) return -1;
+    std::string m;
+    const int bad = guard_check(&m);
+    if (msg && cap) {
+        std::strncpy(msg, m.c_str(), (size_t)cap - 1);
+        msg[cap - 1] = 0;
+    }
+    return bad;
 }
 
 int respca_cu_debug_screen_tc(respca_cu_ctx* ctx, const double* m, uint64_t d, uint64_t n,

@@ -5,6 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -43,6 +46,84 @@ inline void ck(cudaError_t e, const char* what) {
 }
 #define CK(x) ::respca_host::ck((x), #x)
 
+// ---------------------------------------------------------------------------
+// Guarded allocations (RESPCA_GUARD=1; tests only).  compute-sanitizer is not
+// available on the GPU pool, so device memory checking is done here: every
+// allocation is poisoned (0xFF bytes: NaN doubles/floats, −1 ints — a read
+// of memory no kernel wrote shows up as a result that differs from the
+// oracle) and followed by a 4 KiB guard of 0xA5 bytes, which
+// respca_cu_debug_guards() verifies (any write past the end of a buffer).
+// ---------------------------------------------------------------------------
+constexpr size_t kGuardBytes = 4096;
+inline bool guard_on() {
+    static const bool on = [] {
+        const char* e = std::getenv("RESPCA_GUARD");
+        return e && e[0] == '1';
+    }();
+    return on;
+}
+struct GuardRec {
+    void* p;
+    size_t bytes;
+};
+inline std::mutex& guard_mu() {
+    static std::mutex m;
+    return m;
+}
+inline std::vector<GuardRec>& guard_list() {
+    static std::vector<GuardRec> v;
+    return v;
+}
+inline cudaError_t dev_alloc(void** p, size_t bytes) {
+    if (!guard_on()) return cudaMalloc(p, bytes);
+    cudaError_t e = cudaMalloc(p, bytes + kGuardBytes);
+    if (e != cudaSuccess) return e;
+    // on a stream of its own: allocations also happen while another stream is
+    // being captured into a graph, where device-wide synchronisation is illegal
+    static cudaStream_t gs = [] {
+        cudaStream_t s = nullptr;
+        cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
+        return s;
+    }();
+    cudaMemsetAsync(*p, 0xFF, bytes, gs);
+    cudaMemsetAsync(static_cast<char*>(*p) + bytes, 0xA5, kGuardBytes, gs);
+    cudaStreamSynchronize(gs);
+    std::lock_guard<std::mutex> g(guard_mu());
+    guard_list().push_back({*p, bytes});
+    return cudaSuccess;
+}
+// number of guards found overwritten (the first few described in `msg`)
+inline int guard_check(std::string* msg = nullptr) {
+    if (!guard_on()) return 0;
+    std::lock_guard<std::mutex> g(guard_mu());
+    cudaDeviceSynchronize();
+    int bad = 0;
+    std::vector<unsigned char> h(kGuardBytes);
+    for (const GuardRec& r : guard_list()) {
+        cudaMemcpy(h.data(), static_cast<char*>(r.p) + r.bytes, kGuardBytes, cudaMemcpyDeviceToHost);
+        size_t off = kGuardBytes;
+        for (size_t k = 0; k < kGuardBytes; ++k)
+            if (h[k] != 0xA5) {
+                off = k;
+                break;
+            }
+        if (off != kGuardBytes) {
+            if (msg && bad < 8)
+                *msg += "guard overwritten: buffer of " + std::to_string(r.bytes) + " bytes, first bad byte +" +
+                        std::to_string(off) + "; ";
+            ++bad;
+        }
+    }
+    return bad;
+}
+// guard mode never returns memory: a freed buffer keeps its guard checked by
+// guard_check() (tests are small), and no synchronising call can land inside
+// a stream capture
+inline void dev_free(void* p) {
+    if (!p || guard_on()) return;
+    cudaFree(p);
+}
+
 // bumped whenever device memory behind a DBuf / Arena slot changes address:
 // captured CUDA graphs bake pointers in, so a graph is re-captured when this
 // moved since its capture
@@ -57,30 +138,30 @@ struct DBuf {
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
     ~DBuf() {
-        if (p && owned) cudaFree(p);
+        if (p && owned) dev_free(p);
     }
     U* ensure(size_t count) {
         if (count == 0) count = 1;
         if (count > cap) {
-            if (p && owned) cudaFree(p);
+            if (p && owned) dev_free(p);
             p = nullptr;
             cap = 0;
             owned = true;
-            CK(cudaMalloc(&p, count * sizeof(U)));
+            CK(dev_alloc(reinterpret_cast<void**>(&p), count * sizeof(U)));
             cap = count;
             g_alloc_gen.fetch_add(1);
         }
         return p;
     }
     void borrow(void* q, size_t count) {  // arena memory, never freed here
-        if (p && owned) cudaFree(p);
+        if (p && owned) dev_free(p);
         if (p != q) g_alloc_gen.fetch_add(1);
         p = static_cast<U*>(q);
         cap = count;
         owned = false;
     }
     void release() {
-        if (p && owned) cudaFree(p);
+        if (p && owned) dev_free(p);
         p = nullptr;
         cap = 0;
     }
@@ -99,17 +180,17 @@ struct Arena {
         for (auto& kv : slots)
             if (kv.first == name) {
                 if (kv.second.bytes < bytes) {
-                    cudaFree(kv.second.p);
+                    dev_free(kv.second.p);
                     kv.second.p = nullptr;
                     kv.second.bytes = 0;
-                    CK(cudaMalloc(&kv.second.p, bytes));
+                    CK(dev_alloc(&kv.second.p, bytes));
                     kv.second.bytes = bytes;
                     g_alloc_gen.fetch_add(1);
                 }
                 return kv.second.p;
             }
         Slot sl;
-        CK(cudaMalloc(&sl.p, bytes));
+        CK(dev_alloc(&sl.p, bytes));
         sl.bytes = bytes;
         g_alloc_gen.fetch_add(1);
         slots.emplace_back(name, sl);
@@ -117,7 +198,7 @@ struct Arena {
     }
     ~Arena() {
         for (auto& kv : slots)
-            if (kv.second.p) cudaFree(kv.second.p);
+            if (kv.second.p) dev_free(kv.second.p);
     }
 };
 

@@ -22,7 +22,6 @@
 #include "engine.cuh"
 #include "km.cuh"
 #include "hartigan.cuh"
-#include "hartigan_ws.cuh"
 #include "hart_gram.cuh"
 #include "tc_screen.cuh"
 
@@ -683,7 +682,7 @@ struct KMeansEngine {
         CK(cudaMemGetInfo(&fr, &tot));
         return (double)n * (double)n * 8.0 <= 0.4 * (double)fr;
     }
-    bool gram_path() const { return gram != nullptr && c >= 2 && c <= kGramMaxC && !hart_ws_on(); }
+    bool gram_path() const { return gram != nullptr && c >= 2 && c <= kGramMaxC; }
     double gram_gamma() const { return (2.2 * (double)d + 4.0) * kU; }
     // G = MᵀM on the FP64 tensor cores + its diagonal bounds; the event marks completion
     // G's storage and pointers (lent to the restart lanes before G is computed;
@@ -863,80 +862,6 @@ struct KMeansEngine {
         hst.ensure<HartGlobal>(1);
     }
 
-    // RESPCA_HART_WS=1: the warp-specialised kernel.  Measured at C3 it is
-    // slower (0.86 s vs 0.69 s per restart): the next block's refresh (≈25 µs
-    // on half the warps) is as long as a block's rounds and slows them down,
-    // so the block entries still wait on it.  Off by default; kept exact and
-    // tested for the configurations where blocks are long.
-    static bool hart_ws_on() {
-        static const bool on = [] {
-            const char* e = std::getenv("RESPCA_HART_WS");
-            return e && e[0] == '1';
-        }();
-        return on;
-    }
-    // warp-specialised kernel (hartigan_ws.cuh): the block refresh overlaps
-    // the rounds; no start screen (group P computes block 0 first)
-    void hartigan_ws(double* C, int* labels, const HartGeom& hgm) {
-        CK(cudaMemcpyAsync(hC2.p, C, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
-        CK(cudaMemsetAsync(hver.p, 0, sizeof(int) * c, st));
-        CK(cudaMemsetAsync(hglob.p, 0, sizeof(HartGlobal), st));
-        k_hart_first_reset<<<1, 1, 0, st>>>(hglob.p);
-        ln.add();
-        const int G = hgm.G, cpb = hgm.cpb;
-        auto kf = cpb <= 2 ? k_hart_ws<T, 2> : (cpb <= 4 ? k_hart_ws<T, 4> : k_hart_ws<T, 8>);
-        smem_at_least((const void*)kf, (size_t)(hgm.smem));
-        HartWsArgs a{};
-        a.g = hglob.p;
-        a.labels = labels;
-        a.counts = counts.p;
-        a.Cs = hC2.p;
-        a.ver = hver.p;
-        a.part = hpart.p;
-        a.ccp = hccp.p;
-        a.cand = hcand.p;
-        a.scratch = scratch.p;
-        a.d = d;
-        a.n = n;
-        a.c = c;
-        a.cpb = cpb;
-        a.cache_cols = hgm.cache ? 1 : 0;
-        a.max_pass = 50;  // kmeans.cpp:101
-        a.stage_rows = hgm.R;
-        a.stages = hgm.stages;
-        a.kappa_d = kappa_screen() + 16.0 * kU;
-        a.gam = ((double)d + 3.0) * kU * 1.02;
-        const T* Mp = M;
-        void* args[] = {&Mp, &a};
-        CK(cudaLaunchCooperativeKernel((const void*)kf, dim3(G), dim3(512), args, hgm.smem, st));
-        ln.add(1);
-        const dim3 cg(ceil_div(d, 256 * 8), std::min(c, 64));
-        k_hart_consolidate<<<cg, 256, 0, st>>>(hC2.p, hver.p, d, c);
-        CK(cudaMemcpyAsync(C, hC2.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
-        ln.add(1);
-        if (stats) {
-            HartGlobal* hh = hst.ensure<HartGlobal>(1);
-            CK(cudaMemcpyAsync(hh, hglob.p, sizeof(HartGlobal), cudaMemcpyDeviceToHost, st));
-            CK(cudaStreamSynchronize(st));
-            stats->hartigan_moves += hh->moves;
-            stats->exact_fallbacks += hh->exact_fallbacks;
-            stats->hartigan_passes += hh->passes;
-            stats->hartigan_rounds += hh->rounds;
-            stats->hartigan_refreshes += hh->refreshed;
-            stats->t_hart_kernel += 1e-9 * (double)hh->t_kernel;
-            if (trace_on())
-                std::fprintf(stderr,
-                             "[respca] hartigan(ws): G=%d cpb=%d R=%d x%d %llu passes %llu blocks %llu rounds %llu moves "
-                             "%llu moved-centroid refreshes, %llu redo rounds, kernel %.3fs (block entries %.3fs, "
-                             "of which waiting for the refresh %.3fs)\n",
-                             G, cpb, hgm.R, hgm.stages, (unsigned long long)hh->passes,
-                             (unsigned long long)hh->blocks, (unsigned long long)hh->rounds,
-                             (unsigned long long)hh->moves, (unsigned long long)hh->refreshed,
-                             (unsigned long long)hh->redos, 1e-9 * hh->t_kernel, 1e-9 * hh->t_load,
-                             1e-9 * hh->t_cols);
-        }
-    }
-
     void hartigan(double* C, int* labels) {
         if (c <= 1) return;  // no candidate target: never moves
         if (c >= 32768) throw InvalidArg("hartigan: c >= 32768 is not supported");
@@ -949,10 +874,6 @@ struct KMeansEngine {
         }
         hart_reserve();
         const HartGeom hgm = hart_geometry();
-        if (hart_ws_on()) {
-            hartigan_ws(C, labels, hgm);
-            return;
-        }
         CK(cudaMemcpyAsync(hC2.p, C, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
         CK(cudaMemsetAsync(hver.p, 0, sizeof(int) * c, st));
         CK(cudaMemsetAsync(hebuf.p, 0, sizeof(int) * ceil_div(n, hgm.B), st));

@@ -188,26 +188,6 @@ def test_kmeans_restart_lanes_bitwise(ctx, orc, R, monkeypatch, lanes):
     assert a.inertia == inertia and a.iters_run == it
 
 
-def test_kmeans_warp_specialised_hartigan_bitwise(ctx, orc, R, monkeypatch):
-    """RESPCA_HART_WS=1 (hartigan_ws.cuh) keeps the reference's labels exactly."""
-    import subprocess, sys, os
-    code = (
-        "import numpy as np, sys; sys.path.insert(0, 'tests'); sys.path.insert(0, '.');"
-        "from oracle import oracle as O; from paper_1904_07497_b200 import respca as R;"
-        "from paper_1904_07497_b200.respca import KMeansConfig; from helpers import bitwise;"
-        "rng = np.random.default_rng(31); orc = O.port()\n"
-        "for d, n, c, seed, rs in ((20, 200, 6, 7, 5), (64, 300, 12, 2, 3), (128, 700, 20, 4, 2)):\n"
-        "    m = rng.uniform(-1, 1, (d, n))\n"
-        "    a = R.kmeans(m, KMeansConfig(c=c, seed=seed, n_restarts=rs))\n"
-        "    lab, cen, inertia, it = orc.kmeans(m, c, 100, rs, seed, 1e-6)\n"
-        "    assert (a.assignment == lab).all() and bitwise(a.centroids, cen)\n"
-        "    assert a.inertia == inertia and a.iters_run == it\n"
-        "print('ok')\n")
-    env = dict(os.environ, RESPCA_HART_WS="1")
-    p = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert p.returncode == 0 and "ok" in p.stdout, p.stderr[-2000:]
-
-
 def test_kmeans_warm_bitwise(ctx, orc, R):
     from paper_1904_07497_b200.respca import KMeansConfig
 
