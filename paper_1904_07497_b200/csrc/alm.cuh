@@ -244,11 +244,14 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                 Vec<T, RW>::store(Th + off, a_t);
                 if (Lb) {
                     __nv_bfloat16* lb = Lb + (int64_t)col * dpad + i;
-                    if (RW == 2) {
-                        __nv_bfloat162 b2;
-                        b2.x = __double2bfloat16(ln[u][0]);
-                        b2.y = __double2bfloat16(ln[u][RW - 1]);
-                        *reinterpret_cast<__nv_bfloat162*>(lb) = b2;
+                    if (RW >= 2) {
+#pragma unroll
+                        for (int w = 0; w + 1 < RW; w += 2) {
+                            __nv_bfloat162 b2;
+                            b2.x = __double2bfloat16(ln[u][w]);
+                            b2.y = __double2bfloat16(ln[u][w + 1]);
+                            *reinterpret_cast<__nv_bfloat162*>(lb + w) = b2;
+                        }
                     } else {
                         lb[0] = __double2bfloat16(ln[u][0]);
                     }
@@ -939,6 +942,12 @@ __global__ void __launch_bounds__(256) k_exact_chains(const T* __restrict__ X, c
         __syncthreads();
     }
     if (threadIdx.x == 0) out[q] = acc;
+}
+
+// fp32 storage: the exact fp64 copy of X the one-time kmeans(X) runs on
+__global__ void k_widen(const float* __restrict__ src, double* __restrict__ dst, int64_t N) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < N; k += (int64_t)gridDim.x * blockDim.x)
+        dst[k] = (double)src[k];
 }
 
 // mean_w for the current ρ (after the host rebuilt the member lists).

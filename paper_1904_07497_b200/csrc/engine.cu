@@ -107,7 +107,8 @@ struct Alm : AlmBase {
     int ring_cfg() const {  // RESPCA_RING_CFG = 5, 10 or 16 (tuning)
         if (const char* e = std::getenv("RESPCA_RING_CFG")) {
             const int r = std::atoi(e);
-            if (r == 5 || ((r == 10 || r == 16) && d % 2 == 0)) return r;
+            if (r == 5 || ((r == 10 || r == 16) && d % 2 == 0) || ((r == 20 || r == 21) && sizeof(T) == 4 && d % 4 == 0))
+                return r;
         }
         // measured on B200 (fraction of the HBM copy bandwidth):
         //  5: a row per thread, 4-deep ring, 2-member batches — few groups (C5 0.755)
@@ -121,7 +122,7 @@ struct Alm : AlmBase {
     }
     int ring_nt() const {  // rows per CTA of the ring variant
         const int r = ring_cfg();
-        return r == 16 ? 512 : r == 10 ? 256 : 64;
+        return r == 16 || r == 20 || r == 21 ? 512 : r == 10 ? 256 : 64;
     }
     DBuf<T> X, L, S, Th;
     DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm, bn;
@@ -360,14 +361,36 @@ struct Alm : AlmBase {
         } else {
             const uint64_t restarts = std::max<uint64_t>(cfg.km_n_restarts, 5);
             double inertia = 0.0;
-            km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, &inertia,
-                      nullptr);
+            if constexpr (sizeof(T) == 4) {
+                // fp32 storage: kmeans(X) on an exact fp64 copy of X — the same values,
+                // so the same labels, but the FP64 tensor-core Gram and screens read
+                // doubles instead of widening every float in their inner loops
+                // (C3-f32 init 207 -> fp64's time)
+                const int64_t N = d * n;
+                double* Xd = static_cast<double*>(ctx->arena.get("Xd", sizeof(double) * N));
+                k_widen<<<std::min<int64_t>(4 * 148 * 8, ceil_div(N, 256)), 256, 0, st>>>(X.p, Xd, N);
+                ln.add();
+                KMeansEngine<double>& kd = Alm<double>::shared_engine(ctx);
+                kd.st = st;
+                kd.ln = ln;
+                kd.stats = &stats;
+                auto& pool = ctx->lanes[0];
+                if (!pool) pool.reset(new LanePool<double>());
+                kd.lane_pool = static_cast<LanePool<double>*>(pool.get());
+                kd.bind(Xd, d, n, c);
+                kd.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, &inertia, nullptr);
+                kd.fetch_labels(labels.p);
+                km.h_labels = kd.h_labels;
+            } else {
+                km.kmeans(cfg.km_max_iters, restarts, cfg.km_seed, cfg.km_tol, labels.p, Ck.p, &inertia,
+                          nullptr);
+            }
             // mean squared distance to the own centroid vs the scale (‖x‖+‖c‖)² ≈ 4‖x‖²
             // of the BF16 bound: below 1/32 its intervals straddle every decision
             tc_useless = !(inertia >= xnorm * xnorm * 4.0 / 32.0);
             if (tc_useless && lb_on) lb_on = false;
             tr("kmeans");
-            km.fetch_labels(labels.p);
+            if constexpr (sizeof(T) == 8) km.fetch_labels(labels.p);
         }
         labels0_h = km.h_labels;
         km.bind(L.p, d, n, c);  // from here on the p-update clusters L
@@ -446,7 +469,16 @@ struct Alm : AlmBase {
             };
             // the three configurations ring_cfg() chooses from (RESPCA_RING_CFG: the
             // tuning sweep's numbering, kept for reproducibility)
-            switch (ring_cfg()) {
+            const int rc = ring_cfg();
+            if constexpr (sizeof(T) == 4) {  // fp32 storage: four rows per thread, 16-byte copies
+                if (rc == 20 || rc == 21) {
+                    if (rc == 20) go(k_pass_f_ring<T, 8, 128, 1, 4>, 128, 8, 4);
+                    else go(k_pass_f_ring<T, 8, 128, 2, 4>, 128, 8, 4);
+                    ln.add();
+                    return;
+                }
+            }
+            switch (rc) {
                 case 10: go(k_pass_f_ring<T, 4, 128, 2, 2>, 128, 4, 2); break;
                 case 16: go(k_pass_f_ring<T, 8, 256, 4, 2>, 256, 8, 2); break;
                 default: go(k_pass_f_ring<T, 4, 64, 2>, 64, 4); break;
