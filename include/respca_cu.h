@@ -80,6 +80,23 @@ typedef struct {
                                residual chains (the tree-sum interval straddled tol) */
 } respca_cu_report;
 
+/* Decision margins of the last respca_cu_solve on a context (SURVEY.md
+ * Appendix A): how far each discrete decision of the reference sat from its
+ * threshold, so a run whose decisions come near reduction-order noise
+ * (~1e-14 relative) is visible.  Relative margins; +inf where a decision did
+ * not occur. */
+typedef struct {
+    double alm_stop;        /* min over iterations of |max(feas, dL, dS)/tol − 1|  (solver.cpp:197) */
+    double alm_stop_final;  /* the same at the last iteration */
+    double s_support;       /* min over iterations and entries of ||B| − 1/ρ|·ρ (ℓ1, solver.cpp:85);
+                               ℓ2,1: min over columns of |‖B_j‖ − 1/ρ|·ρ (solver.cpp:95) */
+    double lloyd_stop;      /* initial kmeans(X): min over Lloyd steps of |√moved − tol·√scale|/(tol·√scale)
+                               (kmeans.cpp:155) */
+    double restart_gap;     /* initial kmeans(X): (second smallest − smallest inertia)/smallest over the
+                               restarts (kmeans.cpp:246) */
+    uint64_t stop_resolves; /* stop tests decided on the reference's own chains */
+} respca_cu_margins;
+
 void respca_cu_default_config(respca_cu_config* cfg);
 
 /* Context: owns the device buffers, streams and CUDA graphs.  One context per
@@ -170,6 +187,9 @@ int respca_cu_debug_screen_tc(respca_cu_ctx* ctx, const double* m, uint64_t d, u
  * device memory, so every buffer ever allocated is checked), -1 when
  * RESPCA_GUARD is off; `msg` (may be NULL) describes the first ones. */
 int respca_cu_debug_guards(char* msg, uint64_t cap);
+
+/* Decision margins of the context's last solve (respca_cu_margins). */
+int respca_cu_last_margins(const respca_cu_ctx* ctx, respca_cu_margins* out);
 
 /* --- benchmark hooks (device-resident state, no host copies) ------------- */
 /* Upload X and run validation + the one-time initial clustering; leaves the

@@ -45,6 +45,13 @@ class CReport(C.Structure):
     ]
 
 
+class CMargins(C.Structure):
+    """respca_cu_margins — decision margins of the last solve."""
+
+    _fields_ = [("alm_stop", C.c_double), ("alm_stop_final", C.c_double), ("s_support", C.c_double),
+                ("lloyd_stop", C.c_double), ("restart_gap", C.c_double), ("stop_resolves", u64)]
+
+
 _lib = None
 _lock = threading.RLock()
 
@@ -58,7 +65,7 @@ EXPORTS = [
     "respca_cu_frob_norm", "respca_cu_elementwise_l1", "respca_cu_l21_norm",
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
     "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
-    "respca_cu_debug_screen_tc", "respca_cu_debug_guards", "respca_cu_binary_info", "respca_cu_solve_file",
+    "respca_cu_debug_screen_tc", "respca_cu_debug_guards", "respca_cu_last_margins", "respca_cu_binary_info", "respca_cu_solve_file",
     "respca_cu_outlier_scores", "respca_cu_synth_rpca",
 ]
 
@@ -111,6 +118,7 @@ def lib() -> C.CDLL:
             L.respca_cu_debug_screen.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             L.respca_cu_debug_screen_tc.argtypes = [vp, dptr, u64, u64, dptr, u64, dptr, dptr]
             L.respca_cu_debug_guards.argtypes = [C.c_char_p, u64]
+            L.respca_cu_last_margins.argtypes = [vp, C.POINTER(CMargins)]
             L.respca_cu_binary_info.argtypes = [C.c_char_p, u64ptr, u64ptr, C.c_char_p, C.c_size_t]
             L.respca_cu_solve_file.argtypes = [vp, C.c_char_p, C.c_int, C.POINTER(CConfig),
                                                C.c_char_p, C.c_char_p, u64ptr, u64, C.POINTER(CReport)]

@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const int beg = goff[g], end = goff[g + 1];
     const double ng = (double)(end - beg);
     const double mscale = own_w / ng + mw;
-    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
+    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0, smin = INFINITY;
     if (active) {
         double Gi[RW], mt[RW], cacc[RW], gacc[RW];
 #pragma unroll
@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
             // this thread's reads of the B slots are done before they refill
 #pragma unroll
             for (int u = 0; u < B; ++u) issue(t0 + U + u);
-            double ln[B][RW], sn[B][RW], tn[B][RW], rr[B][RW], sm[B][RW];
+            double ln[B][RW], sn[B][RW], tn[B][RW], rr[B][RW], sm[B][RW], mg[B][RW];
 #pragma unroll
             for (int u = 0; u < B; ++u)
 #pragma unroll
@@ -209,6 +209,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                     const double xl = x - ln[u][w];
                     const double b = xl + q;
                     const double mag = fabs(b) - thr;
+                    mg[u][w] = fabs(mag);
                     sn[u][w] = mag > 0.0 ? copysign(mag, b) : 0.0;
                     rr[u][w] = xl - sn[u][w];
                     tn[u][w] = th + rho * rr[u][w];
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                     p1 += fabs(sn[u][w]);
                     const double dm = ln[u][w] - mt[w];
                     psc += dm * dm;
+                    smin = fmin(smin, mg[u][w]);
                 }
                 double a_l[RW], a_s[RW], a_t[RW];
 #pragma unroll
@@ -267,9 +269,12 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     }
     double v[5] = {pf, pl, ps, p1, psc};
     block_sum<5>(v, red);
-    if (threadIdx.x == 0)
+    const double mn = block_min(smin, red);
+    if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * PF_STRIDE + q] = v[q];
+        partials[(int64_t)blockIdx.x * PF_STRIDE + 5] = mn;
+    }
 }
 
 template <typename T>
@@ -354,7 +359,7 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
     const int m = ge - gb;
     const int nst = (m + mps - 1) / mps;
     const double ng = (double)m;
-    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0;
+    double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0, smin = INFINITY;
     if (warp < 8) {
         // ================= element warps =================
         const double mscale = own_w / ng + mw;
@@ -440,6 +445,7 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
                     const double sn = mag > 0.0 ? copysign(mag, bb) : 0.0;
                     const double r = xl - sn;
                     const double tn = th + rho * r;
+                    if (ok) smin = fmin(smin, fabs(mag));
                     // summand layout [2][member][row of the block]
                     const int e = cmem[j] * rb_rows + csub[j] * VEC + v;
                     sm_[e] = ln;
@@ -512,9 +518,12 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
     }
     double pv[5] = {pf, pl, ps, p1, psc};
     block_sum<5>(pv, red);
-    if (tid == 0)
+    const double mn = block_min(smin, red);
+    if (tid == 0) {
 #pragma unroll
-        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = pv[q];
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * PF_STRIDE + q] = pv[q];
+        partials[(int64_t)blockIdx.x * PF_STRIDE + 5] = mn;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -577,9 +586,11 @@ __global__ void __launch_bounds__(256) k_pass_f1(
     }
     double v[5] = {0.0, pl, 0.0, 0.0, psc};
     block_sum<5>(v, red);
-    if (threadIdx.x == 0)
+    if (threadIdx.x == 0) {
 #pragma unroll
-        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * 5 + q] = v[q];
+        for (int q = 0; q < 5; ++q) partials[(int64_t)blockIdx.x * PF_STRIDE + q] = v[q];
+        partials[(int64_t)blockIdx.x * PF_STRIDE + 5] = INFINITY;  // ℓ2,1: k_l21_term's column margin
+    }
 }
 
 // ‖B_j‖ for the ℓ2,1 shrinkage: exact sequential chain per column, warp-
@@ -674,8 +685,8 @@ __global__ void __launch_bounds__(256) k_pass_f2(
     double v[2] = {pf, ps};
     block_sum<2>(v, red);
     if (threadIdx.x == 0) {
-        partials[(int64_t)blockIdx.x * 5 + 0] += v[0];
-        partials[(int64_t)blockIdx.x * 5 + 2] += v[1];
+        partials[(int64_t)blockIdx.x * PF_STRIDE + 0] += v[0];
+        partials[(int64_t)blockIdx.x * PF_STRIDE + 2] += v[1];
     }
 }
 
@@ -684,14 +695,19 @@ __global__ void k_l21_term(const double* __restrict__ bn, int64_t n, Ctl* __rest
     __shared__ double red[32];
     if (ctl->done) return;
     const double thr = ctl->thr;
-    double s = 0.0;
+    double s = 0.0, mn = INFINITY;
     for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
         const double nr = bn[j];
         if (!(nr <= thr)) s += (1.0 - thr / nr) * nr;
+        mn = fmin(mn, fabs(nr - thr));  // the column's support decision margin (solver.cpp:95)
     }
     double v[1] = {s};
     block_sum<1>(v, red);
-    if (threadIdx.x == 0) ctl->sparse_term = v[0];
+    mn = block_min(mn, red);
+    if (threadIdx.x == 0) {
+        ctl->sparse_term = v[0];
+        ctl->l21_smin = mn;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -803,7 +819,8 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
                                                    int nparts, const int* __restrict__ goff,
                                                    double* __restrict__ mean_w, int c,
                                                    double* __restrict__ rep, int has_cond,
-                                                   cudaGraphConditionalHandle cond) {
+                                                   cudaGraphConditionalHandle cond,
+                                                   double* __restrict__ marg) {
     __shared__ double red[32 * 5];
     pdl_enter();
     if (ctl->done) {
@@ -811,10 +828,14 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
         return;
     }
     double v[5] = {0, 0, 0, 0, 0};
-    for (int b = threadIdx.x; b < nparts; b += blockDim.x)
+    double mn = INFINITY;
+    for (int b = threadIdx.x; b < nparts; b += blockDim.x) {
 #pragma unroll
-        for (int q = 0; q < 5; ++q) v[q] += partials[(int64_t)b * 5 + q];
+        for (int q = 0; q < 5; ++q) v[q] += partials[(int64_t)b * PF_STRIDE + q];
+        mn = fmin(mn, partials[(int64_t)b * PF_STRIDE + 5]);
+    }
     block_sum<5>(v, red);
+    mn = block_min(mn, red);
     __shared__ int s_done;
     if (threadIdx.x == 0) {
         Ctl& k = *ctl;
@@ -835,6 +856,8 @@ __global__ void __launch_bounds__(1024) k_finalize(Ctl* __restrict__ ctl,
         rep[(int64_t)t * 4 + 1] = dl;
         rep[(int64_t)t * 4 + 2] = ds;
         rep[(int64_t)t * 4 + 3] = obj;
+        // S-support margin of iteration t: min ||B| − 1/ρ|·ρ (solver.cpp:85 / 95)
+        marg[t] = (k.l21 ? fmin(mn, k.l21_smin) : mn) / k.thr;
         if (!isfinite(feas) || !isfinite(dl) || !isfinite(ds)) k.nonfinite = 1;
         double mx = feas;  // std::max({feas, dl, ds})
         if (mx < dl) mx = dl;

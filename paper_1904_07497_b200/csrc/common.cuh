@@ -57,7 +57,30 @@ struct Ctl {
     int stop_amb;     // the stop test of the last finalized iteration was undecidable
     double sum_eps;   // relative bound |chain − tree| ≤ sum_eps·tree (rounded up)
     double xn_lo, xn_hi;  // bounds on the reference's ‖X‖ (= xnorm once it is the chain value)
+    double l21_smin;      // ℓ2,1: min over columns of |‖B_j‖ − 1/ρ| (k_l21_term)
 };
+
+// Pass F partials per CTA: Σ feas², Σ dL², Σ dS², Σ|S|, Σ scatter, and the
+// minimum over the CTA's elements of ||B| − 1/ρ| (the S-support margin)
+constexpr int PF_STRIDE = 6;
+
+RESPCA_DEV double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+// block minimum (all threads get it); `red` holds ≥ 32 doubles
+RESPCA_DEV double block_min(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nw = (blockDim.x + 31) >> 5;
+    v = warp_min(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    v = warp_min(lane < nw ? red[lane] : INFINITY);
+    __syncthreads();
+    return v;
+}
 
 RESPCA_DEV double warp_sum(double v) {
 #pragma unroll

@@ -43,6 +43,7 @@ struct respca_cu_ctx {
     std::unique_ptr<PoolBase> lanes[2];  // k-means restart lanes (fp64, fp32 storage)
     std::unique_ptr<PoolBase> engines[2];  // solve()'s k-means engine (fp64, fp32 storage)
     std::unique_ptr<AlmBase> solver[2];    // solve()'s ALM state + captured graphs, reused
+    respca_cu_margins margins{};          // decision margins of the last solve
 };
 
 namespace {
@@ -125,7 +126,7 @@ struct Alm : AlmBase {
         return r == 16 || r == 20 || r == 21 ? 512 : r == 10 ? 256 : 64;
     }
     DBuf<T> X, L, S, Th;
-    DBuf<double> G, Cw, Ck, mean_w, partials, rep, nrm, bn;
+    DBuf<double> G, Cw, Ck, mean_w, partials, rep, marg, nrm, bn;
     bool l21 = false;
     DBuf<int> labels, labels_new;
     DBuf<Ctl> ctl;
@@ -134,6 +135,7 @@ struct Alm : AlmBase {
     WhileGraph wg;
     PlainGraph rest;
     double init_ms = 0.0, xnorm = 0.0, xsq_tree = 0.0;
+    double m_lloyd = INFINITY, m_gap = INFINITY;  // initial kmeans(X) decision margins
     // exact ALM stop (resolve_stop): the start of the loop it replays from, and
     // ‖X‖ as the reference's chain once computed
     Ctl ctl0{};
@@ -258,6 +260,7 @@ struct Alm : AlmBase {
         labels.ensure(n);
         labels_new.ensure(n);
         rep.ensure(std::max<uint64_t>(budget, 1) * 4);
+        marg.ensure(std::max<uint64_t>(budget, 1));
         ctl.ensure(1);
         R = (d % 2 == 0) ? 2 : 1;
         rowblocks = ceil_div(d, 256 * R);
@@ -305,7 +308,7 @@ struct Alm : AlmBase {
             stream_nrb = (int)ceil_div(d, (int64_t)stream_rb);
             nbP = c * stream_nrb;
         }
-        partials.ensure((size_t)std::max(nbF, nbP) * 5);
+        partials.ensure((size_t)std::max(nbF, nbP) * PF_STRIDE);
         Ctl h{};
         h.rho = cfg.rho0;
         const double rn = cfg.rho0 * cfg.kappa;
@@ -387,6 +390,24 @@ struct Alm : AlmBase {
             }
             // mean squared distance to the own centroid vs the scale (‖x‖+‖c‖)² ≈ 4‖x‖²
             // of the BF16 bound: below 1/32 its intervals straddle every decision
+            {  // decision margins of the initial clustering
+                const KMeansEngine<double>* kk = nullptr;
+                if constexpr (sizeof(T) == 4) kk = &Alm<double>::shared_engine(ctx);
+                const double lm = kk ? kk->lloyd_margin : km.lloyd_margin;
+                const std::vector<double>& ri = kk ? kk->restart_inertia : km.restart_inertia;
+                double b1 = INFINITY, b2 = INFINITY;
+                for (double v : ri) {
+                    if (!(v == v)) continue;
+                    if (v < b1) {
+                        b2 = b1;
+                        b1 = v;
+                    } else if (v < b2) {
+                        b2 = v;
+                    }
+                }
+                m_lloyd = lm;
+                m_gap = (b2 < INFINITY && b1 > 0.0) ? (b2 - b1) / b1 : INFINITY;
+            }
             tc_useless = !(inertia >= xnorm * xnorm * 4.0 / 32.0);
             if (tc_useless && lb_on) lb_on = false;
             tr("kmeans");
@@ -511,7 +532,7 @@ struct Alm : AlmBase {
     }
     void launch_finalize(bool cond) {
         CK(pdl_launch(k_finalize, dim3(1), dim3(1024), 0, st, ctl.p, partials.p, l21 ? nbF : nbP, km.goff.p,
-                      mean_w.p, c, rep.p, cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{}));
+                      mean_w.p, c, rep.p, cond ? 1 : 0, cond ? wg.handle : cudaGraphConditionalHandle{}, marg.p));
         ln.add();
     }
     int kernels_per_iter() const { return 1 + (c > 1 ? 2 + km.decide_kernels() : 0) + 1 + (l21 ? 3 : 0); }
@@ -563,6 +584,7 @@ struct Alm : AlmBase {
     // slow path: the p-update changed labels (or a Hartigan move) in the last
     // finalized iteration t → finish kmeans_warm exactly, refresh groups, G.
     void slow_path(Ctl& h) {
+        Nvtx r_("ALM slow path (kmeans_warm)");
         const int t = h.iter - 1;
         CK(cudaMemcpyAsync(Ck.p, Cw.p, sizeof(double) * d * c, cudaMemcpyDeviceToDevice, st));
         km.h_labels.resize(n);
@@ -652,6 +674,7 @@ struct Alm : AlmBase {
         }
     }
     void resolve_stop(Ctl& h) {
+        Nvtx r_("exact ALM stop (replay + chains)");
         const int t = h.iter - 1;
         const int64_t N = d * n;
         const Stats s0 = stats;
@@ -748,11 +771,36 @@ struct Alm : AlmBase {
         sinkS(S.p);
         std::vector<int> hl(n);
         CK(cudaMemcpyAsync(hl.data(), labels.p, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-        std::vector<double> hr((size_t)h.iter * 4 + 4);
-        if (h.iter > 0)
+        std::vector<double> hr((size_t)h.iter * 4 + 4), hm((size_t)h.iter + 1);
+        if (h.iter > 0) {
             CK(cudaMemcpyAsync(hr.data(), rep.p, sizeof(double) * 4 * h.iter,
                                cudaMemcpyDeviceToHost, st));
+            CK(cudaMemcpyAsync(hm.data(), marg.p, sizeof(double) * h.iter, cudaMemcpyDeviceToHost, st));
+        }
         CK(cudaStreamSynchronize(st));
+        {
+            respca_cu_margins& mg = ctx->margins;
+            mg = respca_cu_margins{};
+            mg.alm_stop = mg.alm_stop_final = mg.s_support = INFINITY;
+            for (int t = 0; t < h.iter; ++t) {
+                const double mx = std::max({hr[(size_t)t * 4], hr[(size_t)t * 4 + 1], hr[(size_t)t * 4 + 2]});
+                const double am = std::fabs(mx / cfg.tol - 1.0);
+                if (!cfg.has_fixed_iters) {
+                    mg.alm_stop = std::min(mg.alm_stop, am);
+                    if (t + 1 == h.iter) mg.alm_stop_final = am;
+                }
+                mg.s_support = std::min(mg.s_support, hm[(size_t)t]);
+            }
+            mg.lloyd_stop = c > 1 ? m_lloyd : INFINITY;
+            mg.restart_gap = c > 1 ? m_gap : INFINITY;
+            mg.stop_resolves = stop_resolves;
+            if (trace_on())
+                std::fprintf(stderr,
+                             "[respca] margins: ALM stop %.3g (final %.3g), S support %.3g, Lloyd stop %.3g, "
+                             "restart gap %.3g, %llu stop test(s) on the chains\n",
+                             mg.alm_stop, mg.alm_stop_final, mg.s_support, mg.lloyd_stop, mg.restart_gap,
+                             (unsigned long long)mg.stop_resolves);
+        }
         for (int j = 0; j < n; ++j) lab[j] = (uint64_t)hl[j];
         if (rep_out) {
             for (int t = 0; t < h.iter; ++t) {
@@ -784,6 +832,13 @@ struct Alm : AlmBase {
                                    cudaMemcpyDeviceToDevice, st));
             std::swap(rep.p, nr.p);
             std::swap(rep.cap, nr.cap);
+            DBuf<double> nm;
+            nm.ensure(budget);
+            if (h.iter > 0)
+                CK(cudaMemcpyAsync(nm.p, marg.p, sizeof(double) * h.iter, cudaMemcpyDeviceToDevice, st));
+            std::swap(marg.p, nm.p);
+            std::swap(marg.cap, nm.cap);
+            CK(cudaStreamSynchronize(st));  // the old buffers are freed below
             capture();
         }
         h.budget = (int)(h.iter + iters);
@@ -870,30 +925,43 @@ void solve_core(respca_cu_ctx* ctx, uint64_t d, uint64_t n, const respca_cu_conf
     }
     Alm<T>& a = *static_cast<Alm<T>*>(slot.get());
     a.begin_solve();
+    Nvtx r_solve("respca::solve");
     Events ev;
     CK(cudaEventRecord(ev.a, ctx->st));
-    a.upload_with(d, n, cfg, fill);
+    {
+        Nvtx r("upload + validate");
+        a.upload_with(d, n, cfg, fill);
+    }
     CK(cudaEventRecord(ev.b, ctx->st));
     CK(cudaEventSynchronize(ev.b));
     const double h2d = ev.ms();
     Events e2;
     CK(cudaEventRecord(e2.a, ctx->st));
-    a.setup_state();
-    a.init_labels();
-    a.launch_group_D();
+    {
+        Nvtx r("initial kmeans(X)");
+        a.setup_state();
+        a.init_labels();
+        a.launch_group_D();
+    }
     CK(cudaEventRecord(e2.b, ctx->st));
     CK(cudaEventSynchronize(e2.b));
     const double init_ms = e2.ms();
     a.capture_if_needed();
     Events e3;
     CK(cudaEventRecord(e3.a, ctx->st));
-    a.run_loop();
+    {
+        Nvtx r("ALM loop");
+        a.run_loop();
+    }
     CK(cudaEventRecord(e3.b, ctx->st));
     CK(cudaEventSynchronize(e3.b));
     const double loop_ms = e3.ms();
     Events e4;
     CK(cudaEventRecord(e4.a, ctx->st));
-    a.download_with(sinkL, sinkS, lab, rep);
+    {
+        Nvtx r("download");
+        a.download_with(sinkL, sinkS, lab, rep);
+    }
     CK(cudaEventRecord(e4.b, ctx->st));
     CK(cudaEventSynchronize(e4.b));
     if (rep) {
@@ -1493,6 +1561,12 @@ int respca_cu_debug_screen(respca_cu_ctx* ctx, const double* m, uint64_t d, uint
         CK(cudaMemcpyAsync(err_out, e.p, sizeof(double) * n * c, cudaMemcpyDeviceToHost, ctx->st));
         CK(cudaStreamSynchronize(ctx->st));
     });
+}
+
+int respca_cu_last_margins(const respca_cu_ctx* ctx, respca_cu_margins* out) {
+    if (!ctx || !out) return RESPCA_EINVAL;
+    *out = ctx->margins;
+    return RESPCA_OK;
 }
 
 int respca_cu_debug_guards(char* msg, uint64_t cap) {

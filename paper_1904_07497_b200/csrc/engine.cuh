@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "respca_cu.h"
+#include <nvtx3/nvToolsExt.h>
 
 namespace respca_host {
 
@@ -243,6 +244,14 @@ struct Events {
         CK(cudaEventElapsedTime(&t, a, b));
         return t;
     }
+};
+
+// NVTX range for profilers (nsys / ncu --nvtx): solve phases, k-means phases
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+    Nvtx(const Nvtx&) = delete;
+    Nvtx& operator=(const Nvtx&) = delete;
 };
 
 // A graph whose body runs while the device keeps a conditional handle set.

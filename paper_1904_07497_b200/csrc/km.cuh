@@ -443,11 +443,7 @@ RESPCA_DEV void warp_argmin(double& v, int& k) {
         }
     }
 }
-RESPCA_DEV double warp_min(double v) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
-    return v;
-}
+// warp_min: common.cuh
 
 // Decision status of one column
 enum : int { ST_STABLE = 0, ST_CHANGED = 1, ST_MOVE = 2, ST_AMBIG = 3 };

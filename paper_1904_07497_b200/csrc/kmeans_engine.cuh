@@ -497,6 +497,7 @@ struct KMeansEngine {
         };
         double margin;
         bool v = verdict(h[0], h[1], margin);
+        lloyd_margin = std::min(lloyd_margin, margin);
         if (margin < 1e-9 && h[0] != 0.0) {  // too close for a tree sum: reference chain
             if (trace_on())
                 std::fprintf(stderr, "[respca] lloyd stop: exact chain (moved %.17g scale %.17g margin %.3g)\n", h[0],
@@ -509,6 +510,11 @@ struct KMeansEngine {
         }
         return v;
     }
+
+    // decision margins of the last kmeans(): the Lloyd stop
+    // test's relative distance to its threshold, and every restart's inertia
+    double lloyd_margin = INFINITY;
+    std::vector<double> restart_inertia;
 
     // lloyd_run (kmeans.cpp:141-168).  C: in = start centroids, out = final
     // means; labels: device out.  Returns iters_run.
@@ -1145,6 +1151,8 @@ struct KMeansEngine {
         if (c == 0) throw InvalidArg("kmeans: c must be >= 1");
         if ((int64_t)c > n) throw InvalidArg("kmeans: c exceeds column count");
         const int L = lanes_for(n_restarts);
+        lloyd_margin = INFINITY;
+        restart_inertia.assign(n_restarts, std::numeric_limits<double>::quiet_NaN());
         struct GramScope {
             KMeansEngine* e;
             ~GramScope() { e->drop_gram(); }
@@ -1170,6 +1178,7 @@ struct KMeansEngine {
                 const uint64_t it = lloyd_run(cen.p, lab.p, max_iters, tol);
                 const auto ti = HClock::now();
                 const double in = inertia(cen.p, lab.p);
+                restart_inertia[r] = in;
                 if (stats) stats->t_inertia += since(ti);
                 if (in < best) {  // kmeans.cpp:246
                     best = in;
@@ -1253,6 +1262,7 @@ struct KMeansEngine {
             ln_.e.stats = stats ? &ln_.st : nullptr;
             ln_.e.hart_ctas = std::max(1, nsm / L);
             ln_.e.bind(M, d, n, c);
+            ln_.e.lloyd_margin = INFINITY;
             lend_gram(ln_.e);
             // every buffer a lane touches is allocated before the lanes run
             // (cudaFree would synchronise the device under them)
@@ -1296,6 +1306,7 @@ struct KMeansEngine {
         if (n_restarts > 1 && env_int("RESPCA_PP_JOINT", 1) != 0) {
             const auto tj = HClock::now();
             joint_eng.assign(spec.begin(), spec.begin() + (size_t)std::min<uint64_t>(n_restarts, 8));
+            Nvtx r_pp("k-means++ seeding (joint)");
             joint_chosen = pp_joint(joint_eng);
             if (stats) stats->t_pp += since(tj);
         }
@@ -1382,9 +1393,14 @@ struct KMeansEngine {
                     e.gather(chosen, ln_.wc.p);
                     if (e.stats) e.stats->t_pp += since(tp);
                     const double t_pp_end = since(t_k0);
+                    Nvtx r_lane("restart: lloyd + hartigan");
                     const uint64_t it = e.lloyd_run(ln_.wc.p, ln_.wl.p, max_iters, tol);
                     const auto ti = HClock::now();
                     const double in = e.inertia(ln_.wc.p, ln_.wl.p);
+                    {
+                        std::lock_guard<std::mutex> g(mu);
+                        restart_inertia[r] = in;
+                    }
                     if (e.stats) e.stats->t_inertia += since(ti);
                     if (trace_on())
                         std::fprintf(stderr, "[respca] lane %d restart %llu: seeded at %.3fs, done at %.3fs (lloyd %.3fs, hartigan %.3fs)\n", l,
@@ -1415,6 +1431,7 @@ struct KMeansEngine {
         for (int l = 0; l < L; ++l) {
             auto& lp = lanes[l];
             *ln.counter += lp->launches;
+            lloyd_margin = std::min(lloyd_margin, lp->e.lloyd_margin);
             if (stats) {
                 const Stats& s2 = lp->st;
                 stats->hartigan_moves += s2.hartigan_moves;

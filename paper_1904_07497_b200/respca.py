@@ -101,6 +101,7 @@ class DecompositionResult:
     hartigan_moves: int = 0
     exact_fallbacks: int = 0
     stop_resolves: int = 0  # stop tests decided on the reference's sequential residual chains
+    margins: Optional[dict] = None  # decision margins, see last_margins()
 
 
 @dataclass
@@ -176,7 +177,18 @@ def solve(x, cfg: Optional[SolverConfig] = None, precision: str = "f64",
     return DecompositionResult(L, S, lab, report, float(rep.wall_time), float(rep.lambda_),
                                float(rep.init_ms), float(rep.loop_ms), float(rep.h2d_ms),
                                float(rep.d2h_ms), int(rep.slow_iters), int(rep.hartigan_moves),
-                               int(rep.exact_fallbacks), int(rep.stop_resolves))
+                               int(rep.exact_fallbacks), int(rep.stop_resolves), last_margins(ctx))
+
+
+def last_margins(ctx=None) -> dict:
+    """Decision margins of the context's last solve (respca_cu_margins,
+    SURVEY.md Appendix A): relative distance of each discrete decision of the
+    reference from its threshold; inf where the decision did not occur."""
+    ctx = _ctx(ctx)
+    m = N.CMargins()
+    N.check(ctx, N.lib().respca_cu_last_margins(ctx.handle, C.byref(m)))
+    return {k: (int(getattr(m, k)) if k == "stop_resolves" else float(getattr(m, k)))
+            for k, _ in N.CMargins._fields_}
 
 
 def _result(L, S, lab, arrs, rep) -> DecompositionResult:

@@ -150,3 +150,51 @@ def test_tiny_magnitudes_bitwise(ctx, orc):
         assert a.report.iters == b.iters
         assert (a.assignment == b.labels).all()
         assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
+
+
+def _replay_support_margin(orc, X, c, lam, iters, tol=None):
+    """The reference loop replayed with the oracle's building blocks
+    (solver.cpp:157-201), returning min over iterations and entries of
+    ||B| − 1/ρ|·ρ and the per-iteration max residuals."""
+    d, n = X.shape
+    labels = orc.kmeans(X, c, 100, 5, 0, 1e-6)[0]
+    L = X.copy(order="F")
+    S = np.zeros_like(X, order="F")
+    Th = np.zeros_like(X, order="F")
+    rho, best = 1e-4, np.inf
+    for _ in range(iters):
+        D = (X - S) + Th / rho
+        L = orc.l_update(D, labels, c, lam, rho)
+        labels = orc.kmeans_warm(L, c, labels)[0]
+        B = (X - L) + Th / rho
+        t = 1.0 / rho
+        best = min(best, float(np.min(np.abs(np.abs(B) - t))) / t)
+        S = orc.s_update_l1(B, t)
+        Th, rho = orc.multiplier_update(Th, X, L, S, rho, 1.5)
+    return best
+
+
+def test_decision_margins(ctx, orc):
+    """respca_cu_last_margins: the S-support margin equals
+    the one a replay of the reference loop with the oracle's own building
+    blocks measures, bit for bit; the ALM-stop margin is |max(report)/tol − 1|;
+    the initial-clustering margins are reported."""
+    from paper_1904_07497_b200 import synth
+    from paper_1904_07497_b200.respca import SolverConfig
+
+    X = synth.rpca(48, 72, 3, 1.0, 0.06, seed=9)
+    lam = 0.7
+    res = _solve(ctx, X, SolverConfig(c=4, lambda_=lam, fixed_iters=12))
+    m = res.margins
+    ref = _replay_support_margin(orc, X, 4, lam, 12)
+    assert m["s_support"] == ref, (m["s_support"], ref)
+    assert m["alm_stop"] == np.inf  # fixed_iters: no stop test
+    assert 0.0 <= m["restart_gap"] < np.inf and 0.0 < m["lloyd_stop"] < np.inf
+    case = load("solve_C1.json")
+    res = _solve(ctx, make_x(case), cfg_from(case["config"]))
+    m = res.margins
+    mx = max(res.report.feas[-1], res.report.delta_l[-1], res.report.delta_s[-1])
+    assert m["alm_stop_final"] == abs(mx / case["config"]["tol"] - 1.0)
+    assert 1e-9 < m["alm_stop"] <= m["alm_stop_final"]
+    assert 0.0 < m["s_support"] < 1.0 and m["stop_resolves"] == 0
+    print("\nC1 margins:", m)
