@@ -136,6 +136,8 @@ struct Alm : AlmBase {
     PlainGraph rest;
     double init_ms = 0.0, xnorm = 0.0, xsq_tree = 0.0;
     double m_lloyd = INFINITY, m_gap = INFINITY;  // initial kmeans(X) decision margins
+    // (column end, event) per uploaded chunk of X, recorded by a chunked fill
+    std::vector<std::pair<int64_t, cudaEvent_t>> chunk_events;
     // exact ALM stop (resolve_stop): the start of the loop it replays from, and
     // ‖X‖ as the reference's chain once computed
     Ctl ctl0{};
@@ -177,6 +179,7 @@ struct Alm : AlmBase {
         km.st = st;
         km.ln = ln;
         km.stats = &stats;
+        km.gram_early = false;
     }
     static KMeansEngine<T>& shared_engine(respca_cu_ctx* cx) {
         auto& h = cx->engines[sizeof(T) == 8 ? 0 : 1];
@@ -232,6 +235,17 @@ struct Alm : AlmBase {
         }
         fill(X.p);
         const int blocks = std::min<int64_t>(2048, ceil_div(N, 256));
+        // the initial clustering's Gram matrix starts on its own stream while X
+        // is still arriving (the fill recorded chunk events), before the
+        // validation below synchronises
+        if constexpr (sizeof(T) == 8) {
+            const char* ge = std::getenv("RESPCA_GRAM_EARLY");  // =0: G after the upload (round 1)
+            if (!chunk_events.empty() && c > 1 && !(ge && ge[0] == '0')) {
+                km.bind(X.p, d, n, c);
+                if (km.gram_fits()) km.compute_gram_banded(chunk_events);
+            }
+        }
+        chunk_events.clear();
         nrm.ensure(3 * 2048 + 8);
         k_norms<T><<<blocks, 256, 0, st>>>(X.p, N, nrm.p);
         k_sum_partials<<<1, 256, 0, st>>>(nrm.p, blocks, 3, nrm.p + 3 * 2048);
@@ -982,9 +996,35 @@ void solve_impl(respca_cu_ctx* ctx, const T* x, uint64_t d, uint64_t n,
                 respca_cu_report* rep) {
     const size_t N = (size_t)(d * n);
     cudaStream_t st = ctx->st;
+    // X in column chunks (multiples of the Gram tile), an event after each: the
+    // initial clustering's Gram matrix starts on the first chunks while the rest
+    // are still crossing the host link
+    std::vector<cudaEvent_t> evs;
+    struct EvGuard {
+        std::vector<cudaEvent_t>& v;
+        ~EvGuard() {
+            for (cudaEvent_t e : v) cudaEventDestroy(e);
+        }
+    } evg{evs};
     solve_core<T>(
         ctx, d, n, cfg,
-        [&](T* X) { CK(cudaMemcpyAsync(X, x, sizeof(T) * N, cudaMemcpyHostToDevice, st)); },
+        [&](T* X) {
+            Alm<T>& a = *static_cast<Alm<T>*>(ctx->solver[sizeof(T) == 8 ? 0 : 1].get());
+            const int64_t blk = 128, nchunk = (n >= 8 * blk && cfg.c > 1) ? 8 : 1;
+            const int64_t per = ((int64_t)n / nchunk + blk - 1) / blk * blk;
+            for (int64_t j0 = 0; j0 < (int64_t)n; j0 += per) {
+                const int64_t j1 = std::min<int64_t>(n, j0 + per);
+                CK(cudaMemcpyAsync(X + (size_t)j0 * d, x + (size_t)j0 * d, sizeof(T) * (size_t)(j1 - j0) * d,
+                                   cudaMemcpyHostToDevice, st));
+                if (nchunk > 1) {
+                    cudaEvent_t e;
+                    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    evs.push_back(e);
+                    CK(cudaEventRecord(e, st));
+                    a.chunk_events.emplace_back(j1, e);
+                }
+            }
+        },
         [&](const T* L) { CK(cudaMemcpyAsync(Lo, L, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); },
         [&](const T* S) { CK(cudaMemcpyAsync(So, S, sizeof(T) * N, cudaMemcpyDeviceToHost, st)); }, lab, rep);
 }

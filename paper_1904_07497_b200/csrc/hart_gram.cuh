@@ -50,7 +50,7 @@ size_t gram_smem() {
 
 template <typename T>
 __global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_t d, int n,
-                                                 double* __restrict__ G, long long ntiles) {
+                                                 double* __restrict__ G, long long ntiles, long long t0 = 0) {
     extern __shared__ __align__(16) unsigned char sm[];
     T* As = reinterpret_cast<T*>(sm);        // [ST][128][AS]  columns i0.. (rows of A)
     T* Bs = As + GR_ST * GR_T * GR_AS;       // [ST][128][AS]  columns j0..
@@ -60,7 +60,9 @@ __global__ void __launch_bounds__(256, 1) k_gram(const T* __restrict__ M, int64_
     const int wr = warp >> 2, wc = warp & 3;
     // a grid smaller than the tile count loops over tiles (G can then share
     // the GPU with the restarts' seeding and Lloyd steps)
-    for (long long tix = blockIdx.x; tix < ntiles; tix += gridDim.x) {
+    // tiles [t0, ntiles) of the row-major lower triangle (a band of block rows
+    // when G is computed while X is still arriving)
+    for (long long tix = t0 + blockIdx.x; tix < ntiles; tix += gridDim.x) {
     __syncthreads();  // the previous tile's stages are free
     int bi = (int)((sqrt(8.0 * (double)tix + 1.0) - 1.0) * 0.5);
     while ((long long)(bi + 1) * (bi + 2) / 2 <= tix) ++bi;

@@ -299,14 +299,19 @@ struct KMeansEngine {
         }
         const int tiles = ceil_div(n, TC_M);
         const int64_t total_kb = dpad / TC_KB;
-        int ns = (int)std::max<int64_t>(1, std::min<int64_t>(total_kb / 4, (2 * 148) / tiles));
+        // RESPCA_TMA_CFG: 0 = 4 stages, 2 CTAs/SM; 1 = 3 stages, 3 CTAs/SM
+        const int cfg3 = env_int("RESPCA_TMA_CFG", 0);
+        const int per_sm = cfg3 ? 3 : 2;
+        int ns = (int)std::max<int64_t>(1, std::min<int64_t>(total_kb / 4, (per_sm * 148) / tiles));
         ns = std::max(1, std::min(ns, 16));
         if (const char* e = std::getenv("RESPCA_TMA_NS")) ns = std::max(1, std::min(16, std::atoi(e)));
         const int kbps = (int)((total_kb + ns - 1) / ns);
         part.ensure((size_t)ns * n * c);
         xxp.ensure((size_t)ns * n);
-        smem_at_least((const void*)k_screen_tma, (size_t)(TC_SMEM));
-        CK(pdl_launch(k_screen_tma, dim3(tiles, ns), dim3(TM_THREADS), TC_SMEM, st, mapA, mapB, d, n, c, kbps,
+        auto kf = cfg3 ? k_screen_tma<3, 3> : k_screen_tma<4, 2>;
+        const size_t sm = cfg3 ? tm_smem<3>() : tm_smem<4>();
+        smem_at_least((const void*)kf, sm);
+        CK(pdl_launch(kf, dim3(tiles, ns), dim3(TM_THREADS), sm, st, mapA, mapB, d, n, c, kbps,
                       part.p, xxp.p, tcerr.p));
         ln.add(2);
         scr_n = n;
@@ -739,6 +744,36 @@ struct KMeansEngine {
         gram_xn = gxn.p;
         gram_xl = gxl.p;
     }
+    // G computed while X still arrives: the upload records an event per column
+    // chunk; the tiles of block rows up to a chunk's end (a contiguous range of
+    // the row-major lower triangle) wait only for that chunk.  kmeans() then
+    // finds G launched (gram_early) and only waits on gram_ev.
+    bool gram_early = false;
+    void compute_gram_banded(const std::vector<std::pair<int64_t, cudaEvent_t>>& chunks) {
+        if (!gram_st) {
+            int lo = 0, hi = 0;
+            CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            CK(cudaStreamCreateWithPriority(&gram_st, cudaStreamNonBlocking, lo));
+        }
+        alloc_gram();
+        const size_t sm = gram_smem<T>();
+        smem_at_least((const void*)k_gram<T>, sm);
+        long long t_prev = 0;
+        for (const auto& ch : chunks) {
+            const long long nbe = ceil_div((int64_t)std::min<int64_t>(ch.first, n), (int64_t)GR_T);
+            const long long t_end = nbe * (nbe + 1) / 2;
+            CK(cudaStreamWaitEvent(gram_st, ch.second, 0));
+            if (t_end > t_prev) {
+                k_gram<T><<<(unsigned)(t_end - t_prev), 256, sm, gram_st>>>(M, d, n, gG.p, t_end, t_prev);
+                ln.add();
+            }
+            t_prev = t_end;
+        }
+        k_gram_diag<<<ceil_div(n, 256), 256, 0, gram_st>>>(gG.p, n, gram_gamma(), gxx.p, gxn.p, gxl.p);
+        ln.add();
+        CK(cudaEventRecord(gram_ev, gram_st));
+        gram_early = true;
+    }
     void lend_gram(KMeansEngine& o) const {
         o.gram = gram;
         o.gram_xx = gram_xx;
@@ -1155,11 +1190,14 @@ struct KMeansEngine {
         restart_inertia.assign(n_restarts, std::numeric_limits<double>::quiet_NaN());
         struct GramScope {
             KMeansEngine* e;
-            ~GramScope() { e->drop_gram(); }
+            ~GramScope() {
+                e->drop_gram();
+                e->gram_early = false;
+            }
         } gram_scope{this};
-        const bool want_gram = gram_fits();
+        const bool want_gram = gram_early || gram_fits();
         const bool overlap = L > 1 && env_int("RESPCA_GRAM_OVERLAP", 1) != 0;
-        if (want_gram && !overlap) compute_gram();
+        if (want_gram && !overlap && !gram_early) compute_gram();
         if (L > 1) {
             kmeans_lanes(L, max_iters, n_restarts, seed, tol, labels, C, inertia_out, iters_out, want_gram && overlap);
         } else {
@@ -1245,7 +1283,7 @@ struct KMeansEngine {
             compute_gram(gram_st);
         };
         if (want_gram) alloc_gram();  // pointers lent to the lanes below
-        if (want_gram && !gram_when) launch_gram(ready);
+        if (want_gram && !gram_when && !gram_early) launch_gram(ready);
         while ((int)lanes.size() < L) {
             lanes.emplace_back(new Lane());
             {
@@ -1310,7 +1348,7 @@ struct KMeansEngine {
             joint_chosen = pp_joint(joint_eng);
             if (stats) stats->t_pp += since(tj);
         }
-        if (want_gram && gram_when) {
+        if (want_gram && gram_when && !gram_early) {
             cudaEvent_t seeded;
             CK(cudaEventCreateWithFlags(&seeded, cudaEventDisableTiming));
             CK(cudaEventRecord(seeded, st));

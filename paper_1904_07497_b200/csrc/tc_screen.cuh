@@ -355,10 +355,17 @@ RESPCA_DEV void tma_load_2d(uint32_t dst, const CUtensorMap* map, int x, int y, 
         : "memory");
 }
 
-__global__ void __launch_bounds__(TM_THREADS, 2) k_screen_tma(
+// STAGES-deep TMA ring, MINB CTAs per SM (smem ≈ STAGES·24 KB)
+template <int STAGES>
+constexpr size_t tm_smem() {
+    return 1024 + (size_t)STAGES * TC_STAGE_BYTES + 1024;
+}
+template <int STAGES, int MINB>
+__global__ void __launch_bounds__(TM_THREADS, MINB) k_screen_tma(
     const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB, int64_t d,
     int n, int c, int kblocks_per_split, double* __restrict__ part, double* __restrict__ xxp,
     int* __restrict__ err) {
+    constexpr int TC_STAGES = STAGES;  // this kernel's ring depth
     pdl_enter();
     extern __shared__ __align__(1024) unsigned char tsm_raw[];
     unsigned char* tsm = reinterpret_cast<unsigned char*>(((uintptr_t)tsm_raw + 1023) & ~(uintptr_t)1023);
