@@ -146,6 +146,9 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const double* Gc = par ? G1 : G0;
     double* Gn = par ? Gn0 : Gn1;
     const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
+    // fp32 storage only (its tolerance is 1e-4 of the fp64 reference): the two
+    // FP64 divisions per element become multiplies by the reciprocals
+    const double irn = sizeof(T) == 8 ? 0.0 : 1.0 / rho_n;
     const double mw = mean_w[g];
     const int beg = goff[g], end = goff[g + 1];
     const double ng = (double)(end - beg);
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                 for (int w = 0; w < RW; ++w) {
                     // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
                     const double x = xs[u][w], s = ss[u][w], th = ts[u][w];
-                    const double q = th / rho;
+                    const double q = sizeof(T) == 8 ? th / rho : th * thr;  // fp32 storage: reciprocal (1e-4 tolerance)
                     const double dv = (x - s) + q;
                     ln[u][w] = own_w * dv + mw * Gi[w];
                     const double xl = x - ln[u][w];
@@ -213,7 +216,7 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                     sn[u][w] = mag > 0.0 ? copysign(mag, b) : 0.0;
                     rr[u][w] = xl - sn[u][w];
                     tn[u][w] = th + rho * rr[u][w];
-                    sm[u][w] = (x - sn[u][w]) + tn[u][w] / rho_n;
+                    sm[u][w] = (x - sn[u][w]) + (sizeof(T) == 8 ? tn[u][w] / rho_n : tn[u][w] * irn);
                 }
 #pragma unroll
             for (int u = 0; u < B; ++u) {
@@ -354,6 +357,7 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
     const double* Gc = par ? G1 : G0;
     double* Gn = par ? Gn0 : Gn1;
     const double rho = ctl->rho, rho_n = ctl->rho_next, own_w = ctl->own_w, thr = ctl->thr;
+    const double irn = sizeof(T) == 8 ? 0.0 : 1.0 / rho_n;  // fp32 storage: reciprocal multiplies
     const double mw = mean_w[g];
     const int gb = __ldg(goff + g), ge = __ldg(goff + g + 1);
     const int m = ge - gb;
@@ -436,7 +440,7 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
                 for (int v = 0; v < VEC; ++v) {
                     // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
                     const double x = (double)xs[v], sv = (double)ss[v], th = (double)ts[v], lp = (double)ls[v];
-                    const double qq = th / rho;
+                    const double qq = sizeof(T) == 8 ? th / rho : th * thr;  // fp32 storage: reciprocal
                     const double dv = (x - sv) + qq;
                     const double ln = own_w * dv + mw * Gi[j][v];
                     const double xl = x - ln;
@@ -449,7 +453,7 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
                     // summand layout [2][member][row of the block]
                     const int e = cmem[j] * rb_rows + csub[j] * VEC + v;
                     sm_[e] = ln;
-                    sm_[CPS * VEC + e] = (x - sn) + tn / rho_n;
+                    sm_[CPS * VEC + e] = (x - sn) + (sizeof(T) == 8 ? tn / rho_n : tn * irn);
                     lo_[v] = ln;
                     so_[v] = sn;
                     to_[v] = tn;

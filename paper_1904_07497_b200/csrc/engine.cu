@@ -138,6 +138,14 @@ struct Alm : AlmBase {
     double m_lloyd = INFINITY, m_gap = INFINITY;  // initial kmeans(X) decision margins
     // (column end, event) per uploaded chunk of X, recorded by a chunked fill
     std::vector<std::pair<int64_t, cudaEvent_t>> chunk_events;
+    // fp32 storage: the fp64 copy of X widened chunk by chunk during the upload
+    cudaStream_t wide_st = nullptr;
+    std::vector<cudaEvent_t> wide_evs;
+    bool xd_ready = false;
+    ~Alm() override {
+        for (cudaEvent_t e : wide_evs) cudaEventDestroy(e);
+        if (wide_st) cudaStreamDestroy(wide_st);
+    }
     // exact ALM stop (resolve_stop): the start of the loop it replays from, and
     // ‖X‖ as the reference's chain once computed
     Ctl ctl0{};
@@ -180,6 +188,10 @@ struct Alm : AlmBase {
         km.ln = ln;
         km.stats = &stats;
         km.gram_early = false;
+        if constexpr (sizeof(T) == 4) Alm<double>::shared_engine(ctx).gram_early = false;
+        for (cudaEvent_t e : wide_evs) cudaEventDestroy(e);
+        wide_evs.clear();
+        xd_ready = false;
     }
     static KMeansEngine<T>& shared_engine(respca_cu_ctx* cx) {
         auto& h = cx->engines[sizeof(T) == 8 ? 0 : 1];
@@ -238,11 +250,40 @@ struct Alm : AlmBase {
         // the initial clustering's Gram matrix starts on its own stream while X
         // is still arriving (the fill recorded chunk events), before the
         // validation below synchronises
-        if constexpr (sizeof(T) == 8) {
-            const char* ge = std::getenv("RESPCA_GRAM_EARLY");  // =0: G after the upload (round 1)
-            if (!chunk_events.empty() && c > 1 && !(ge && ge[0] == '0')) {
+        const char* ge = std::getenv("RESPCA_GRAM_EARLY");  // =0: G after the upload (round 1)
+        if (!chunk_events.empty() && c > 1 && !(ge && ge[0] == '0')) {
+            if constexpr (sizeof(T) == 8) {
                 km.bind(X.p, d, n, c);
                 if (km.gram_fits()) km.compute_gram_banded(chunk_events);
+            } else {
+                // fp32 storage: each chunk widened to the fp64 copy the initial
+                // clustering runs on (its own stream), G banded behind the widening
+                KMeansEngine<double>& kd = Alm<double>::shared_engine(ctx);
+                kd.st = st;
+                kd.ln = ln;
+                kd.stats = &stats;
+                double* Xd = static_cast<double*>(ctx->arena.get("Xd", sizeof(double) * N));
+                kd.bind(Xd, d, n, c);
+                if (kd.gram_fits()) {
+                    if (!wide_st) CK(cudaStreamCreateWithFlags(&wide_st, cudaStreamNonBlocking));
+                    std::vector<std::pair<int64_t, cudaEvent_t>> wev;
+                    int64_t j0 = 0;
+                    for (const auto& ch : chunk_events) {
+                        CK(cudaStreamWaitEvent(wide_st, ch.second, 0));
+                        const int64_t cnt = (ch.first - j0) * d;
+                        k_widen<<<std::min<int64_t>(4 * 148 * 8, ceil_div(cnt, 256)), 256, 0, wide_st>>>(
+                            X.p + j0 * d, Xd + j0 * d, cnt);
+                        ln.add();
+                        cudaEvent_t e;
+                        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                        wide_evs.push_back(e);
+                        CK(cudaEventRecord(e, wide_st));
+                        wev.emplace_back(ch.first, e);
+                        j0 = ch.first;
+                    }
+                    kd.compute_gram_banded(wev);
+                    xd_ready = true;
+                }
             }
         }
         chunk_events.clear();
@@ -385,8 +426,12 @@ struct Alm : AlmBase {
                 // (C3-f32 init 207 -> fp64's time)
                 const int64_t N = d * n;
                 double* Xd = static_cast<double*>(ctx->arena.get("Xd", sizeof(double) * N));
-                k_widen<<<std::min<int64_t>(4 * 148 * 8, ceil_div(N, 256)), 256, 0, st>>>(X.p, Xd, N);
-                ln.add();
+                if (xd_ready) {  // widened during the upload
+                    CK(cudaStreamWaitEvent(st, wide_evs.back(), 0));
+                } else {
+                    k_widen<<<std::min<int64_t>(4 * 148 * 8, ceil_div(N, 256)), 256, 0, st>>>(X.p, Xd, N);
+                    ln.add();
+                }
                 KMeansEngine<double>& kd = Alm<double>::shared_engine(ctx);
                 kd.st = st;
                 kd.ln = ln;
