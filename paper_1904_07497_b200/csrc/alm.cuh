@@ -323,9 +323,47 @@ struct StreamCfg {
 RESPCA_DEV void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 RESPCA_DEV void named_bar_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(n) : "memory"); }
 
+// the stream kernel's chain warp (RP rows per lane): per stage, wait for the
+// element warps' summands (FULL), add them in member order, release (EMPTY)
+template <int RP>
+RESPCA_DEV void stream_chain(const double* summ, int half, int rb_rows, int nst, int m, int mps, int lane,
+                             int64_t r0, int64_t d, int g, double ng, double* __restrict__ Cw,
+                             double* __restrict__ Gn) {
+    constexpr int BAR_FULL = 1, BAR_EMPTY = 3, NT = 288;
+    double a[RP], b[RP];
+    int rl[RP];
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+        a[q] = b[q] = 0.0;
+        rl[q] = (lane + 32 * q) < rb_rows ? lane + 32 * q : 0;
+    }
+    for (int s = 0; s < nst; ++s) {
+        named_bar_sync(BAR_FULL + (s & 1), NT);
+        const double* y0 = summ + (size_t)(s & 1) * 2 * half;
+        const double* y1 = y0 + half;
+        const int cnt = m - s * mps < mps ? m - s * mps : mps;
+#pragma unroll 4
+        for (int u = 0; u < cnt; ++u)
+#pragma unroll
+            for (int q = 0; q < RP; ++q) {
+                a[q] += y0[u * rb_rows + rl[q]];  // ascending member order (solver.cpp:64, kmeans.cpp:73)
+                b[q] += y1[u * rb_rows + rl[q]];
+            }
+        if (s + 2 < nst) named_bar_arrive(BAR_EMPTY + (s & 1), NT);
+    }
+#pragma unroll
+    for (int q = 0; q < RP; ++q) {
+        const int r_ = lane + 32 * q;
+        if (r_ < rb_rows && r0 + r_ < d) {
+            Cw[(int64_t)g * d + r0 + r_] = a[q] * (1.0 / ng);  // kmeans.cpp:78-79
+            Gn[(int64_t)g * d + r0 + r_] = b[q];
+        }
+    }
+}
+
 constexpr int PFS_THREADS = 288;  // 8 element warps + 1 chain warp
 template <typename T, int K, int NS, int RBMAX>
-__global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
+__global__ void __launch_bounds__(PFS_THREADS, NS <= 3 ? 3 : 2) k_pass_f_stream(
     const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members, const int* __restrict__ gorder,
     const double* G0, const double* G1, double* Gn0, double* Gn1, double* __restrict__ Cw,
@@ -490,35 +528,16 @@ __global__ void __launch_bounds__(PFS_THREADS, 2) k_pass_f_stream(
         cp_wait<0>();
     } else {
         // ================= the chain warp: each row's two sums in member order =================
-        double a[RPL], b[RPL];
-        int rl[RPL];
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            a[q] = b[q] = 0.0;
-            rl[q] = (lane + 32 * q) < rb_rows ? lane + 32 * q : 0;
-        }
-        for (int s = 0; s < nst; ++s) {
-            named_bar_sync(BAR_FULL + (s & 1), PFS_THREADS);
-            const double* y0 = summ + (size_t)(s & 1) * 2 * CPS * VEC;
-            const double* y1 = y0 + CPS * VEC;
-            const int cnt = m - s * mps < mps ? m - s * mps : mps;
-#pragma unroll 4
-            for (int u = 0; u < cnt; ++u)
-#pragma unroll
-                for (int q = 0; q < RPL; ++q) {
-                    a[q] += y0[u * rb_rows + rl[q]];  // ascending member order (solver.cpp:64, kmeans.cpp:73)
-                    b[q] += y1[u * rb_rows + rl[q]];
-                }
-            if (s + 2 < nst) named_bar_arrive(BAR_EMPTY + (s & 1), PFS_THREADS);
-        }
-#pragma unroll
-        for (int q = 0; q < RPL; ++q) {
-            const int r_ = lane + 32 * q;
-            if (r_ < rb_rows && r0 + r_ < d) {
-                Cw[(int64_t)g * d + r0 + r_] = a[q] * (1.0 / ng);  // kmeans.cpp:78-79
-                Gn[(int64_t)g * d + r0 + r_] = b[q];
-            }
-        }
+        // (instantiated for the rows per lane this stream needs: no idle chains)
+        const int rpl = (rb_rows + 31) / 32;
+        auto run = [&](auto rplc) {
+            constexpr int RP = decltype(rplc)::value;
+            stream_chain<RP>(summ, CPS * VEC, rb_rows, nst, m, mps, lane, r0, d, g, ng, Cw, Gn);
+        };
+        if (rpl <= 1) run(std::integral_constant<int, 1>{});
+        else if (rpl == 2) run(std::integral_constant<int, 2>{});
+        else if (rpl <= 4 || RPL <= 4) run(std::integral_constant<int, (RPL < 4 ? RPL : 4)>{});
+        else run(std::integral_constant<int, RPL>{});
     }
     double pv[5] = {pf, pl, ps, p1, psc};
     block_sum<5>(pv, red);

@@ -104,6 +104,11 @@ struct Alm : AlmBase {
         return e ? std::atoi(e) : -1;
     }();
     bool pf_stream = false;
+    // RESPCA_STREAM_NS=3 (fp64): 3-stage pipeline, 3 CTAs per SM (else 5 stages, 2 per SM)
+    bool stream_ns3 = [] {
+        const char* e = std::getenv("RESPCA_STREAM_NS");
+        return e && e[0] == '3';
+    }();
     int stream_rb = 32, stream_nrb = 0;
     int ring_cfg() const {  // RESPCA_RING_CFG = 5, 10 or 16 (tuning)
         if (const char* e = std::getenv("RESPCA_RING_CFG")) {
@@ -342,7 +347,7 @@ struct Alm : AlmBase {
             // should fill whole waves of the 2·148 resident CTAs — the fill
             // (streams / (waves·slots)) decides, ties to the wider segment
             const int vec = 16 / (int)sizeof(T), rbmax = sizeof(T) == 8 ? 128 : 256;
-            const int64_t slots = 2 * 148;
+            const int64_t slots = (stream_ns3 ? 3 : 2) * 148;
             double best = -1.0;
             for (int r = 16; r <= rbmax; r += vec) {
                 if (r / vec > 256) break;
@@ -533,8 +538,12 @@ struct Alm : AlmBase {
             return;
         }
         if (pf_stream) {
-            if constexpr (sizeof(T) == 8) launch_stream<1, 5, 128>();
-            else launch_stream<1, 4, 256>();
+            if constexpr (sizeof(T) == 8) {
+                if (stream_ns3) launch_stream<1, 3, 128>();
+                else launch_stream<1, 5, 128>();
+            } else {
+                launch_stream<1, 4, 256>();
+            }
             ln.add();
             return;
         }
