@@ -173,6 +173,35 @@ __global__ void k_gram_diag(const double* __restrict__ G, int n, double gamG, do
     xl[j] = __dsqrt_rd(fmax(__dmul_rd(v, __dsub_rd(1.0, 2.0 * gamG)), 0.0));
 }
 
+// k-means++ d² (kmeans.cpp:188-191) of R restarts from G: one row of G per
+// restart and pick instead of a pass over the d×n columns.
+//   d̃(j, m) = max((Ĝ_jj + Ĝ_mm) − 2Ĝ_jm, 0)
+//   |d̃(j, m) − sq_dist(x_j, x_m)| ≤ (γ_G + γ_c + 8u)·(‖x_j‖ + ‖x_m‖)²
+// (γ_G: any DMMA accumulation order; γ_c: the reference's chain of rounded
+// squares; 8u: the three FP64 operations here).  The host turns the d̃ values
+// into the pick with this bound and falls back to the exact chains when the
+// draw lands inside it (KMeansEngine::pp_joint).
+template <int R>
+__global__ void __launch_bounds__(256) k_pp_gram(const double* __restrict__ G, const double* __restrict__ xx, int n,
+                                                 PPLast last, double* __restrict__ d2) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const double xj = xx[j];
+    double g[R], xm[R], o[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int m = last.v[r];
+        g[r] = __ldg(G + (int64_t)m * n + j);
+        xm[r] = __ldg(xx + m);
+        o[r] = d2[(int64_t)r * n + j];
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const double v = fmax((xj + xm[r]) - 2.0 * g[r], 0.0);
+        d2[(int64_t)r * n + j] = fmin(o[r], v);
+    }
+}
+
 // per-centroid state of the Gram refinement
 struct GramScal {
     double Q, A, ES, EQ, Dl;  // Q̂_k, Σ‖x_m‖ (upper), S error / ‖x_j‖, Q error, ‖c_k − μ_k‖

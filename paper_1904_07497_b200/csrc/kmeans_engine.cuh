@@ -1091,11 +1091,42 @@ struct KMeansEngine {
         ln.add();
     }
     HBuf hpp;
-    std::vector<std::vector<int>> pp_joint(std::vector<std::mt19937_64>& engs) {
+    template <int R>
+    void launch_pp_gram(const PPLast& lasts) {
+        k_pp_gram<R><<<ceil_div(n, 256), 256, 0, st>>>(gram, gram_xx, n, lasts, d2.p);
+        ln.add();
+    }
+    // on_gram: the d² values come from the Gram matrix (k_pp_gram: one row of G
+    // per restart and pick, no pass over the columns) with the rigorous bound
+    // E = κ·(2·max‖x‖)² per value.  The reference's pick is the first column
+    // where its running remainder r − Σ d² turns ≤ 0; the remainder computed
+    // from the d̃ values differs from the reference's by at most B (derived
+    // below), so the pick is the reference's whenever no remainder up to the
+    // pick lies within ±B.  Otherwise the restart is seeded again on the exact
+    // chains (pp_init) from its start state — the draws a restart consumes do
+    // not depend on the d² values, only on `total > 0`.
+    uint64_t pp_gram_fallbacks = 0;
+    std::vector<std::vector<int>> pp_joint(std::vector<std::mt19937_64>& engs, bool on_gram = false) {
         const int R = (int)engs.size();
         if (R < 1 || R > 8) throw InvalidArg("pp_joint: 1..8 restarts");
         if (c == 0) throw InvalidArg("kmeans_pp_init: c must be >= 1");
         if ((int64_t)c > n) throw InvalidArg("kmeans_pp_init: c exceeds column count");
+        const bool og = on_gram && gram != nullptr && gram_ev != nullptr && env_int("RESPCA_PP_GRAM", 1) != 0;
+        double E = 0.0;
+        if (og) {
+            CK(cudaStreamWaitEvent(st, gram_ev, 0));
+            std::vector<double> hx(n);
+            CK(cudaMemcpyAsync(hx.data(), gram_xn, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+            CK(cudaStreamSynchronize(st));
+            double xm = 0.0;
+            for (int j = 0; j < n; ++j) xm = std::max(xm, hx[j]);
+            const double kap = (gram_gamma() + ((double)d + 3.0) * kU * 1.02 + 8.0 * kU) * 1.01;
+            E = kap * (2.0 * xm) * (2.0 * xm) * 1.0001;
+            if (!(E == E) || std::isinf(E)) throw InvalidArg("kmeans_pp_init: non-finite Gram norms");
+        }
+        const std::vector<std::mt19937_64> start = engs;
+        std::vector<char> amb(R, 0);
+        const int force_amb = og ? env_int("RESPCA_PP_GRAM_FORCE_AMB", 0) : 0;  // tests: restart v−1 falls back
         std::vector<std::vector<int>> chosen(R);
         std::vector<std::vector<char>> is_chosen(R, std::vector<char>(n, 0));
         for (int r = 0; r < R; ++r) {
@@ -1111,18 +1142,81 @@ struct KMeansEngine {
         for (int p = 1; p < c; ++p) {
             PPLast lasts{};
             for (int r = 0; r < 8; ++r) lasts.v[r] = chosen[r < R ? r : 0].back();
-            switch (R) {
-                case 1: launch_pp_multi<1>(lasts); break;
-                case 2: launch_pp_multi<2>(lasts); break;
-                case 3: launch_pp_multi<3>(lasts); break;
-                case 4: launch_pp_multi<4>(lasts); break;
-                case 5: launch_pp_multi<5>(lasts); break;
-                case 6: launch_pp_multi<6>(lasts); break;
-                case 7: launch_pp_multi<7>(lasts); break;
-                default: launch_pp_multi<8>(lasts); break;
+            if (og) {
+                switch (R) {
+                    case 1: launch_pp_gram<1>(lasts); break;
+                    case 2: launch_pp_gram<2>(lasts); break;
+                    case 3: launch_pp_gram<3>(lasts); break;
+                    case 4: launch_pp_gram<4>(lasts); break;
+                    case 5: launch_pp_gram<5>(lasts); break;
+                    case 6: launch_pp_gram<6>(lasts); break;
+                    case 7: launch_pp_gram<7>(lasts); break;
+                    default: launch_pp_gram<8>(lasts); break;
+                }
+            } else {
+                switch (R) {
+                    case 1: launch_pp_multi<1>(lasts); break;
+                    case 2: launch_pp_multi<2>(lasts); break;
+                    case 3: launch_pp_multi<3>(lasts); break;
+                    case 4: launch_pp_multi<4>(lasts); break;
+                    case 5: launch_pp_multi<5>(lasts); break;
+                    case 6: launch_pp_multi<6>(lasts); break;
+                    case 7: launch_pp_multi<7>(lasts); break;
+                    default: launch_pp_multi<8>(lasts); break;
+                }
             }
             CK(cudaMemcpyAsync(hd2, d2.p, sizeof(double) * R * n, cudaMemcpyDeviceToHost, st));
             CK(cudaStreamSynchronize(st));
+            if (og) {
+                for (int r = 0; r < R; ++r) {
+                    if (amb[r]) continue;
+                    if (force_amb > 0 && (force_amb - 1) % R == r && p == std::min(3, c - 1)) {
+                        amb[r] = 1;
+                        continue;
+                    }
+                    const double* h = hd2 + (size_t)r * n;
+                    double total = 0.0;
+                    for (int j = 0; j < n; ++j) total += h[j];
+                    // |total − reference total|: n values within E, two recursive sums of n terms
+                    const double gn = (double)n * kU * 1.01;
+                    const double ET = (double)n * E * (1.0 + gn) + 2.02 * gn * total;
+                    if (!(total > 2.0 * ET) || std::isinf(total)) {  // `total > 0` not certain
+                        amb[r] = 1;
+                        continue;
+                    }
+                    std::uniform_real_distribution<double> u(0.0, total);
+                    double rr = u(engs[r]);
+                    // start value within ET + 3u·total; each step adds ≤ E + u·(2·total + ET)
+                    const double B = (ET + 3.0 * kU * total) + (double)n * E + 2.2 * (double)n * kU * (total + ET);
+                    int pick = n, hit = n;
+                    for (int j = 0; j < n; ++j) {
+                        rr -= h[j];
+                        if (rr <= B) {
+                            hit = j;
+                            break;
+                        }
+                    }
+                    if (hit < n && rr >= -B) {  // the sign of the reference's remainder is not certain here
+                        amb[r] = 1;
+                        continue;
+                    }
+                    // certainly ≤ 0 from column `hit` on (it only decreases): the first unchosen one
+                    for (int j = hit; j < n; ++j)
+                        if (!is_chosen[r][j]) {
+                            pick = j;
+                            break;
+                        }
+                    if (pick == n)
+                        for (int j = 0; j < n; ++j)
+                            if (!is_chosen[r][j]) {
+                                pick = j;
+                                break;
+                            }
+                    chosen[r].push_back(pick);
+                    is_chosen[r][pick] = 1;
+                }
+                continue;
+            }
             for (int r = 0; r < R; ++r) {  // kmeans.cpp:192-221, restart by restart
                 const double* h = hd2 + (size_t)r * n;
                 double total = 0.0;
@@ -1149,6 +1243,19 @@ struct KMeansEngine {
                 is_chosen[r][pick] = 1;
             }
         }
+        if (og && trace_on()) {
+            int na = 0;
+            for (int r = 0; r < R; ++r) na += amb[r];
+            std::fprintf(stderr, "[respca] k-means++ on G: %d restarts, %d picks each, bound per value %.3g, %d to the exact chains\n",
+                         R, c - 1, E, na);
+        }
+        for (int r = 0; r < R; ++r)
+            if (amb[r]) {  // exact chains from the restart's start state
+                engs[r] = start[r];
+                chosen[r] = pp_init(engs[r]);
+                ++pp_gram_fallbacks;
+                if (trace_on()) std::fprintf(stderr, "[respca] k-means++ on G: restart %d seeded again on the exact chains\n", r);
+            }
         return chosen;
     }
 
@@ -1345,7 +1452,7 @@ struct KMeansEngine {
             const auto tj = HClock::now();
             joint_eng.assign(spec.begin(), spec.begin() + (size_t)std::min<uint64_t>(n_restarts, 8));
             Nvtx r_pp("k-means++ seeding (joint)");
-            joint_chosen = pp_joint(joint_eng);
+            joint_chosen = pp_joint(joint_eng, want_gram && !gram_when);
             if (stats) stats->t_pp += since(tj);
         }
         if (want_gram && gram_when && !gram_early) {

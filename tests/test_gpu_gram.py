@@ -101,6 +101,26 @@ def test_init_switches_bitwise(env):
     assert r.stdout.count(" OK ") == 6, r.stdout
 
 
+@pytest.mark.parametrize("env,exact", [({"RESPCA_KM_LANES": "3"}, None),
+                                       ({"RESPCA_KM_LANES": "3", "RESPCA_PP_GRAM_FORCE_AMB": "2"}, 1),
+                                       ({"RESPCA_KM_LANES": "2", "RESPCA_PP_GRAM": "0"}, -1)])
+def test_seeding_on_gram_bitwise(env, exact):
+    """k-means++ d² from the Gram matrix (k_pp_gram) with its rigorous bound:
+    the same picks as the reference's chains on tie-heavy, duplicate, tiny and
+    large inputs; a restart forced to the exact chains (and the switch off)
+    gives the same results."""
+    r = run(env)
+    assert r.returncode == 0, r.stdout + r.stderr[-4000:]
+    assert r.stdout.count(" OK ") == 6, r.stdout
+    lines = [ln for ln in r.stderr.splitlines() if "k-means++ on G:" in ln and "restarts," in ln]
+    if exact == -1:
+        assert not lines
+    else:
+        assert len(lines) >= 6, r.stderr[-2000:]
+        if exact:
+            assert all(int(ln.split(",")[-1].split()[0]) >= 1 for ln in lines), lines
+
+
 def test_per_pass_refinement_bitwise():
     r = run({"RESPCA_HART_GRAM": "0"})
     assert r.returncode == 0, r.stdout + r.stderr[-4000:]
