@@ -236,6 +236,19 @@ int respca_cu_outlier_scores(respca_cu_ctx* ctx, const double* s, uint64_t d, ui
 int respca_cu_synth_rpca(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t r, double sigma, double p,
                          double lo, double hi, uint64_t seed, int dtype, void* X_out);
 
+/* io::synth_generate (proj/src/io.cpp:232-294, declared at proj/include/respca/
+ * io.hpp:88) with its O(d·n) assembly on the device: near-equal contiguous
+ * groups of identical uniform(0,1) prototype columns (L0), round(sparsity·d·n)
+ * corruptions at partial-Fisher–Yates positions with a random sign and a
+ * magnitude in [magnitude/2, magnitude) (S0), X = L0 + S0 (+ N(0, noise_sigma²)
+ * per element when noise_sigma > 0).  The libstdc++ draws run on the host in
+ * the reference's order, so every output is byte-identical to the reference's.
+ * X_out / L0_out / S0_out (host, d×n column-major fp64) and labels_out (n) may
+ * each be NULL.  Invalid specs → EINVAL with the reference's message. */
+int respca_cu_synth_generate(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t c, double sparsity,
+                             double magnitude, double noise_sigma, uint64_t seed, double* X_out,
+                             double* L0_out, double* S0_out, uint64_t* labels_out);
+
 #ifdef __cplusplus
 }
 #endif

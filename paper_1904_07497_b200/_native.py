@@ -66,7 +66,7 @@ EXPORTS = [
     "respca_cu_column_l2_norms", "respca_cu_column_mean", "respca_cu_bench_prepare",
     "respca_cu_bench_steps", "respca_cu_debug_screen", "respca_cu_kmeans_pp_init_cb",
     "respca_cu_debug_screen_tc", "respca_cu_debug_guards", "respca_cu_last_margins", "respca_cu_binary_info", "respca_cu_solve_file",
-    "respca_cu_outlier_scores", "respca_cu_synth_rpca",
+    "respca_cu_outlier_scores", "respca_cu_synth_rpca", "respca_cu_synth_generate",
 ]
 
 
@@ -126,6 +126,8 @@ def lib() -> C.CDLL:
                                                    u64ptr]
             L.respca_cu_synth_rpca.argtypes = [vp, u64, u64, u64, C.c_double, C.c_double, C.c_double,
                                                C.c_double, u64, C.c_int, vp]
+            L.respca_cu_synth_generate.argtypes = [vp, u64, u64, u64, C.c_double, C.c_double, C.c_double,
+                                                   u64, vp, vp, vp, vp]
             _lib = L
         return _lib
 

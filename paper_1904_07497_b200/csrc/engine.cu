@@ -15,6 +15,7 @@
 #include <cstring>
 #include <memory>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "alm.cuh"
@@ -1819,6 +1820,94 @@ int respca_cu_synth_rpca(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t r,
             ctx->launches++;
         }
         CK(cudaMemcpyAsync(X_out, dx, es * d * n, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+    });
+}
+
+int respca_cu_synth_generate(respca_cu_ctx* ctx, uint64_t d, uint64_t n, uint64_t c, double sparsity,
+                             double magnitude, double noise_sigma, uint64_t seed, double* X_out, double* L0_out,
+                             double* S0_out, uint64_t* labels_out) {
+    return guarded(ctx, [&] {  // io::synth_generate (io.cpp:232-294)
+        if (d == 0 || n == 0) throw InvalidArg("synth_generate: dimensions must be >= 1");
+        if (c == 0 || c > n) throw InvalidArg("synth_generate: need 1 <= c <= n");
+        if (!(sparsity >= 0.0) || sparsity >= 1.0) throw InvalidArg("synth_generate: sparsity must be in [0,1)");
+        check_dims(d, n);
+        if (n > 65535ULL) throw InvalidArg("synth_generate: too many columns for one launch");
+        const uint64_t N = d * n;
+        std::mt19937_64 rng(seed);
+        std::uniform_real_distribution<double> unit(0.0, 1.0);
+        const uint64_t base = n / c, rem = n % c;
+        if (labels_out) {
+            uint64_t col = 0;
+            for (uint64_t g = 0; g < c; ++g)
+                for (uint64_t k = 0; k < base + (g < rem ? 1 : 0); ++k) labels_out[col++] = g;
+        }
+        std::vector<double> proto(c * d);  // group after group, row after row (io.cpp:253-256)
+        for (double& v : proto) v = unit(rng);
+        // partial Fisher–Yates over positions 0..N-1 (io.cpp:267-273): only the
+        // entries a swap has touched are stored
+        const uint64_t nnz = (uint64_t)std::llround(sparsity * (double)N);
+        std::vector<uint64_t> pos(nnz);
+        std::vector<double> val(nnz);
+        {
+            std::unordered_map<uint64_t, uint64_t> moved;
+            moved.reserve((size_t)(2 * nnz + 16));
+            auto at = [&](uint64_t k) {
+                auto it = moved.find(k);
+                return it == moved.end() ? k : it->second;
+            };
+            std::uniform_real_distribution<double> mag(magnitude / 2.0, magnitude);
+            for (uint64_t k = 0; k < nnz; ++k) {
+                std::uniform_int_distribution<std::size_t> pick((std::size_t)k, (std::size_t)(N - 1));
+                const uint64_t q = (uint64_t)pick(rng);
+                const uint64_t vk = at(k), vq = at(q);
+                moved[k] = vq;
+                moved[q] = vk;
+                const double sign = unit(rng) < 0.5 ? -1.0 : 1.0;
+                pos[k] = vq;
+                val[k] = sign * mag(rng);
+            }
+        }
+        cudaStream_t st = ctx->st;
+        DBuf<double> dproto, dval, dz;
+        DBuf<uint64_t> dpos;
+        dproto.ensure(c * d);
+        CK(cudaMemcpyAsync(dproto.p, proto.data(), sizeof(double) * c * d, cudaMemcpyHostToDevice, st));
+        double* dX = static_cast<double*>(ctx->arena.get("X", sizeof(double) * N));
+        double* dL = static_cast<double*>(ctx->arena.get("L", sizeof(double) * N));
+        double* dS = static_cast<double*>(ctx->arena.get("S", sizeof(double) * N));
+        k_sg_fill<<<dim3((unsigned)std::min<uint64_t>(ceil_div(d, 256), 64), (unsigned)n), 256, 0, st>>>(
+            dproto.p, d, n, base, rem, dL, dS);
+        ctx->launches++;
+        if (nnz) {
+            dpos.ensure(nnz);
+            dval.ensure(nnz);
+            CK(cudaMemcpyAsync(dpos.p, pos.data(), sizeof(uint64_t) * nnz, cudaMemcpyHostToDevice, st));
+            CK(cudaMemcpyAsync(dval.p, val.data(), sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+            k_sg_scatter<<<(unsigned)ceil_div(nnz, 256), 256, 0, st>>>(dpos.p, dval.p, nnz, dS);
+            ctx->launches++;
+        }
+        const unsigned gb = (unsigned)std::min<uint64_t>(ceil_div(N, 256), 148 * 16);
+        k_sg_sum<<<gb, 256, 0, st>>>(dL, dS, N, dX);
+        ctx->launches++;
+        if (noise_sigma > 0.0) {  // io.cpp:279-282: one normal draw per element, in storage order
+            std::normal_distribution<double> noise(0.0, noise_sigma);
+            const uint64_t CH = 1ULL << 22;
+            std::vector<double> z(std::min(CH, N));
+            dz.ensure(z.size());
+            for (uint64_t e0 = 0; e0 < N; e0 += CH) {
+                const uint64_t cnt = std::min(CH, N - e0);
+                for (uint64_t e = 0; e < cnt; ++e) z[e] = noise(rng);
+                CK(cudaMemcpyAsync(dz.p, z.data(), sizeof(double) * cnt, cudaMemcpyHostToDevice, st));
+                k_sg_noise<<<(unsigned)std::min<uint64_t>(ceil_div(cnt, 256), 148 * 16), 256, 0, st>>>(dz.p, cnt,
+                                                                                                      dX + e0);
+                ctx->launches++;
+                CK(cudaStreamSynchronize(st));  // z is reused by the next chunk
+            }
+        }
+        if (X_out) CK(cudaMemcpyAsync(X_out, dX, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+        if (L0_out) CK(cudaMemcpyAsync(L0_out, dL, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
+        if (S0_out) CK(cudaMemcpyAsync(S0_out, dS, sizeof(double) * N, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
     });
 }

@@ -43,4 +43,46 @@ __global__ void __launch_bounds__(256) k_synth_rpca(const double* __restrict__ U
     X[j * d + i] = (T)__dadd_rn(acc, s);
 }
 
+// ---------------------------------------------------------------------------
+// io::synth_generate (io.cpp:232-294) with its O(d·n) assembly on the device.
+// The libstdc++ draws stay on the host in the reference's order (c·d uniform
+// prototype entries, then per corruption one position, one sign and one
+// magnitude draw, then d·n normal draws when noise_sigma > 0); the device
+// writes L0 (each column = its group's prototype), scatters the nnz
+// corruptions into S0, forms X = L0 + S0 and adds the noise chunk by chunk.
+// ---------------------------------------------------------------------------
+// column j's group under the reference's near-equal contiguous blocks
+RESPCA_DEV uint64_t sg_label(uint64_t j, uint64_t base, uint64_t rem) {
+    const uint64_t big = (base + 1) * rem;  // columns covered by the `rem` groups of base+1
+    return j < big ? j / (base + 1) : rem + (j - big) / base;
+}
+
+__global__ void __launch_bounds__(256) k_sg_fill(const double* __restrict__ proto, uint64_t d, uint64_t n,
+                                                 uint64_t base, uint64_t rem, double* __restrict__ L0,
+                                                 double* __restrict__ S0) {
+    const uint64_t j = blockIdx.y;
+    const uint64_t g = sg_label(j, base, rem);
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < d; i += (uint64_t)gridDim.x * blockDim.x) {
+        L0[j * d + i] = __ldg(proto + g * d + i);
+        S0[j * d + i] = 0.0;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_sg_scatter(const uint64_t* __restrict__ pos, const double* __restrict__ val,
+                                                    uint64_t nnz, double* __restrict__ S0) {
+    const uint64_t k = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < nnz) S0[pos[k]] = val[k];  // positions are distinct (a partial permutation)
+}
+
+__global__ void __launch_bounds__(256) k_sg_sum(const double* __restrict__ L0, const double* __restrict__ S0,
+                                                uint64_t N, double* __restrict__ X) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < N; e += (uint64_t)gridDim.x * blockDim.x)
+        X[e] = __dadd_rn(L0[e], S0[e]);
+}
+
+__global__ void __launch_bounds__(256) k_sg_noise(const double* __restrict__ z, uint64_t cnt, double* __restrict__ X) {
+    for (uint64_t e = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; e < cnt; e += (uint64_t)gridDim.x * blockDim.x)
+        X[e] = __dadd_rn(X[e], z[e]);
+}
+
 }  // namespace respca_dev

@@ -259,6 +259,33 @@ def outlier_scores(s, threshold: float, ctx=None) -> OutlierScores:
     return OutlierScores(sc, fl[: nf.value].copy())
 
 
+@dataclass
+class SynthData:
+    """io.hpp SynthData: the generated problem and its ground truth."""
+    x: np.ndarray
+    l0: np.ndarray
+    s0: np.ndarray
+    assignment: np.ndarray
+
+
+def synth_generate(d: int, n: int, c: int, sparsity: float = 0.05, magnitude: float = 1.0,
+                   noise_sigma: float = 0.0, seed: int = 0, ctx=None) -> SynthData:
+    """io::synth_generate (io.cpp:232-294): the reference's synthetic problem,
+    byte-identical, with the d×n assembly on the device
+    (respca_cu_synth_generate).  ValueError carries the reference's message."""
+    ctx = _ctx(ctx)
+    d, n, c = int(d), int(n), int(c)
+    shape = (max(d, 0), max(n, 0))
+    x, l0, s0 = (np.empty(shape, order="F") for _ in range(3))
+    lab = np.empty(max(n, 0), dtype=np.uint64)
+    rc = N.lib().respca_cu_synth_generate(ctx.handle, d, n, c, float(sparsity), float(magnitude),
+                                          float(noise_sigma), int(seed), x.ctypes.data_as(C.c_void_p),
+                                          l0.ctypes.data_as(C.c_void_p), s0.ctypes.data_as(C.c_void_p),
+                                          lab.ctypes.data_as(C.c_void_p))
+    N.check(ctx, rc)
+    return SynthData(x, l0, s0, lab)
+
+
 def write_binary_matrix(path, m) -> None:
     """RESPCA1 writer (io.cpp:156-164): magic, u64le rows, u64le cols, f64le
     column-major payload.  Host-side helper (tests, tools)."""

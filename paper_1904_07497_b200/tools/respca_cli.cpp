@@ -430,8 +430,24 @@ int run_outliers(const Args& a) {  // respca_cli.cpp:229-264
 
 int run_synth(const Args& a) {  // respca_cli.cpp:166-185
     const uint64_t d = a.u("d", 100), n = a.u("n", 200), c = a.u("c", 3);
-    const Synth s = synth_generate(d, n, c, a.num("sparsity", 0.05), a.num("magnitude", 1.0),
-                                   a.num("noise-sigma", 0.0), a.u("seed", 0));
+    Synth s;
+    if (a.has("device")) {  // the d×n assembly on the GPU (respca_cu_synth_generate), same bytes
+        if (d == 0 || n == 0) throw UsageError("synth_generate: dimensions must be >= 1");
+        Ctx ctx((int)a.u("device", 0));
+        for (Matrix* m : {&s.x, &s.l0, &s.s0}) {
+            m->rows = d;
+            m->cols = n;
+            m->v.assign(d * n, 0.0);
+        }
+        s.labels.assign(n, 0);
+        const int rc = respca_cu_synth_generate(ctx.h, d, n, c, a.num("sparsity", 0.05), a.num("magnitude", 1.0),
+                                                a.num("noise-sigma", 0.0), a.u("seed", 0), s.x.v.data(),
+                                                s.l0.v.data(), s.s0.v.data(), s.labels.data());
+        ctx.check(rc);
+    } else {
+        s = synth_generate(d, n, c, a.num("sparsity", 0.05), a.num("magnitude", 1.0), a.num("noise-sigma", 0.0),
+                           a.u("seed", 0));
+    }
     if (a.has("out-x")) write_binary(a.str("out-x"), s.x);
     if (a.has("out-l0")) write_binary(a.str("out-l0"), s.l0);
     if (a.has("out-s0")) write_binary(a.str("out-s0"), s.s0);
@@ -523,7 +539,7 @@ int main(int argc, char** argv) {
         if (sub == "synth")
             return run_synth(parse(argc, argv, 2,
                                    {"d", "n", "c", "sparsity", "magnitude", "noise-sigma", "seed", "out-x",
-                                    "out-l0", "out-s0", "out-labels"}));
+                                    "out-l0", "out-s0", "out-labels", "device"}));
         if (sub == "bench")
             return run_bench(parse(argc, argv, 2, {"mode", "sizes", "fixed", "repeats", "iters", "seed", "out", "device"}));
         if (sub == "frames") throw UsageError("frames: PGM frame stacks are not supported by this build");
