@@ -123,13 +123,38 @@ struct Vec<float, 4> {
 // elements in flight per thread instead of the few a register batch holds.
 // ---------------------------------------------------------------------------
 constexpr int PFR_T = 64;  // default CTA rows
-template <typename T, int U, int NT = PFR_T, int B = 1, int RW = 1>
+RESPCA_DEV double abs_a(double v) { return fabs(v); }
+RESPCA_DEV float abs_a(float v) { return fabsf(v); }
+RESPCA_DEV double copysign_a(double m, double s) { return copysign(m, s); }
+RESPCA_DEV float copysign_a(float m, float s) { return copysignf(m, s); }
+RESPCA_DEV double min_a(double a, double b) { return fmin(a, b); }
+RESPCA_DEV float min_a(float a, float b) { return fminf(a, b); }
+template <typename T, int RW, typename A>
+RESPCA_DEV void store_row(T* p, const A (&a)[RW]) {
+    if constexpr (sizeof(T) == 8) {
+        if constexpr (RW == 2) __stcs(reinterpret_cast<double2*>(p), make_double2(a[0], a[1]));
+        else __stcs(p, (double)a[0]);
+    } else {
+        if constexpr (RW == 4) __stcs(reinterpret_cast<float4*>(p), make_float4((float)a[0], (float)a[1], (float)a[2], (float)a[3]));
+        else if constexpr (RW == 2) __stcs(reinterpret_cast<float2*>(p), make_float2((float)a[0], (float)a[1]));
+        else __stcs(p, (float)a[0]);
+    }
+}
+// F32A (fp32 storage only): the element chain in FP32 arithmetic — fp32 mode's
+// tolerance is 1e-4 of the fp64 reference and every stored value is rounded to
+// FP32 anyway; the ordered group sums (Cw, G_{t+1}) and the residual partials
+// still accumulate in FP64 (one widening per term / per batch).  Without it
+// the kernel spends its issue slots on F2F conversions and FP64 operations
+// (ncu: fp64 30 %, xu 30 % busy at 29 % occupancy) and stays at 0.69 of HBM.
+template <typename T, int U, int NT = PFR_T, int B = 1, int RW = 1, bool F32A = false>
 __global__ void __launch_bounds__(NT) k_pass_f_ring(
     const T* __restrict__ X, T* __restrict__ L, T* __restrict__ S, T* __restrict__ Th,
     const int* __restrict__ goff, const int* __restrict__ members, const double* G0, const double* G1,
     double* Gn0, double* Gn1, double* __restrict__ Cw, const double* __restrict__ mean_w,
     const Ctl* __restrict__ ctl, double* __restrict__ partials, int64_t d, int rowblocks,
     __nv_bfloat16* __restrict__ Lb, int64_t dpad) {
+    static_assert(!F32A || sizeof(T) == 4, "FP32 arithmetic is for fp32 storage");
+    using A = std::conditional_t<F32A, float, double>;  // arithmetic type of the element chain
     // RW rows per thread (RW = 2 needs d even): one 2·sizeof(T)-byte copy per
     // array and member, so a warp moves 32·RW·sizeof(T) contiguous bytes
     __shared__ double red[32 * 5];
@@ -149,17 +174,20 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
     // fp32 storage only (its tolerance is 1e-4 of the fp64 reference): the two
     // FP64 divisions per element become multiplies by the reciprocals
     const double irn = sizeof(T) == 8 ? 0.0 : 1.0 / rho_n;
+    const A rho_a = (A)rho, own_a = (A)own_w, thr_a = (A)thr, irn_a = (A)irn;
     const double mw = mean_w[g];
     const int beg = goff[g], end = goff[g + 1];
     const double ng = (double)(end - beg);
     const double mscale = own_w / ng + mw;
     double pf = 0.0, pl = 0.0, ps = 0.0, p1 = 0.0, psc = 0.0, smin = INFINITY;
     if (active) {
-        double Gi[RW], mt[RW], cacc[RW], gacc[RW];
+        double cacc[RW], gacc[RW];
+        A gterm[RW], mt[RW];  // mean_w·G_t[i,g] (solver.cpp:72), m̃_g[i]
 #pragma unroll
         for (int w = 0; w < RW; ++w) {
-            Gi[w] = Gc[(int64_t)g * d + i + w];
-            mt[w] = Gi[w] * mscale;
+            const double Gi = Gc[(int64_t)g * d + i + w];
+            gterm[w] = (A)(mw * Gi);
+            mt[w] = (A)(Gi * mscale);
             cacc[w] = 0.0;
             gacc[w] = 0.0;
         }
@@ -184,40 +212,45 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
         for (int t = beg; t < beg + U; ++t) issue(t);
         for (int t0 = beg; t0 < end; t0 += B) {
             cp_wait<U - B>();
-            double xs[B][RW], ss[B][RW], ts[B][RW], lo[B][RW];
+            A xs[B][RW], ss[B][RW], ts[B][RW], lo[B][RW];
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 const int slot = (t0 + u - beg) % U;
 #pragma unroll
                 for (int w = 0; w < RW; ++w) {
-                    xs[u][w] = (double)ring[slot][0][tid * RW + w];
-                    ss[u][w] = (double)ring[slot][1][tid * RW + w];
-                    ts[u][w] = (double)ring[slot][2][tid * RW + w];
-                    lo[u][w] = (double)ring[slot][3][tid * RW + w];
+                    xs[u][w] = (A)ring[slot][0][tid * RW + w];
+                    ss[u][w] = (A)ring[slot][1][tid * RW + w];
+                    ts[u][w] = (A)ring[slot][2][tid * RW + w];
+                    lo[u][w] = (A)ring[slot][3][tid * RW + w];
                 }
             }
             // this thread's reads of the B slots are done before they refill
 #pragma unroll
             for (int u = 0; u < B; ++u) issue(t0 + U + u);
-            double ln[B][RW], sn[B][RW], tn[B][RW], rr[B][RW], sm[B][RW], mg[B][RW];
+            A ln[B][RW], sn[B][RW], tn[B][RW], rr[B][RW], sm[B][RW], mg[B][RW];
 #pragma unroll
             for (int u = 0; u < B; ++u)
 #pragma unroll
                 for (int w = 0; w < RW; ++w) {
-                    // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
-                    const double x = xs[u][w], s = ss[u][w], th = ts[u][w];
-                    const double q = sizeof(T) == 8 ? th / rho : th * thr;  // fp32 storage: reciprocal (1e-4 tolerance)
-                    const double dv = (x - s) + q;
-                    ln[u][w] = own_w * dv + mw * Gi[w];
-                    const double xl = x - ln[u][w];
-                    const double b = xl + q;
-                    const double mag = fabs(b) - thr;
-                    mg[u][w] = fabs(mag);
-                    sn[u][w] = mag > 0.0 ? copysign(mag, b) : 0.0;
+                    // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (the reference's op order)
+                    const A x = xs[u][w], s = ss[u][w], th = ts[u][w];
+                    A q;
+                    if constexpr (sizeof(T) == 8) q = th / rho;
+                    else q = th * thr_a;  // fp32 storage: reciprocal (1e-4 tolerance)
+                    const A dv = (x - s) + q;
+                    ln[u][w] = own_a * dv + gterm[w];
+                    const A xl = x - ln[u][w];
+                    const A b = xl + q;
+                    const A mag = abs_a(b) - thr_a;
+                    mg[u][w] = abs_a(mag);
+                    sn[u][w] = mag > (A)0 ? copysign_a(mag, b) : (A)0;
                     rr[u][w] = xl - sn[u][w];
-                    tn[u][w] = th + rho * rr[u][w];
-                    sm[u][w] = (x - sn[u][w]) + (sizeof(T) == 8 ? tn[u][w] / rho_n : tn[u][w] * irn);
+                    tn[u][w] = th + rho_a * rr[u][w];
+                    if constexpr (sizeof(T) == 8) sm[u][w] = (x - sn[u][w]) + tn[u][w] / rho_n;
+                    else sm[u][w] = (x - sn[u][w]) + tn[u][w] * irn_a;
                 }
+            // residual partials of the batch in the arithmetic type, widened once per batch
+            A bf = (A)0, bl = (A)0, bs = (A)0, b1 = (A)0, bsc = (A)0, bmin = (A)INFINITY;
 #pragma unroll
             for (int u = 0; u < B; ++u) {
                 if (t0 + u >= end) break;
@@ -225,42 +258,57 @@ __global__ void __launch_bounds__(NT) k_pass_f_ring(
                 const int64_t off = (int64_t)col * d + i;
 #pragma unroll
                 for (int w = 0; w < RW; ++w) {
-                    cacc[w] += ln[u][w];
-                    gacc[w] += sm[u][w];
-                    pf += rr[u][w] * rr[u][w];
-                    const double dl = ln[u][w] - lo[u][w];
-                    pl += dl * dl;
-                    const double ds = sn[u][w] - ss[u][w];
-                    ps += ds * ds;
-                    p1 += fabs(sn[u][w]);
-                    const double dm = ln[u][w] - mt[w];
-                    psc += dm * dm;
-                    smin = fmin(smin, mg[u][w]);
+                    cacc[w] += (double)ln[u][w];  // ascending member order (solver.cpp:64, kmeans.cpp:73)
+                    gacc[w] += (double)sm[u][w];
+                    const A dl = ln[u][w] - lo[u][w];
+                    const A ds = sn[u][w] - ss[u][w];
+                    const A dm = ln[u][w] - mt[w];
+                    if constexpr (F32A) {
+                        bf += rr[u][w] * rr[u][w];
+                        bl += dl * dl;
+                        bs += ds * ds;
+                        b1 += abs_a(sn[u][w]);
+                        bsc += dm * dm;
+                        bmin = min_a(bmin, mg[u][w]);
+                    } else {
+                        pf += rr[u][w] * rr[u][w];
+                        pl += dl * dl;
+                        ps += ds * ds;
+                        p1 += abs_a(sn[u][w]);
+                        psc += dm * dm;
+                        smin = fmin(smin, mg[u][w]);
+                    }
                 }
-                double a_l[RW], a_s[RW], a_t[RW];
-#pragma unroll
-                for (int w = 0; w < RW; ++w) {
-                    a_l[w] = ln[u][w];
-                    a_s[w] = sn[u][w];
-                    a_t[w] = tn[u][w];
-                }
-                Vec<T, RW>::store(L + off, a_l);
-                Vec<T, RW>::store(S + off, a_s);
-                Vec<T, RW>::store(Th + off, a_t);
+                store_row<T, RW, A>(L + off, ln[u]);
+                store_row<T, RW, A>(S + off, sn[u]);
+                store_row<T, RW, A>(Th + off, tn[u]);
                 if (Lb) {
                     __nv_bfloat16* lb = Lb + (int64_t)col * dpad + i;
                     if (RW >= 2) {
 #pragma unroll
                         for (int w = 0; w + 1 < RW; w += 2) {
                             __nv_bfloat162 b2;
-                            b2.x = __double2bfloat16(ln[u][w]);
-                            b2.y = __double2bfloat16(ln[u][w + 1]);
+                            if constexpr (F32A) {
+                                b2 = __floats2bfloat162_rn(ln[u][w], ln[u][w + 1]);
+                            } else {
+                                b2.x = __double2bfloat16(ln[u][w]);
+                                b2.y = __double2bfloat16(ln[u][w + 1]);
+                            }
                             *reinterpret_cast<__nv_bfloat162*>(lb + w) = b2;
                         }
                     } else {
-                        lb[0] = __double2bfloat16(ln[u][0]);
+                        if constexpr (F32A) lb[0] = __float2bfloat16(ln[u][0]);
+                        else lb[0] = __double2bfloat16(ln[u][0]);
                     }
                 }
+            }
+            if constexpr (F32A) {
+                pf += (double)bf;
+                pl += (double)bl;
+                ps += (double)bs;
+                p1 += (double)b1;
+                psc += (double)bsc;
+                smin = fmin(smin, (double)bmin);
             }
         }
         cp_wait<0>();
@@ -473,7 +521,7 @@ __global__ void __launch_bounds__(PFS_THREADS, NS <= 3 ? 3 : 2) k_pass_f_stream(
                 const T* ls = reinterpret_cast<const T*>(base + 3 * CPS * 16);
                 const int col = scol[(s % NS) * CPS + k];
                 const bool ok = col >= 0;
-                double lo_[VEC], so_[VEC], to_[VEC];
+                double lo_[VEC], so_[VEC], to_[VEC], gs_[VEC];
 #pragma unroll
                 for (int v = 0; v < VEC; ++v) {
                     // solver.cpp:163-164, 72, 172-173, 83-85, 107-108 (op order as k_pass_f)
@@ -488,10 +536,7 @@ __global__ void __launch_bounds__(PFS_THREADS, NS <= 3 ? 3 : 2) k_pass_f_stream(
                     const double r = xl - sn;
                     const double tn = th + rho * r;
                     if (ok) smin = fmin(smin, fabs(mag));
-                    // summand layout [2][member][row of the block]
-                    const int e = cmem[j] * rb_rows + csub[j] * VEC + v;
-                    sm_[e] = ln;
-                    sm_[CPS * VEC + e] = (x - sn) + (sizeof(T) == 8 ? tn / rho_n : tn * irn);
+                    gs_[v] = (x - sn) + (sizeof(T) == 8 ? tn / rho_n : tn * irn);
                     lo_[v] = ln;
                     so_[v] = sn;
                     to_[v] = tn;
@@ -504,6 +549,14 @@ __global__ void __launch_bounds__(PFS_THREADS, NS <= 3 ? 3 : 2) k_pass_f_stream(
                         p1 += fabs(sn);
                         const double dm = ln - mt[j][v];
                         psc += dm * dm;
+                    }
+                }
+                {   // summand layout [2][member][row of the block]; 16-byte stores (rb_rows % VEC == 0)
+                    const int e = cmem[j] * rb_rows + csub[j] * VEC;
+#pragma unroll
+                    for (int v = 0; v < VEC; v += 2) {
+                        *reinterpret_cast<double2*>(sm_ + e + v) = make_double2(lo_[v], lo_[v + 1]);
+                        *reinterpret_cast<double2*>(sm_ + CPS * VEC + e + v) = make_double2(gs_[v], gs_[v + 1]);
                     }
                 }
                 if (ok) {

@@ -111,25 +111,34 @@ struct Alm : AlmBase {
         return e && e[0] == '3';
     }();
     int stream_rb = 32, stream_nrb = 0;
-    int ring_cfg() const {  // RESPCA_RING_CFG = 5, 10 or 16 (tuning)
+    // fp32 storage: the element chain in FP32 arithmetic (k_pass_f_ring F32A);
+    // RESPCA_F32_ARITH=64 keeps the FP64 chain (A/B: C3-f32 0.69 -> 0.78 of HBM)
+    bool f32_arith = [] {
+        const char* e = std::getenv("RESPCA_F32_ARITH");
+        return !(e && std::atoi(e) == 64);
+    }();
+    int ring_cfg() const {  // RESPCA_RING_CFG (tuning)
         if (const char* e = std::getenv("RESPCA_RING_CFG")) {
             const int r = std::atoi(e);
-            if (r == 5 || ((r == 10 || r == 16) && d % 2 == 0) || ((r == 20 || r == 21) && sizeof(T) == 4 && d % 4 == 0))
+            if (r == 5 || ((r == 10 || r == 16) && d % 2 == 0) || (r == 33 && sizeof(T) == 4 && d % 4 == 0))
                 return r;
         }
         // measured on B200 (fraction of the HBM copy bandwidth):
         //  5: a row per thread, 4-deep ring, 2-member batches — few groups (C5 0.755)
-        //  10: two rows per thread, 128-thread CTAs, 4-deep — fp32 storage (C3-f32
-        //      0.71, C4 0.79) and fp64 up to 256 MB (C2 0.685)
+        //  10: two rows per thread, 128-thread CTAs, 4-deep — fp64 up to 256 MB
+        //      (C2 0.685), fp32 storage with d % 4 != 0
         //  16: two rows per thread, 256-thread CTAs, 8-deep, 4-member batches —
         //      fp64 larger (C3 0.926)
+        //  33: fp32 storage, four rows per thread (16-byte copies), 64-thread CTAs,
+        //      8-deep (C3-f32 0.78, C4 0.82; 8-byte copies: 0.71 / 0.79)
         if (d % 2 != 0 || c * ceil_div(d, 512) < 2 * 148) return 5;
-        if (sizeof(T) == 4 || (double)d * (double)n * sizeof(T) <= 256e6) return 10;
+        if (sizeof(T) == 4) return d % 4 == 0 ? 33 : 10;
+        if ((double)d * (double)n * sizeof(T) <= 256e6) return 10;
         return 16;
     }
     int ring_nt() const {  // rows per CTA of the ring variant
         const int r = ring_cfg();
-        return r == 16 || r == 20 || r == 21 ? 512 : r == 10 ? 256 : 64;
+        return r == 16 ? 512 : (r == 10 || r == 33) ? 256 : 64;
     }
     DBuf<T> X, L, S, Th;
     DBuf<double> G, Cw, Ck, mean_w, partials, rep, marg, nrm, bn;
@@ -355,8 +364,12 @@ struct Alm : AlmBase {
                 const int64_t ns = (int64_t)c * ceil_div(d, (int64_t)r);
                 const int64_t waves = ceil_div(ns, slots);
                 const double fill = (double)ns / (double)(waves * slots);
-                // a stream needs enough rows for whole 128-byte lines (r·s ≥ 128)
-                const double score = fill - (r * (int)sizeof(T) < 256 ? 0.05 : 0.0);
+                // a stream needs enough rows for whole 128-byte lines (r·s ≥ 128), and
+                // segments that start on 64-byte boundaries: DRAM moves 64 bytes at a
+                // time (C3-c1: rb = 34 → 0.66 of HBM with 12 % more DRAM reads than
+                // algorithmic, rb = 40 → 0.74; rb = 36 0.64, 42 0.54 — measured)
+                const double score = fill - (r * (int)sizeof(T) < 256 ? 0.05 : 0.0) -
+                                     ((r * (int)sizeof(T)) % 64 != 0 ? 0.25 : 0.0);
                 if (score >= best) {
                     best = score;
                     stream_rb = r;
@@ -560,10 +573,19 @@ struct Alm : AlmBase {
             // the three configurations ring_cfg() chooses from (RESPCA_RING_CFG: the
             // tuning sweep's numbering, kept for reproducibility)
             const int rc = ring_cfg();
-            if constexpr (sizeof(T) == 4) {  // fp32 storage: four rows per thread, 16-byte copies
-                if (rc == 20 || rc == 21) {
-                    if (rc == 20) go(k_pass_f_ring<T, 8, 128, 1, 4>, 128, 8, 4);
-                    else go(k_pass_f_ring<T, 8, 128, 2, 4>, 128, 8, 4);
+            if constexpr (sizeof(T) == 4) {
+                if (f32_arith) {
+                    switch (rc) {
+                        case 33: go(k_pass_f_ring<T, 8, 64, 2, 4, true>, 64, 8, 4); break;
+                        case 10: go(k_pass_f_ring<T, 4, 128, 2, 2, true>, 128, 4, 2); break;
+                        case 16: go(k_pass_f_ring<T, 8, 256, 4, 2, true>, 256, 8, 2); break;
+                        default: go(k_pass_f_ring<T, 4, 64, 2, 1, true>, 64, 4); break;
+                    }
+                    ln.add();
+                    return;
+                }
+                if (rc == 33) {
+                    go(k_pass_f_ring<T, 8, 64, 2, 4>, 64, 8, 4);
                     ln.add();
                     return;
                 }
