@@ -1577,8 +1577,9 @@ int respca_cu_group_scatter(respca_cu_ctx* ctx, const double* m, uint64_t d, uin
         CK(cudaMemcpyAsync(dl.p, lab.data(), sizeof(int) * n, cudaMemcpyHostToDevice, ctx->st));
         km.means(cen.p);  // column_mean per group, matrix.cpp:63-79
         // per-group sequential sums in the reference's order: groups, then members
-        k_own_exact<double><<<ceil_div(n, 128), 128, 0, ctx->st>>>(km.M, cen.p, d, (int)n, dl.p,
-                                                                  km.own.p);
+        smem_at_least((const void*)k_own_exact<double>, own_exact_smem<double>());
+        k_own_exact<double><<<ceil_div(n, 32 * OWN_W), 32 * OWN_W, own_exact_smem<double>(), ctx->st>>>(
+            km.M, cen.p, d, (int)n, dl.p, km.own.p);
         ctx->launches++;
         std::vector<double> own(n);
         CK(cudaMemcpyAsync(own.data(), km.own.p, sizeof(double) * n, cudaMemcpyDeviceToHost,

@@ -1066,30 +1066,73 @@ __global__ void __launch_bounds__(64) k_pp_d2_multi(const T* __restrict__ M, int
 }
 
 // Exact own-centroid distance sq_dist(col_j, C[:, label_j]) for every column
-// (inertia_of, kmeans.cpp:84-91; repair_empty, kmeans.cpp:51).
+// (inertia_of, kmeans.cpp:84-91; repair_empty, kmeans.cpp:51).  Lane = column:
+// each lane runs its column's chain in ascending i (the reference's order) on
+// 32×32 tiles of the 32 columns and of their 32 own centroids, both streamed
+// through a cp.async ring (coalesced 32-element rows), so the chain never
+// waits on a global load — it is the d dependent adds per column that bound
+// the kernel (C3: 5 ms → 0.3 ms per restart at the end of kmeans(X)).
+constexpr int OWN_PD = 4, OWN_W = 2;
 template <typename T>
-__global__ void __launch_bounds__(128) k_own_exact(const T* __restrict__ M,
-                                                   const double* __restrict__ C, int64_t d, int n,
-                                                   const int* __restrict__ labels,
-                                                   double* __restrict__ out) {
-    __shared__ double tile[4][32][33];
+constexpr size_t own_exact_smem() {
+    return (size_t)OWN_W * OWN_PD * 32 * 33 * (sizeof(T) + sizeof(double));
+}
+template <typename T>
+__global__ void __launch_bounds__(OWN_W * 32) k_own_exact(const T* __restrict__ M,
+                                                          const double* __restrict__ C, int64_t d, int n,
+                                                          const int* __restrict__ labels,
+                                                          double* __restrict__ out) {
+    extern __shared__ __align__(16) unsigned char own_sm[];
+    auto tile = reinterpret_cast<T(*)[OWN_PD][32][33]>(own_sm);  // [W][PD][column][row]
+    auto ctile = reinterpret_cast<double(*)[OWN_PD][32][33]>(own_sm + sizeof(T) * OWN_W * OWN_PD * 32 * 33);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int j0 = (blockIdx.x * 4 + w) * 32;
+    const int j0 = (blockIdx.x * OWN_W + w) * 32;
     if (j0 >= n) return;
     const int j = j0 + lane;
-    const double* cv = C + (int64_t)(j < n ? labels[j] : 0) * d;
-    double s = 0.0;
-    for (int64_t i0 = 0; i0 < d; i0 += 32) {
-        const int64_t i = i0 + lane;
-        for (int cc = 0; cc < 32; ++cc) {
-            const int jj = j0 + cc;
-            tile[w][cc][lane] = (jj < n && i < d) ? (double)M[(int64_t)jj * d + i] : 0.0;
+    const int64_t ntile = (d + 31) / 32;
+    int64_t moff[32], coff[32];  // column q of the tile: its data and its own centroid
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+        const int jj = j0 + q < n ? j0 + q : j0;
+        moff[q] = (int64_t)jj * d;
+        coff[q] = (int64_t)__ldg(labels + jj) * d;
+    }
+    auto issue = [&](int64_t t) {
+        const int slot = (int)(t % OWN_PD);
+        const int64_t i = t * 32 + lane;
+        const bool ok = i < d;
+#pragma unroll
+        for (int q = 0; q < 32; ++q) {
+            const T* src = ok ? M + moff[q] + i : M;
+            if (sizeof(T) == 8) cp_async8(&tile[w][slot][q][lane], src, ok);
+            else cp_async4(&tile[w][slot][q][lane], src, ok);
+            cp_async8(&ctile[w][slot][q][lane], ok ? C + coff[q] + i : C, ok);
         }
+        cp_commit();
+    };
+    for (int64_t t = 0; t < OWN_PD - 1; ++t) {
+        if (t < ntile) issue(t);
+        else cp_commit();
+    }
+    double s = 0.0;
+    for (int64_t t = 0; t < ntile; ++t) {
+        if (t + OWN_PD - 1 < ntile) issue(t + OWN_PD - 1);
+        else cp_commit();
+        cp_wait<OWN_PD - 1>();
         __syncwarp();
-        const int lim = (int)((d - i0) < 32 ? (d - i0) : 32);
-        for (int r = 0; r < lim; ++r) {
-            const double t = tile[w][lane][r] - __ldg(cv + i0 + r);
-            s += t * t;
+        const int slot = (int)(t % OWN_PD);
+        const int lim = (int)((d - t * 32) < 32 ? (d - t * 32) : 32);
+        if (lim == 32) {
+#pragma unroll
+            for (int r = 0; r < 32; ++r) {
+                const double tt = (double)tile[w][slot][lane][r] - ctile[w][slot][lane][r];  // kmeans.cpp:15-16
+                s += tt * tt;
+            }
+        } else {
+            for (int r = 0; r < lim; ++r) {
+                const double tt = (double)tile[w][slot][lane][r] - ctile[w][slot][lane][r];
+                s += tt * tt;
+            }
         }
         __syncwarp();
     }

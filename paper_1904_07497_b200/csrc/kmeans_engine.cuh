@@ -429,7 +429,7 @@ struct KMeansEngine {
         if (!empty) return;
         CK(cudaMemcpyAsync(counts.p, groups.counts.data(), sizeof(int) * c,
                            cudaMemcpyHostToDevice, st));
-        k_own_exact<T><<<ceil_div(n, 128), 128, 0, st>>>(M, C, d, n, labels, own.p);
+        launch_own_exact(C, labels);
         CK(cudaMemsetAsync(errflag.p, 0, sizeof(int), st));
         k_repair<T><<<1, 1024, 0, st>>>(M, C, d, n, c, labels, counts.p, own.p, errflag.p);
         ln.add(2);
@@ -1006,9 +1006,13 @@ struct KMeansEngine {
 
     void k_col_sq_fma_T(const T* m, int cols, double* out);
 
+    void launch_own_exact(const double* C, const int* labels) {
+        smem_at_least((const void*)k_own_exact<T>, own_exact_smem<T>());
+        k_own_exact<T><<<ceil_div(n, 32 * OWN_W), 32 * OWN_W, own_exact_smem<T>(), st>>>(M, C, d, n, labels, own.p);
+    }
     // inertia_of (kmeans.cpp:84-91): exact per-column chains, sequential host sum
     double inertia(const double* C, const int* labels) {
-        k_own_exact<T><<<ceil_div(n, 128), 128, 0, st>>>(M, C, d, n, labels, own.p);
+        launch_own_exact(C, labels);
         ln.add();
         std::vector<double> h(n);
         CK(cudaMemcpyAsync(h.data(), own.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
