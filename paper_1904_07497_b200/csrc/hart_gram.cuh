@@ -34,6 +34,8 @@
 #pragma once
 
 #include "km.cuh"
+#include "tc_screen.cuh"  // mbarrier helpers
+#include "hartigan.cuh"   // bulk_g2s
 
 namespace respca_dev {
 
@@ -806,6 +808,530 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
         if (tid == 0) --cnt[pf];
         if (tid == 32) ++cnt[pt];
     }
+    __syncthreads();
+    if (rank == 0) {
+        for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];
+        if (tid == 0) {
+            a.stats[0] = moves;
+            a.stats[1] = (unsigned long long)pass;
+            a.stats[2] = windows;
+            a.stats[3] = fallbacks;
+            a.stats[4] = replay_work;
+            for (int q = 0; q < 8; ++q) a.stats[5 + q] = tph[q];
+        }
+    }
+    gcl_sync();  // no CTA leaves while another may still read its shared memory
+}
+
+// ---------------------------------------------------------------------------
+// k_hart_gram2: the same refinement with the window's data resident on chip.
+//
+// k_hart_gram stages every window's Ŝ block from L2 (columns move between CTAs
+// as the window start moves), so each window pays an L2 round trip before it
+// can decide, and every CTA's global Ŝ stores must be fenced cluster-wide for
+// the others.  Here column ownership is fixed: columns are dealt to the CTAs in
+// groups of GW = GRAM_WARPS (group g → CTA g mod CL), so ANY window of
+// W = GW·CL consecutive columns holds exactly GW columns of every CTA (one
+// whole group, or the two partial groups of the CTA straddling the window
+// start).  Each CTA keeps, in shared memory, for its current and next group:
+//   * Ŝ_k[j] of the group's columns for every centroid k,
+//   * the Ĝ row segments Ĝ[j][J0 − 2W .. J0 + W + GW) of its columns — every
+//     column that can move while the group is cached,
+//   * label, Ĝ_jj and the norm bounds,
+// loaded with cp.async one group-stride (≈ five windows) ahead.  The elected
+// move is applied to the cached groups from shared memory (Ŝ_from −= Ĝ[j][m],
+// Ŝ_to += Ĝ[j][m], one rounded operation each — the arithmetic of k_hart_gram)
+// and to the CTA's other columns in global memory, which only this CTA ever
+// reads or writes.  A window is then: patch (shared memory) → decide → push the
+// CTA's first candidate → cluster barrier → elect the lowest column; no load
+// from L2 sits on that path.  Decisions, fallbacks and results are those of
+// k_hart_gram (same intervals, same exact fallback), so the labels are the
+// reference's.
+// ---------------------------------------------------------------------------
+// asynchronous store into another CTA's shared memory that completes bytes on
+// that CTA's mbarrier: the receiver's mbarrier wait orders the data, no
+// cluster-wide fence or barrier is involved
+RESPCA_DEV void gcl_st_async_b64(uint32_t remote_addr, uint64_t v, uint32_t remote_bar) {
+    asm volatile("st.async.weak.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];\n" ::"r"(remote_addr),
+                 "l"(v), "r"(remote_bar)
+                 : "memory");
+}
+
+template <typename T, int KPL>
+__global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram2(GramArgs a) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    const int c = a.c, n = a.n;
+    const int64_t d = a.d;
+    constexpr int GW = GRAM_WARPS;
+    constexpr int MVW = 5;  // a move's inputs: Ŝ_from[j], Ŝ_to[j], Ĝ_jj, ‖x_j‖ upper / lower bound
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int rank = (int)gcl_rank(), CL = (int)gcl_size();
+    const int W = GW * CL;
+    const int LCL = __ffs(CL) - 1, LW = LCL + 3;  // CL is a power of two (host): divisions by CL, W are shifts
+    static_assert(GW == 8, "LW = log2(GW·CL)");
+    constexpr int NSL = 3;      // cached groups per CTA: the blocks of the window and the next one
+    const int GL = 4 * W;       // cached Ĝ row segment of block m's group: columns (m − 2)W .. (m + 2)W − 1
+    const int CS = (c + 1) & ~1;
+    GramCoef* cf = reinterpret_cast<GramCoef*>(sm);
+    GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
+    double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
+    int* cnt = reinterpret_cast<int*>(dist + c);
+    double* scache = reinterpret_cast<double*>(
+        (reinterpret_cast<uintptr_t>(cnt + ((c + 1) & ~1)) + 15) & ~(uintptr_t)15);  // [NSL][GW][CS]
+    double* gseg = scache + (size_t)NSL * GW * CS;                                   // [NSL][GW][GL]
+    __shared__ int clab[NSL][GW];
+    __shared__ double cxx[NSL][GW], cxn[NSL][GW], cxl[NSL][GW];
+    __shared__ int s_loc[GW];                  // this CTA's verdicts: status | to << 2 | from << 17
+    __shared__ double s_sv[GW][MVW];           // this CTA's candidates' move inputs
+    // every CTA's first candidate of the window: word 0 = verdict | column << 32,
+    // words 1..5 = the move's inputs; written by st.async from every CTA, each
+    // store completing 8 bytes on this CTA's mbarrier xbar[parity]
+    constexpr int XW = 1 + MVW;
+    __shared__ __align__(16) unsigned long long s_xch[2][GRAM_MAXCL][XW];
+    __shared__ __align__(8) uint64_t xbar[2];
+    __shared__ __align__(8) uint64_t gbar;  // the Ĝ row segments of a group load (bulk copies)
+    __shared__ int s_xres;        // exact fallback verdict (CTA 0)
+    __shared__ double s_xsv[MVW];  // ... and the move's inputs (the column's owner)
+    const T* M = static_cast<const T*>(a.M);
+    const double gamG = a.gamG, gamc = a.gamc;
+    // this CTA's groups: m = 0 .. NG − 1, group m = columns J0(m) .. J0(m) + GW − 1 of
+    // block m = columns mW .. (m + 1)W − 1.  Cached: the groups of blocks cur, cur + 1
+    // (any window starting in block cur lies inside them) and cur + 2 (loaded one
+    // block ahead); every CTA rotates in the same window, when the cursor enters the
+    // next block, so no CTA waits at the cluster barrier for another's rotation
+    const int ngroups = (n + GW - 1) / GW;
+    const int NG = rank < ngroups ? (ngroups - rank + CL - 1) / CL : 0;
+    auto J0 = [&](int m) { return (m * CL + rank) * GW; };
+    constexpr int UPT = 3;  // far columns per thread held across the window
+
+    for (int k = tid; k < c; k += blockDim.x) {
+        const int ck = a.counts[k];
+        cnt[k] = ck;
+        sc[k] = a.scal0[k];
+        gram_coef(sc[k], ck, cf[k]);
+    }
+    if (tid == 0) {
+        mbar_init(&xbar[0], 1);  // one arrival per window: this CTA's expect_tx
+        mbar_init(&xbar[1], 1);
+        mbar_init(&gbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    __syncthreads();
+    gcl_sync();  // every replica and mbarrier initialised before remote stores land
+    unsigned xph[2] = {0, 0};  // completed phases of xbar[0], xbar[1]
+    unsigned gph = 0;          // completed phases of gbar
+    const bool gbulk = (n & 1) == 0 && (reinterpret_cast<uintptr_t>(a.G) & 15) == 0;  // 16-byte aligned rows
+
+    unsigned long long moves = 0, windows = 0, fallbacks = 0, replay_work = 0;
+    unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long tmk = clock64();
+    auto lap = [&](int slot) {
+        if (tid == 0) {
+            const unsigned long long t = clock64();
+            tph[slot] += t - tmk;
+            tmk = t;
+        }
+    };
+    uint32_t gbytes = 0;  // thread 0: bytes of the bulk copies issued since the last commit
+    // group m's Ŝ columns, Ĝ row segments and per-column scalars → shared memory (cp.async / bulk copies)
+    auto load_group = [&](int m) {
+        if (m >= NG) return;
+        const int slot = m % NSL, j0 = J0(m);
+        for (int e = tid; e < c * GW; e += GRAM_THREADS) {
+            const int k = e / GW, col = e - k * GW;
+            const bool ok = j0 + col < n;
+            cp_async8(&scache[(size_t)(slot * GW + col) * CS + k], ok ? a.S + (int64_t)k * n + j0 + col : a.S, ok);
+        }
+        const int base = (m - 2) * W;
+        if (gbulk) {  // one bulk copy per column (thread 0 issues them; gbar counts the bytes)
+            if (tid == 0) {
+                const int q0 = base < 0 ? -base : 0, q1 = base + GL > n ? n - base : GL;  // even: W, n even
+                for (int col = 0; col < GW; ++col)
+                    if (j0 + col < n && q1 > q0) {
+                        bulk_g2s(&gseg[(size_t)(slot * GW + col) * GL + q0], a.G + (int64_t)(j0 + col) * n + base + q0,
+                                 (uint32_t)(q1 - q0) * 8u, &gbar);
+                        gbytes += (uint32_t)(q1 - q0) * 8u;
+                    }
+            }
+        } else {
+            for (int e = tid; e < GW * GL; e += GRAM_THREADS) {
+                const int col = e / GL, q = e - col * GL;
+                const int jq = base + q;
+                const bool ok = j0 + col < n && jq >= 0 && jq < n;
+                cp_async8(&gseg[(size_t)(slot * GW + col) * GL + q], ok ? a.G + (int64_t)(j0 + col) * n + jq : a.G, ok);
+            }
+        }
+        if (tid < GW) {  // per-column scalars, asynchronously too (a plain load would stall this warp for an L2 round trip)
+            const int j = j0 + tid;
+            const bool ok = j < n;
+            cp_async4(&clab[slot][tid], ok ? a.labels + j : a.labels, ok);
+            cp_async8(&cxx[slot][tid], ok ? a.xx + j : a.xx, ok);
+            cp_async8(&cxn[slot][tid], ok ? a.xn + j : a.xn, ok);
+            cp_async8(&cxl[slot][tid], ok ? a.xl + j : a.xl, ok);
+        }
+    };
+    auto writeback_group = [&](int m) {
+        if (m >= NG) return;
+        const int slot = m % NSL, j0 = J0(m);
+        for (int e = tid; e < c * GW; e += GRAM_THREADS) {
+            const int k = e / GW, col = e - k * GW;
+            if (j0 + col < n) __stcg(a.S + (int64_t)k * n + j0 + col, scache[(size_t)(slot * GW + col) * CS + k]);
+        }
+    };
+    // the pending move on the cached groups (one thread per cached column); the
+    // replicas took it when it was elected
+    auto patch_cached = [&](int cur, int pj, int pf, int pt, const double (&pmv)[5]) {
+        if (tid < NSL * GW) {
+            const int gi = tid / GW, col = tid - gi * GW, m = cur + gi;
+            if (m < NG && J0(m) + col < n) {
+                const int slot = m % NSL;
+                const double g = gseg[(size_t)(slot * GW + col) * GL + (pj - (m - 2) * W)];
+                double* sv = &scache[(size_t)(slot * GW + col) * CS];
+                sv[pf] = sv[pf] - g;
+                sv[pt] = sv[pt] + g;
+                if (J0(m) + col == pj) clab[slot][col] = pt;
+            }
+        }
+    };
+    // e-th far column of this CTA (its columns outside the cached groups cur .. cur + 2), or −1
+    auto far_col = [&](int e, int cur) -> int {
+        const int gi = e / GW;
+        if (gi >= NG || (gi >= cur && gi <= cur + 2)) return -1;
+        const int q = J0(gi) + (e - gi * GW);
+        return q < n ? q : -1;
+    };
+
+    bool loading = false;  // a group load is outstanding
+    auto commit_load = [&]() {
+        cp_commit();
+        if (gbulk && tid == 0) {
+            if (gbytes) mbar_expect_tx_cta(&gbar, gbytes);
+            else mbar_arrive(&gbar);
+            gbytes = 0;
+        }
+        loading = true;
+    };
+    auto finish_load = [&]() {  // all threads: the outstanding group load has landed
+        cp_wait<0>();
+        if (gbulk) {
+            if (!mbar_wait(&gbar, gph & 1u)) asm volatile("trap;\n");
+            ++gph;
+        }
+        __syncthreads();
+        loading = false;
+    };
+    int nlog = 0, replayed = 0, pass = 0, par = 0;
+    int pj = -1, pf = 0, pt = 0;  // the pending move (uniform over the cluster)
+    double pmv[5] = {0, 0, 0, 0, 0};
+    int cur = -1;           // current block (−1: nothing cached)
+    for (;;) {
+        // ---- pass start: drain the pending move, write the cached groups back, cache groups 0, 1, 2
+        {
+            if (loading) finish_load();  // never two group loads outstanding
+            if (pj >= 0) {
+                for (int e = tid; e < NG * GW; e += GRAM_THREADS) {
+                    const int q = far_col(e, cur);
+                    if (q >= 0) {
+                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
+                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
+                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
+                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
+                    }
+                }
+                patch_cached(cur, pj, pf, pt, pmv);
+                ++nlog;
+                pj = -1;
+            }
+            __syncthreads();
+            if (cur >= 0) {
+                writeback_group(cur);
+                writeback_group(cur + 1);
+                writeback_group(cur + 2);
+            }
+            __syncthreads();
+            cur = 0;
+            load_group(0);
+            load_group(1);
+            load_group(2);
+            commit_load();
+            finish_load();
+        }
+        int improved = 0;
+        int cursor = 0;
+        while (cursor < n) {
+            const bool mv = pj >= 0;
+            const int fcur = cur;
+            if (loading) finish_load();  // the group loaded at the last block change (a window ago at least)
+            // ---- (1) the pending move: far columns loaded, cached columns patched in shared memory
+            double ug[UPT], uf[UPT], ut[UPT];
+            int uq[UPT];
+            if (mv) {
+#pragma unroll
+                for (int e = 0; e < UPT; ++e) {
+                    uq[e] = far_col(tid + e * GRAM_THREADS, cur);
+                    if (uq[e] >= 0) {
+                        ug[e] = __ldcg(a.G + (int64_t)pj * n + uq[e]);
+                        uf[e] = __ldcg(a.S + (int64_t)pf * n + uq[e]);
+                        ut[e] = __ldcg(a.S + (int64_t)pt * n + uq[e]);
+                    }
+                }
+                patch_cached(cur, pj, pf, pt, pmv);
+                ++nlog;
+            }
+            lap(2);
+            __syncthreads();
+            // ---- (3) this warp's column of the window: the warp-th of this CTA's columns in it
+            int j = n;
+            {
+                const int g0 = cursor / GW, o = cursor - g0 * GW;
+                const int dg = (rank - g0) & (CL - 1);
+                if (dg == 0 && o > 0) j = warp < GW - o ? cursor + warp : (g0 + CL) * GW + (warp - (GW - o));
+                else j = (g0 + dg) * GW + warp;
+                if (j >= n) j = n;
+            }
+            const int jm = j < n ? j >> LW : cur;  // the column's block: cur or cur + 1, both landed
+            int st = 0, to = -1, from = 0;
+            if (j < n) {
+                const int slot = jm % NSL, col = j - (j / GW) * GW;
+                from = clab[slot][col];
+                const double gjj = cxx[slot][col], xnj = cxn[slot][col];
+                const double* svp = &scache[(size_t)(slot * GW + col) * CS];
+                double sv[KPL];
+#pragma unroll
+                for (int q = 0; q < KPL; ++q) {
+                    const int k = lane + 32 * q;
+                    sv[q] = k < c ? svp[k] : 0.0;
+                }
+                if (cnt[from] > 1) {
+                    GramCol colv;
+                    colv.gjj = gjj;
+                    colv.xnj = xnj;
+                    colv.gq = gamG * xnj * xnj * (1.0 + 4.0 * kU) + 7.1 * kU * gjj;
+                    double lo[KPL], hi[KPL], mid[KPL];
+#pragma unroll
+                    for (int q = 0; q < KPL; ++q) {
+                        const int k = lane + 32 * q;
+                        if (k < c) gram_iv(colv, cf[k], sv[q], gamc, lo[q], hi[q], mid[q]);
+                        else lo[q] = hi[q] = mid[q] = INFINITY;
+                    }
+                    st = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, to);
+                    if (a.force_exact && st == 1) st = 2;
+                    if (st != 0 && lane == 0) {
+                        // a candidate: its Ĝ row (every CTA's far update) to L2
+                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.G + (int64_t)j * n);
+                        const uintptr_t s0 = b0 & ~(uintptr_t)15;
+                        const unsigned bytes = (unsigned)((b0 + (uintptr_t)n * 8 - s0 + 15) & ~(uintptr_t)15);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s0), "r"(bytes) : "memory");
+                    }
+                    if (st == 1 && lane == 0) {  // the move's inputs
+                        s_sv[warp][0] = svp[from];
+                        s_sv[warp][1] = svp[to];
+                        s_sv[warp][2] = gjj;
+                        s_sv[warp][3] = xnj;
+                        s_sv[warp][4] = cxl[slot][col];
+                    }
+                }
+            }
+            lap(4);
+            // ---- (4) this warp's verdict; the CTA's first candidate → every CTA
+            if (lane == 0) s_loc[warp] = st | ((to < 0 ? 0 : to) << 2) | (from << 17);
+            __syncthreads();
+            {
+                const int v = lane < GW ? s_loc[lane] : 0;
+                const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
+                const int fw = bal ? __ffs(bal) - 1 : 0;  // warps are in column order
+                if (warp == fw) {
+                    const int fv = __shfl_sync(0xffffffffu, v, fw);
+                    const unsigned long long vw =
+                        (unsigned long long)(unsigned)(bal ? fv : 0) | ((unsigned long long)(unsigned)j << 32);
+                    // CL·XW words, always all of them (every CTA expects CL·XW·8 bytes per
+                    // window), spread over the warp's lanes: word q of receiver r
+                    for (int e = lane; e < CL * XW; e += 32) {
+                        const int r = e / XW, q = e - r * XW;
+                        const unsigned long long word =
+                            q == 0 ? vw
+                                   : ((fv & 3) == 1 ? (unsigned long long)__double_as_longlong(s_sv[fw][q - 1]) : 0ull);
+                        gcl_st_async_b64(gcl_map(&s_xch[par][rank][q], (uint32_t)r), word,
+                                         gcl_map(&xbar[par], (uint32_t)r));
+                    }
+                }
+                if (tid == 0) mbar_expect_tx_cta(&xbar[par], (uint32_t)(CL * XW * 8));
+            }
+            lap(5);
+            // the far stores and the block change ride in the shadow of the exchange
+            // ---- (3b) far stores: their loads were issued at the window's start and have
+            //      landed behind the decide; nothing below waits for them (no fence)
+            if (mv) {
+#pragma unroll
+                for (int e = 0; e < UPT; ++e)
+                    if (uq[e] >= 0) {
+                        __stcg(a.S + (int64_t)pf * n + uq[e], uf[e] - ug[e]);
+                        __stcg(a.S + (int64_t)pt * n + uq[e], ut[e] + ug[e]);
+                    }
+                for (int e = tid + UPT * GRAM_THREADS; e < NG * GW; e += GRAM_THREADS) {
+                    const int q = far_col(e, fcur);
+                    if (q >= 0) {
+                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
+                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
+                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
+                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
+                    }
+                }
+                pj = -1;
+            }
+            lap(1);
+            // ---- (3c) the cursor entered the next block (every CTA in this same window): the
+            //      old block's group goes back to global memory, its slot takes block cur + 3's
+            //      group — after the far stores above, under which it was still a far group
+            if ((cursor >> LW) > cur) {
+                writeback_group(cur);
+                __syncthreads();  // far stores and write-back issued; the slot's readers are done
+                ++cur;
+                load_group(cur + 2);
+                commit_load();
+            }
+            lap(3);
+            if (!mbar_wait(&xbar[par], xph[par] & 1u)) asm volatile("trap;\n");  // a lost exchange: abort, never hang
+            ++xph[par];
+            lap(6);
+            // ---- (5) every warp: the window's first candidate = the lowest column
+            int pr = -1, jj = 0x7fffffff, w = 0;
+            {
+                const unsigned long long vw = lane < CL ? s_xch[par][lane][0] : 0ull;
+                const int v = (int)(unsigned)(vw & 0xffffffffull);
+                const int jc = lane < CL && (v & 3) != 0 ? (int)(unsigned)(vw >> 32) : 0x7fffffff;
+                int bj = jc, br = lane;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int oj = __shfl_xor_sync(0xffffffffu, bj, o), orr = __shfl_xor_sync(0xffffffffu, br, o);
+                    if (oj < bj) {
+                        bj = oj;
+                        br = orr;
+                    }
+                }
+                if (bj != 0x7fffffff) {
+                    pr = br;
+                    jj = bj;
+                    w = (int)(unsigned)(s_xch[par][pr][0] & 0xffffffffull);
+                }
+            }
+            ++windows;
+            lap(0);
+            if (pr < 0) {
+                cursor += W;
+                par ^= 1;
+                continue;
+            }
+            cursor = jj + 1;
+            const int mfrom = w >> 17;
+            int mst = w & 3, mto = (w >> 2) & 0x7fff;
+            double mvin[MVW];
+            if (mst == 1) {
+#pragma unroll
+                for (int q = 0; q < MVW; ++q) mvin[q] = __longlong_as_double((long long)s_xch[par][pr][1 + q]);
+            } else {
+                // ---- near-tie (CTA 0): the reference's own chain on the reference's
+                //      centroids (logged moves replayed, kmeans.cpp:128-129)
+                ++fallbacks;
+                if (rank == 0) {
+                    for (int64_t i = tid; i < d; i += blockDim.x) {
+                        for (int e = replayed; e < nlog; ++e) {
+                            const int* lg = a.log + 5 * (int64_t)e;
+                            const int m = __ldcg(lg), f = __ldcg(lg + 1), t = __ldcg(lg + 2);
+                            const double nf = (double)__ldcg(lg + 3), nt = (double)__ldcg(lg + 4);
+                            const double x = (double)M[(int64_t)m * d + i];
+                            double* cfp = a.Cs + (int64_t)f * d + i;
+                            double* ctp = a.Cs + (int64_t)t * d + i;
+                            *cfp = (*cfp * nf - x) / (nf - 1.0);
+                            *ctp = (*ctp * nt + x) / (nt + 1.0);
+                        }
+                    }
+                    __syncthreads();
+                    for (int k = tid; k < c; k += blockDim.x) {  // kmeans.cpp:12-19
+                        const T* x = M + (int64_t)jj * d;
+                        const double* ck = a.Cs + (int64_t)k * d;
+                        double s = 0.0;
+                        for (int64_t i = 0; i < d; ++i) {
+                            const double t = (double)x[i] - ck[i];
+                            s += t * t;
+                        }
+                        dist[k] = s;
+                    }
+                    __syncthreads();
+                    if (warp == 0) {
+                        double lo[KPL], hi[KPL], mid[KPL];
+#pragma unroll
+                        for (int q = 0; q < KPL; ++q) {
+                            const int k = lane + 32 * q;
+                            lo[q] = hi[q] = mid[q] = k < c ? dist[k] : INFINITY;
+                        }
+                        int t2 = -1;
+                        const int s2 = gram_decide<KPL>(mfrom, c, cf, cnt, lo, hi, mid, t2);
+                        if (lane == 0) s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;  // exact: 2 only for NaN
+                    }
+                }
+                replay_work += (unsigned long long)(nlog - replayed);
+                replayed = nlog;
+                gcl_sync();
+                const int xr = gcl_ld_i32(gcl_map(&s_xres, 0));
+                mst = xr & 3;
+                mto = xr >> 2;
+                // the move's inputs live in the column owner's cache
+                const int orank = (jj >> 3) & (CL - 1);
+                if (mst == 1 && rank == orank && tid == 0) {
+                    const int jm2 = jj >> LW, slot = jm2 % NSL, col = jj - (jj / GW) * GW;
+                    const double* svp = &scache[(size_t)(slot * GW + col) * CS];
+                    s_xsv[0] = svp[mfrom];
+                    s_xsv[1] = svp[mto];
+                    s_xsv[2] = cxx[slot][col];
+                    s_xsv[3] = cxn[slot][col];
+                    s_xsv[4] = cxl[slot][col];
+                }
+                gcl_sync();
+                if (mst == 1)
+#pragma unroll
+                    for (int q = 0; q < MVW; ++q) mvin[q] = gcl_ld_f64(gcl_map(&s_xsv[q], (uint32_t)orank));
+                gcl_sync();  // s_xsv / s_xres read before a later fallback rewrites them
+                lap(1);
+            }
+            if (mst == 1) {
+                // the last warp: the log (the counts before the move), then the replicas'
+                // per-centroid state — two lanes, identical inputs in every CTA → identical
+                // replicas — while the other warps go on to the next window's far loads and
+                // cache patch; nothing reads cf / cnt before the next window's first barrier
+                if (warp == GRAM_WARPS - 1) {
+                    if (lane == 0 && rank == 0) {
+                        int* lg = a.log + 5 * (int64_t)(nlog + (pj >= 0 ? 1 : 0));
+                        lg[0] = jj;
+                        lg[1] = mfrom;
+                        lg[2] = mto;
+                        lg[3] = cnt[mfrom];
+                        lg[4] = cnt[mto];
+                    }
+                    __syncwarp();
+                    if (lane < 2) {
+                        const int kk = lane ? mto : mfrom;
+                        gram_side(lane, sc[kk], cf[kk], cnt[kk], lane ? mvin[1] : mvin[0], mvin[2], mvin[3], mvin[4], gamG);
+                    }
+                }
+                if (tid == 0 && rank == ((jj >> 3) & (CL - 1))) __stcg(a.labels + jj, mto);
+#pragma unroll
+                for (int q = 0; q < MVW; ++q) pmv[q] = mvin[q];
+                lap(7);
+                pj = jj;
+                pf = mfrom;
+                pt = mto;
+                ++moves;
+                improved = 1;
+            }
+            par ^= 1;
+        }
+        ++pass;
+        if (!improved || pass >= a.max_pass) break;
+    }
+    // the last move's label and counts were taken when it was elected (its Ŝ
+    // update is no longer needed)
+    if (loading) finish_load();
     __syncthreads();
     if (rank == 0) {
         for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];

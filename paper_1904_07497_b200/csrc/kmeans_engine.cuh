@@ -840,14 +840,25 @@ struct KMeansEngine {
         // (16, non-portable, where available: C3 refinement 189 -> 176 ms vs 8)
         int CL = n >= 8192 ? 16 : std::max(1, std::min(8, n / 1024));
         if (const char* e = std::getenv("RESPCA_GRAM_CL")) CL = std::max(1, std::min(GRAM_MAXCL, std::atoi(e)));
+        // RESPCA_HART_GRAM2=0: the window-staging kernel (k_hart_gram); default: the
+        // resident-window kernel (k_hart_gram2: fixed column ownership, cached groups)
+        const bool resident = env_int("RESPCA_HART_GRAM2", 1) != 0;
+        if (resident)
+            while (CL & (CL - 1)) CL &= CL - 1;  // a power of two (the kernel's column → CTA map uses shifts)
+        auto smem_for = [&](int cl) -> size_t {
+            if (!resident) return sm;
+            const size_t cs = (size_t)((c + 1) & ~1), gl = (size_t)4 * GRAM_WARPS * cl;
+            return (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double)) + sizeof(int) * cs +
+                   sizeof(double) * (3 * GRAM_WARPS * cs + 3 * GRAM_WARPS * gl) + 80;
+        };
         auto launch = [&](auto kf) {
-            smem_at_least((const void*)kf, (size_t)(sm));
+            smem_at_least((const void*)kf, smem_for(CL));
             if (CL > 8) CK(cudaFuncSetAttribute((const void*)kf, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
             for (;; CL = std::max(1, CL / 2)) {
                 cudaLaunchConfig_t lc = {};
                 lc.gridDim = dim3(CL);
                 lc.blockDim = dim3(GRAM_THREADS);
-                lc.dynamicSmemBytes = sm;
+                lc.dynamicSmemBytes = smem_for(CL);
                 lc.stream = st;
                 cudaLaunchAttribute at[1];
                 at[0].id = cudaLaunchAttributeClusterDimension;
@@ -862,7 +873,12 @@ struct KMeansEngine {
                 (void)cudaGetLastError();  // cluster not schedulable: halve it
             }
         };
-        if (c <= 32) launch(k_hart_gram<T, 1>);
+        if (resident) {
+            if (c <= 32) launch(k_hart_gram2<T, 1>);
+            else if (c <= 64) launch(k_hart_gram2<T, 2>);
+            else if (c <= 128) launch(k_hart_gram2<T, 4>);
+            else launch(k_hart_gram2<T, 8>);
+        } else if (c <= 32) launch(k_hart_gram<T, 1>);
         else if (c <= 64) launch(k_hart_gram<T, 2>);
         else if (c <= 128) launch(k_hart_gram<T, 4>);
         else launch(k_hart_gram<T, 8>);
