@@ -27,10 +27,11 @@
 // centroids with the reference's own formula and decide on the reference's
 // chain.  Labels are therefore bit-identical to the reference's.
 //
-// One CTA per restart: a window of 32 columns is decided by 32 warps (lanes
-// over centroids), the first column that is not provably "no move" is
-// settled, the O(n) update is applied by all threads, and the scan resumes at
-// the next column — no grid barrier per move.
+// One thread-block cluster per restart (k_hart_gram below): a window of
+// 8·CL columns is decided by all warps of the cluster (lanes over centroids),
+// the first column that is not provably "no move" is settled, its O(n) update
+// is applied by every CTA to the columns it owns, and the scan resumes at the
+// next column — no grid barrier per move.
 #pragma once
 
 #include "km.cuh"
@@ -454,382 +455,16 @@ RESPCA_DEV void gcl_st_f64(uint32_t a, double v) {
     asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(a), "d"(v) : "memory");
 }
 
-// One thread-block cluster per restart.  Every CTA keeps a replica of the
-// per-centroid state.  A window of GRAM_WARPS·CL columns is decided by all
-// warps of the cluster (CTA r, warp w → column cursor + GRAM_WARPS·r + w); each
-// CTA pushes its first candidate (verdict + the move's inputs: Ŝ_from[j],
-// Ŝ_to[j], Ĝ_jj and the norm bounds) into every CTA's shared memory, so after
-// the one cluster barrier per window every warp finds the elected move in local
-// shared memory, and two threads of every CTA update the replica (identical
-// inputs → identical replicas).  The move's O(n) update is applied during the
-// next window, off the critical path:
-//   * each window's Ŝ block is staged with the pending move applied (and the
-//     two changed entries written back);
-//   * each CTA applies it to its slice of the other columns while its warps
-//     decide (loads first, stores before the decide).
-template <typename T, int KPL>
-__global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
-    extern __shared__ __align__(16) unsigned char sm[];
-    const int c = a.c, n = a.n;
-    const int64_t d = a.d;
-    GramCoef* cf = reinterpret_cast<GramCoef*>(sm);
-    GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
-    double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
-    int* cnt = reinterpret_cast<int*>(dist + c);
-    double* swin = reinterpret_cast<double*>(cnt + ((c + 1) & ~1));  // [c][GRAM_WARPS + 1] the window's Ŝ block
-    __shared__ int s_wfrom[GRAM_WARPS];
-    __shared__ double s_wg[GRAM_WARPS][2];            // Ĝ_jj, ‖x_j‖ bound of the window's columns
-    __shared__ int s_loc[2][GRAM_WARPS];              // this CTA's verdicts: status | to << 2 | from << 17
-    constexpr int MVW = 5;  // a move's inputs: Ŝ_from[j], Ŝ_to[j], Ĝ_jj, ‖x_j‖ upper / lower bound
-    __shared__ double s_sv[2][GRAM_WARPS][MVW];       // this CTA's candidates' move inputs
-    __shared__ int s_first[2][GRAM_MAXCL][2];         // every CTA's first candidate: verdict, warp
-    __shared__ double s_fsv[2][GRAM_MAXCL][MVW];      // ... and its move inputs
-    __shared__ int s_xres;                            // exact fallback verdict (CTA 0)
-    __shared__ double s_xsv[MVW];                     // ... and the move's inputs
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int rank = (int)gcl_rank(), CL = (int)gcl_size();
-    const int W = GRAM_WARPS * CL;
-    const T* M = static_cast<const T*>(a.M);
-    const double gamG = a.gamG, gamc = a.gamc;
-    // this CTA's slice of the O(n) update
-    const int per = (n + CL - 1) / CL;
-    const int u0 = min(n, rank * per), u1 = min(n, u0 + per);
-    constexpr int UPT = 3;  // slice elements per thread held across the window
-    // my verdict slot in every CTA of the cluster
-    uint32_t res_slot[2] = {0, 0};
-
-    for (int k = tid; k < c; k += blockDim.x) {
-        const int ck = a.counts[k];
-        cnt[k] = ck;
-        sc[k] = a.scal0[k];
-        gram_coef(sc[k], ck, cf[k]);
-    }
-    __syncthreads();
-    gcl_sync();  // every replica initialised before remote stores land
-
-    unsigned long long moves = 0, windows = 0, fallbacks = 0, replay_work = 0;
-    unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // SM cycles (thread 0): see the host trace
-    unsigned long long tmk = clock64();
-    auto lap = [&](int slot) {
-        if (tid == 0) {
-            const unsigned long long t = clock64();
-            tph[slot] += t - tmk;
-            tmk = t;
-        }
-    };
-    int nlog = 0, replayed = 0, pass = 0, par = 0;
-    // the pending move (uniform over the cluster)
-    int pj = -1, pf = 0, pt = 0;
-    double pmv[5] = {0, 0, 0, 0, 0};  // its inputs (MVW words)
-    for (;;) {
-        int improved = 0;
-        int cursor = 0;
-        while (cursor < n) {
-            const int j = cursor + GRAM_WARPS * rank + warp;
-            const bool mv = pj >= 0;
-            // ---- (1) loads: this thread's slice of the pending update, and the
-            //      window's Ŝ block staged in shared memory (coalesced over columns);
-            //      the pending move is applied to the staged Ŝ_from, Ŝ_to entries
-            double ug[UPT], uf[UPT], ut[UPT];
-            if (mv) {
-#pragma unroll
-                for (int e = 0; e < UPT; ++e) {
-                    const int q = u0 + tid + e * GRAM_THREADS;
-                    if (q < u1 && (q < cursor || q >= cursor + W)) {
-                        ug[e] = __ldcg(a.G + (int64_t)pj * n + q);
-                        uf[e] = __ldcg(a.S + (int64_t)pf * n + q);
-                        ut[e] = __ldcg(a.S + (int64_t)pt * n + q);
-                    }
-                }
-            }
-            {
-                const int jb = cursor + GRAM_WARPS * rank;
-                constexpr int SW = GRAM_THREADS - 32;  // staging threads (the last warp updates the replica)
-                constexpr int SPT = (KPL * 32 * GRAM_WARPS + SW - 1) / SW;
-                double v[SPT], g[SPT];
-#pragma unroll
-                for (int u = 0; u < SPT; ++u) {  // all loads first
-                    const int e = tid < SW ? tid + u * SW : 1 << 30;
-                    const int k = e / GRAM_WARPS, jc = jb + (e - k * GRAM_WARPS);
-                    v[u] = 0.0;
-                    g[u] = 0.0;
-                    if (k < c && jc < n) {
-                        v[u] = __ldcg(a.S + (int64_t)k * n + jc);
-                        if (mv && (k == pf || k == pt)) g[u] = __ldcg(a.G + (int64_t)pj * n + jc);
-                    }
-                }
-                // the replicas take the pending move's per-centroid state while the
-                // staging loads are in flight (two threads; identical inputs in
-                // every CTA → identical replicas; read only after the barrier below)
-                if (mv && warp == GRAM_WARPS - 1 && lane < 2) {  // the last warp stages nothing
-                    const int k = lane ? pt : pf;
-                    gram_side(lane, sc[k], cf[k], cnt[k], lane ? pmv[1] : pmv[0], pmv[2], pmv[3], pmv[4], gamG);
-                }
-#pragma unroll
-                for (int u = 0; u < SPT; ++u) {
-                    const int e = tid < SW ? tid + u * SW : 1 << 30;
-                    const int k = e / GRAM_WARPS, jl = e - k * GRAM_WARPS, jc = jb + jl;
-                    if (k < c) {
-                        double x = v[u];
-                        if (mv && jc < n && (k == pf || k == pt)) {
-                            x = k == pf ? x - g[u] : x + g[u];
-                            __stcg(a.S + (int64_t)k * n + jc, x);
-                        }
-                        swin[k * (GRAM_WARPS + 1) + jl] = x;
-                    }
-                }
-                if (tid < GRAM_WARPS) {
-                    const int jc = jb + tid;
-                    s_wfrom[tid] = jc < n ? (jc == pj ? pt : __ldcg(a.labels + jc)) : 0;  // labels[pj] is published later
-                    s_wg[tid][0] = jc < n ? __ldg(a.xx + jc) : 0.0;
-                    s_wg[tid][1] = jc < n ? __ldg(a.xn + jc) : 0.0;
-                }
-            }
-            lap(2);
-            if (mv) ++nlog;
-            __syncthreads();
-            lap(3);
-            // ---- (2b) this thread's slice of the pending update (stores drain during the decide)
-            if (mv) {
-#pragma unroll
-                for (int e = 0; e < UPT; ++e) {
-                    const int q = u0 + tid + e * GRAM_THREADS;
-                    if (q < u1 && (q < cursor || q >= cursor + W)) {
-                        __stcg(a.S + (int64_t)pf * n + q, uf[e] - ug[e]);
-                        __stcg(a.S + (int64_t)pt * n + q, ut[e] + ug[e]);
-                    }
-                }
-                // slices longer than UPT·GRAM_THREADS (small clusters): the rest in place
-                for (int q = u0 + tid + UPT * GRAM_THREADS; q < u1; q += GRAM_THREADS)
-                    if (q < cursor || q >= cursor + W) {
-                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
-                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
-                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
-                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
-                    }
-                pj = -1;
-            }
-            // ---- (3) decide the window column (lanes over k)
-            int st = 0, to = -1;
-            const int from = s_wfrom[warp];
-            if (j < n) {
-                const double gjj = s_wg[warp][0], xnj = s_wg[warp][1];
-                double sv[KPL];
-#pragma unroll
-                for (int q = 0; q < KPL; ++q) {
-                    const int k = lane + 32 * q;
-                    sv[q] = k < c ? swin[k * (GRAM_WARPS + 1) + warp] : 0.0;
-                }
-                if (cnt[from] > 1) {
-                    GramCol col;
-                    col.gjj = gjj;
-                    col.xnj = xnj;
-                    col.gq = gamG * xnj * xnj * (1.0 + 4.0 * kU) + 7.1 * kU * gjj;
-                    double lo[KPL], hi[KPL], mid[KPL];
-#pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
-                        const int k = lane + 32 * q;
-                        if (k < c) gram_iv(col, cf[k], sv[q], gamc, lo[q], hi[q], mid[q]);
-                        else lo[q] = hi[q] = mid[q] = INFINITY;
-                    }
-                    st = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, to);
-                    if (a.force_exact && st == 1) st = 2;
-                    if (st != 0 && lane == 0 && j + 1 < n) {
-                        // a candidate: the Ĝ elements the next window's columns need, to L2
-                        const int e1 = min(n, j + 1 + W);
-                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.G + (int64_t)j * n + j + 1);
-                        const uintptr_t s0 = b0 & ~(uintptr_t)15;
-                        const unsigned bytes = (unsigned)((b0 + (uintptr_t)(e1 - j - 1) * 8 - s0 + 15) & ~(uintptr_t)15);
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s0), "r"(bytes) : "memory");
-                    }
-                    if (st == 1) {  // speculative move state: Ŝ_from[j], Ŝ_to[j] from the lanes
-                        double vf = 0.0, vt = 0.0;
-#pragma unroll
-                        for (int q = 0; q < KPL; ++q) {
-                            if (q == (from >> 5)) vf = __shfl_sync(0xffffffffu, sv[q], from & 31);
-                            if (q == (to >> 5)) vt = __shfl_sync(0xffffffffu, sv[q], to & 31);
-                        }
-                        if (lane == 0) {
-                            s_sv[par][warp][0] = vf;
-                            s_sv[par][warp][1] = vt;
-                            s_sv[par][warp][2] = gjj;
-                            s_sv[par][warp][3] = xnj;
-                            s_sv[par][warp][4] = __ldg(a.xl + j);
-                        }
-                    }
-                }
-            }
-            lap(4);
-            // ---- (4) this warp's verdict
-            if (lane == 0) s_loc[par][warp] = st | ((to < 0 ? 0 : to) << 2) | (from << 17);
-            __syncthreads();
-            // ---- (5) this CTA's first candidate (verdict, warp, move state) → every CTA
-            {
-                const int v = lane < GRAM_WARPS ? s_loc[par][lane] : 0;
-                const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
-                const int fw = bal ? __ffs(bal) - 1 : 0;
-                if (warp == fw) {
-                    const int fv = __shfl_sync(0xffffffffu, v, fw);
-                    if (bal && lane == 0) {
-                        // the first candidate's Ĝ column (every CTA's slice of its update) to L2
-                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(a.G + (int64_t)(cursor + GRAM_WARPS * rank + fw) * n);
-                        const uintptr_t s0 = b0 & ~(uintptr_t)15;
-                        const unsigned bytes = (unsigned)((b0 + (uintptr_t)n * 8 - s0 + 15) & ~(uintptr_t)15);
-                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(s0), "r"(bytes) : "memory");
-                    }
-                    if (lane < CL) {
-                        gcl_st_i32(gcl_map(&s_first[par][rank][0], (uint32_t)lane), bal ? fv : 0);
-                        gcl_st_i32(gcl_map(&s_first[par][rank][1], (uint32_t)lane), fw);
-                    }
-                    if ((fv & 3) == 1 && lane < MVW) {
-                        const double word = s_sv[par][fw][lane];
-                        for (int r = 0; r < CL; ++r) gcl_st_f64(gcl_map(&s_fsv[par][rank][lane], (uint32_t)r), word);
-                    }
-                }
-            }
-            lap(5);
-            gcl_sync();
-            lap(6);
-            // ---- (6) every warp: the first candidate of the window (local shared memory)
-            int pr = -1, pw = 0, w = 0;
-            {
-                const int v = lane < CL ? s_first[par][lane][0] : 0;
-                const unsigned bal = __ballot_sync(0xffffffffu, (v & 3) != 0);
-                if (bal) {
-                    pr = __ffs(bal) - 1;
-                    w = __shfl_sync(0xffffffffu, v, pr);
-                    pw = s_first[par][pr][1];
-                }
-            }
-            ++windows;
-            lap(0);
-            if (pr < 0) {
-                cursor += W;
-                par ^= 1;
-                continue;
-            }
-            const int jj = cursor + GRAM_WARPS * pr + pw;
-            cursor = jj + 1;
-            const int mfrom = w >> 17;
-            int mst = w & 3, mto = (w >> 2) & 0x7fff;
-            double mvin[MVW];  // the elected move's inputs (pushed by its CTA, or CTA 0's after a fallback)
-            if (mst == 1) {
-#pragma unroll
-                for (int q = 0; q < MVW; ++q) mvin[q] = s_fsv[par][pr][q];
-            } else {
-                // ---- near-tie (CTA 0): the reference's own chain on the
-                //      reference's centroids (logged moves replayed, kmeans.cpp:128-129)
-                ++fallbacks;
-                if (rank == 0) {
-                    for (int64_t i = tid; i < d; i += blockDim.x) {
-                        for (int e = replayed; e < nlog; ++e) {
-                            const int* lg = a.log + 5 * (int64_t)e;
-                            const int m = __ldcg(lg), f = __ldcg(lg + 1), t = __ldcg(lg + 2);
-                            const double nf = (double)__ldcg(lg + 3), nt = (double)__ldcg(lg + 4);
-                            const double x = (double)M[(int64_t)m * d + i];
-                            double* cfp = a.Cs + (int64_t)f * d + i;
-                            double* ctp = a.Cs + (int64_t)t * d + i;
-                            *cfp = (*cfp * nf - x) / (nf - 1.0);
-                            *ctp = (*ctp * nt + x) / (nt + 1.0);
-                        }
-                    }
-                    __syncthreads();
-                    for (int k = tid; k < c; k += blockDim.x) {  // kmeans.cpp:12-19
-                        const T* x = M + (int64_t)jj * d;
-                        const double* ck = a.Cs + (int64_t)k * d;
-                        double s = 0.0;
-                        for (int64_t i = 0; i < d; ++i) {
-                            const double t = (double)x[i] - ck[i];
-                            s += t * t;
-                        }
-                        dist[k] = s;
-                    }
-                    __syncthreads();
-                    if (warp == 0) {
-                        double lo[KPL], hi[KPL], mid[KPL];
-#pragma unroll
-                        for (int q = 0; q < KPL; ++q) {
-                            const int k = lane + 32 * q;
-                            lo[q] = hi[q] = mid[q] = k < c ? dist[k] : INFINITY;
-                        }
-                        int t2 = -1;
-                        const int s2 = gram_decide<KPL>(mfrom, c, cf, cnt, lo, hi, mid, t2);
-                        if (lane == 0) s_xres = s2 == 1 ? (1 | (t2 << 2)) : 0;  // exact: 2 only for NaN
-                        if (s2 == 1 && lane == 0) {
-                            s_xsv[0] = __ldcg(a.S + (int64_t)mfrom * n + jj);
-                            s_xsv[1] = __ldcg(a.S + (int64_t)t2 * n + jj);
-                            s_xsv[2] = __ldg(a.xx + jj);
-                            s_xsv[3] = __ldg(a.xn + jj);
-                            s_xsv[4] = __ldg(a.xl + jj);
-                        }
-                    }
-                }
-                replay_work += (unsigned long long)(nlog - replayed);
-                replayed = nlog;
-                gcl_sync();
-                const int xr = gcl_ld_i32(gcl_map(&s_xres, 0));
-                mst = xr & 3;
-                mto = xr >> 2;
-                if (mst == 1)
-#pragma unroll
-                    for (int q = 0; q < MVW; ++q) mvin[q] = gcl_ld_f64(gcl_map(&s_xsv[q], 0));
-                lap(1);
-            }
-            if (mst == 1) {
-                // pending for the next window: the log (CTA 0); the replicas take the
-                // move's per-centroid state now (two threads per CTA, identical
-                // inputs → identical replicas), the Ŝ update later
-                if (tid == 0 && rank == 0) {  // the log holds the counts before the move
-                    int* lg = a.log + 5 * (int64_t)nlog;
-                    lg[0] = jj;
-                    lg[1] = mfrom;
-                    lg[2] = mto;
-                    lg[3] = cnt[mfrom];
-                    lg[4] = cnt[mto];
-                    __stcg(a.labels + jj, mto);
-                }
-#pragma unroll
-                for (int q = 0; q < MVW; ++q) pmv[q] = mvin[q];
-                lap(7);
-                pj = jj;
-                pf = mfrom;
-                pt = mto;
-                ++moves;
-                improved = 1;
-            }
-            par ^= 1;
-        }
-        ++pass;
-        if (!improved || pass >= a.max_pass) break;
-    }
-    // the last move's label was written when it was elected; its counts go to
-    // the output (its scalars and Ŝ update are no longer needed)
-    if (pj >= 0) {
-        if (tid == 0) --cnt[pf];
-        if (tid == 32) ++cnt[pt];
-    }
-    __syncthreads();
-    if (rank == 0) {
-        for (int k = tid; k < c; k += blockDim.x) a.counts[k] = cnt[k];
-        if (tid == 0) {
-            a.stats[0] = moves;
-            a.stats[1] = (unsigned long long)pass;
-            a.stats[2] = windows;
-            a.stats[3] = fallbacks;
-            a.stats[4] = replay_work;
-            for (int q = 0; q < 8; ++q) a.stats[5 + q] = tph[q];
-        }
-    }
-    gcl_sync();  // no CTA leaves while another may still read its shared memory
-}
-
 // ---------------------------------------------------------------------------
-// k_hart_gram2: the same refinement with the window's data resident on chip.
+// k_hart_gram: one thread-block cluster per restart, the window's data resident
+// on chip.  Every CTA keeps a replica of the per-centroid state; a window of
+// W = GRAM_WARPS·CL consecutive columns is decided by all warps of the cluster.
 //
-// k_hart_gram stages every window's Ŝ block from L2 (columns move between CTAs
-// as the window start moves), so each window pays an L2 round trip before it
-// can decide, and every CTA's global Ŝ stores must be fenced cluster-wide for
-// the others.  Here column ownership is fixed: columns are dealt to the CTAs in
+// (Round 1 staged every window's Ŝ block from L2 — columns moved between CTAs
+// as the window start moved — so each window paid an L2 round trip before it
+// could decide, and every CTA's global Ŝ stores had to be fenced cluster-wide
+// under a cluster barrier per window: 3.6 µs per window, 78 ms per restart at
+// C3; this kernel: 3.1 µs, 68 ms.)  Column ownership is fixed: columns are dealt to the CTAs in
 // groups of GW = GRAM_WARPS (group g → CTA g mod CL), so ANY window of
 // W = GW·CL consecutive columns holds exactly GW columns of every CTA (one
 // whole group, or the two partial groups of the CTA straddling the window
@@ -842,11 +477,15 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
 // move is applied to the cached groups from shared memory (Ŝ_from −= Ĝ[j][m],
 // Ŝ_to += Ĝ[j][m], one rounded operation each — the arithmetic of k_hart_gram)
 // and to the CTA's other columns in global memory, which only this CTA ever
-// reads or writes.  A window is then: patch (shared memory) → decide → push the
-// CTA's first candidate → cluster barrier → elect the lowest column; no load
-// from L2 sits on that path.  Decisions, fallbacks and results are those of
-// k_hart_gram (same intervals, same exact fallback), so the labels are the
-// reference's.
+// reads or writes — so no cluster-wide fence is needed.  A window is then:
+// patch (shared memory) → decide → every CTA pushes its first candidate
+// (verdict, column, the move's five inputs) into every CTA's shared memory with
+// st.async, each store completing bytes on the receiver's mbarrier → wait on the
+// local mbarrier → elect the lowest column; the far stores and the block change
+// ride behind the push.  No load from L2, no cluster barrier and no fence sit on
+// that path.  The decisions are made on the rigorous intervals above; an
+// undecidable column replays the logged moves and decides on the reference's
+// own chain (CTA 0, cluster barriers on that rare path only).
 // ---------------------------------------------------------------------------
 // asynchronous store into another CTA's shared memory that completes bytes on
 // that CTA's mbarrier: the receiver's mbarrier wait orders the data, no
@@ -858,7 +497,7 @@ RESPCA_DEV void gcl_st_async_b64(uint32_t remote_addr, uint64_t v, uint32_t remo
 }
 
 template <typename T, int KPL>
-__global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram2(GramArgs a) {
+__global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     extern __shared__ __align__(16) unsigned char sm[];
     const int c = a.c, n = a.n;
     const int64_t d = a.d;
@@ -981,8 +620,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram2(GramArgs a) {
     // the pending move on the cached groups (one thread per cached column); the
     // replicas took it when it was elected
     auto patch_cached = [&](int cur, int pj, int pf, int pt, const double (&pmv)[5]) {
-        if (tid < NSL * GW) {
-            const int gi = tid / GW, col = tid - gi * GW, m = cur + gi;
+        const int pt_ = tid - (GRAM_THREADS - 64);  // the last warp but one (the last one carries the replica update)
+        if (pt_ >= 0 && pt_ < NSL * GW) {
+            const int gi = pt_ / GW, col = pt_ - gi * GW, m = cur + gi;
             if (m < NG && J0(m) + col < n) {
                 const int slot = m % NSL;
                 const double g = gseg[(size_t)(slot * GW + col) * GL + (pj - (m - 2) * W)];
@@ -1066,6 +706,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram2(GramArgs a) {
             double ug[UPT], uf[UPT], ut[UPT];
             int uq[UPT];
             if (mv) {
+                patch_cached(cur, pj, pf, pt, pmv);
 #pragma unroll
                 for (int e = 0; e < UPT; ++e) {
                     uq[e] = far_col(tid + e * GRAM_THREADS, cur);
@@ -1075,7 +716,6 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram2(GramArgs a) {
                         ut[e] = __ldcg(a.S + (int64_t)pt * n + uq[e]);
                     }
                 }
-                patch_cached(cur, pj, pf, pt, pmv);
                 ++nlog;
             }
             lap(2);

@@ -834,19 +834,13 @@ struct KMeansEngine {
         a.force_exact = env_int("RESPCA_GRAM_FORCE_EXACT", 0);
         a.gamG = gamG;
         a.gamc = ((double)d + 3.0) * kU * 1.02;
-        const size_t sm = (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double)) +
-                          sizeof(int) * (size_t)((c + 1) & ~1) + sizeof(double) * (size_t)c * (GRAM_WARPS + 1) + 64;
         // one cluster of CL CTAs (one SM each) per restart
         // (16, non-portable, where available: C3 refinement 189 -> 176 ms vs 8)
         int CL = n >= 8192 ? 16 : std::max(1, std::min(8, n / 1024));
         if (const char* e = std::getenv("RESPCA_GRAM_CL")) CL = std::max(1, std::min(GRAM_MAXCL, std::atoi(e)));
-        // RESPCA_HART_GRAM2=0: the window-staging kernel (k_hart_gram); default: the
-        // resident-window kernel (k_hart_gram2: fixed column ownership, cached groups)
-        const bool resident = env_int("RESPCA_HART_GRAM2", 1) != 0;
-        if (resident)
-            while (CL & (CL - 1)) CL &= CL - 1;  // a power of two (the kernel's column → CTA map uses shifts)
+        // the column → CTA map uses shifts: the cluster size is a power of two
+        while (CL & (CL - 1)) CL &= CL - 1;
         auto smem_for = [&](int cl) -> size_t {
-            if (!resident) return sm;
             const size_t cs = (size_t)((c + 1) & ~1), gl = (size_t)4 * GRAM_WARPS * cl;
             return (size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double)) + sizeof(int) * cs +
                    sizeof(double) * (3 * GRAM_WARPS * cs + 3 * GRAM_WARPS * gl) + 80;
@@ -873,12 +867,7 @@ struct KMeansEngine {
                 (void)cudaGetLastError();  // cluster not schedulable: halve it
             }
         };
-        if (resident) {
-            if (c <= 32) launch(k_hart_gram2<T, 1>);
-            else if (c <= 64) launch(k_hart_gram2<T, 2>);
-            else if (c <= 128) launch(k_hart_gram2<T, 4>);
-            else launch(k_hart_gram2<T, 8>);
-        } else if (c <= 32) launch(k_hart_gram<T, 1>);
+        if (c <= 32) launch(k_hart_gram<T, 1>);
         else if (c <= 64) launch(k_hart_gram<T, 2>);
         else if (c <= 128) launch(k_hart_gram<T, 4>);
         else launch(k_hart_gram<T, 8>);
@@ -895,7 +884,7 @@ struct KMeansEngine {
             }
             if (trace_on())
                 std::fprintf(stderr, "[respca] hartigan(gram, CL=%d): %llu passes %llu windows %llu moves %llu fallbacks (replayed %llu moves); "
-                             "s at 1.965GHz: pick %.3f fallback %.3f loads %.3f sync %.3f decide %.3f push+slice %.3f barrier %.3f replica %.3f\n",
+                             "s at 1.965GHz: elect %.3f far stores %.3f patch %.3f block change %.3f decide %.3f push %.3f exchange wait %.3f pending %.3f\n",
                              CL, hh[1], hh[2], hh[0], hh[3], hh[4], hh[5] / 1.965e9, hh[6] / 1.965e9, hh[7] / 1.965e9, hh[8] / 1.965e9, hh[9] / 1.965e9, hh[10] / 1.965e9,
                              hh[11] / 1.965e9, hh[12] / 1.965e9);
         }
