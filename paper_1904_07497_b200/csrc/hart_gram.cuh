@@ -279,6 +279,7 @@ struct GramArgs {
     int64_t d;
     int n, c, max_pass;
     int force_exact;   // tests: every candidate goes through the exact fallback
+    int timing;        // RESPCA_TRACE: per-phase SM cycle counters in stats[5..12]
     double gamG, gamc;
 };
 
@@ -564,8 +565,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     unsigned long long moves = 0, windows = 0, fallbacks = 0, replay_work = 0;
     unsigned long long tph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long tmk = clock64();
+    const bool timing = a.timing != 0;
     auto lap = [&](int slot) {
-        if (tid == 0) {
+        if (timing && tid == 0) {
             const unsigned long long t = clock64();
             tph[slot] += t - tmk;
             tmk = t;
@@ -625,8 +627,8 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             const int gi = pt_ / GW, col = pt_ - gi * GW, m = cur + gi;
             if (m < NG && J0(m) + col < n) {
                 const int slot = m % NSL;
-                const double g = gseg[(size_t)(slot * GW + col) * GL + (pj - (m - 2) * W)];
-                double* sv = &scache[(size_t)(slot * GW + col) * CS];
+                const double g = gseg[(slot * GW + col) * GL + (pj - (m - 2) * W)];
+                double* sv = scache + (slot * GW + col) * CS;
                 sv[pf] = sv[pf] - g;
                 sv[pt] = sv[pt] + g;
                 if (J0(m) + col == pj) clab[slot][col] = pt;
@@ -705,15 +707,18 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
             // ---- (1) the pending move: far columns loaded, cached columns patched in shared memory
             double ug[UPT], uf[UPT], ut[UPT];
             int uq[UPT];
+            const double* Gp = a.G + (int64_t)(mv ? pj : 0) * n;  // the pending move's rows
+            double* Sf = a.S + (int64_t)pf * n;
+            double* St = a.S + (int64_t)pt * n;
             if (mv) {
                 patch_cached(cur, pj, pf, pt, pmv);
 #pragma unroll
                 for (int e = 0; e < UPT; ++e) {
                     uq[e] = far_col(tid + e * GRAM_THREADS, cur);
                     if (uq[e] >= 0) {
-                        ug[e] = __ldcg(a.G + (int64_t)pj * n + uq[e]);
-                        uf[e] = __ldcg(a.S + (int64_t)pf * n + uq[e]);
-                        ut[e] = __ldcg(a.S + (int64_t)pt * n + uq[e]);
+                        ug[e] = __ldcg(Gp + uq[e]);
+                        uf[e] = __ldcg(Sf + uq[e]);
+                        ut[e] = __ldcg(St + uq[e]);
                     }
                 }
                 ++nlog;
@@ -735,7 +740,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 const int slot = jm % NSL, col = j - (j / GW) * GW;
                 from = clab[slot][col];
                 const double gjj = cxx[slot][col], xnj = cxn[slot][col];
-                const double* svp = &scache[(size_t)(slot * GW + col) * CS];
+                const double* svp = scache + (slot * GW + col) * CS;
                 double sv[KPL];
 #pragma unroll
                 for (int q = 0; q < KPL; ++q) {
@@ -805,18 +810,19 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
 #pragma unroll
                 for (int e = 0; e < UPT; ++e)
                     if (uq[e] >= 0) {
-                        __stcg(a.S + (int64_t)pf * n + uq[e], uf[e] - ug[e]);
-                        __stcg(a.S + (int64_t)pt * n + uq[e], ut[e] + ug[e]);
+                        __stcg(Sf + uq[e], uf[e] - ug[e]);
+                        __stcg(St + uq[e], ut[e] + ug[e]);
                     }
-                for (int e = tid + UPT * GRAM_THREADS; e < NG * GW; e += GRAM_THREADS) {
-                    const int q = far_col(e, fcur);
-                    if (q >= 0) {
-                        const double g = __ldcg(a.G + (int64_t)pj * n + q);
-                        const double f0 = __ldcg(a.S + (int64_t)pf * n + q), t0 = __ldcg(a.S + (int64_t)pt * n + q);
-                        __stcg(a.S + (int64_t)pf * n + q, f0 - g);
-                        __stcg(a.S + (int64_t)pt * n + q, t0 + g);
+                if (NG * GW > UPT * GRAM_THREADS)
+                    for (int e = tid + UPT * GRAM_THREADS; e < NG * GW; e += GRAM_THREADS) {
+                        const int q = far_col(e, fcur);
+                        if (q >= 0) {
+                            const double g = __ldcg(Gp + q);
+                            const double f0 = __ldcg(Sf + q), t0 = __ldcg(St + q);
+                            __stcg(Sf + q, f0 - g);
+                            __stcg(St + q, t0 + g);
+                        }
                     }
-                }
                 pj = -1;
             }
             lap(1);

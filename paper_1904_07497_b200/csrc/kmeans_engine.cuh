@@ -832,6 +832,7 @@ struct KMeansEngine {
         a.c = c;
         a.max_pass = 50;  // kmeans.cpp:101
         a.force_exact = env_int("RESPCA_GRAM_FORCE_EXACT", 0);
+        a.timing = trace_on() ? 1 : 0;
         a.gamG = gamG;
         a.gamc = ((double)d + 3.0) * kU * 1.02;
         // one cluster of CL CTAs (one SM each) per restart
