@@ -835,9 +835,12 @@ struct KMeansEngine {
         a.timing = trace_on() ? 1 : 0;
         a.gamG = gamG;
         a.gamc = ((double)d + 3.0) * kU * 1.02;
-        // one cluster of CL CTAs (one SM each) per restart
-        // (16, non-portable, where available: C3 refinement 189 -> 176 ms vs 8)
-        int CL = n >= 8192 ? 16 : std::max(1, std::min(8, n / 1024));
+        // one cluster of CL CTAs (one SM each) per restart: 16 (the non-portable size,
+        // halved below when the GPU cannot place it) — with the st.async exchange a
+        // wider window costs nothing per window and saves windows at every size
+        // (C2, n = 2000: refinement-dominated init 49 ms at CL = 1, 20 ms at 16; C1 27 → 18.5)
+        int CL = 16;
+        while (CL > 1 && (CL / 2) * GRAM_WARPS >= n) CL /= 2;  // tiny n: no CTA without a column
         if (const char* e = std::getenv("RESPCA_GRAM_CL")) CL = std::max(1, std::min(GRAM_MAXCL, std::atoi(e)));
         // the column → CTA map uses shifts: the cluster size is a power of two
         while (CL & (CL - 1)) CL &= CL - 1;
