@@ -387,6 +387,7 @@ RESPCA_DEV int gram_decide(int from, int c, const GramCoef* cf, const int* cnt, 
     return 1;
 }
 
+constexpr unsigned long long kHartWaitNs = 30000000000ULL;  // mbarrier waits of the refinement: 30 s
 constexpr int GRAM_THREADS = 256;
 constexpr int GRAM_WARPS = GRAM_THREADS / 32;
 
@@ -656,7 +657,7 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     auto finish_load = [&]() {  // all threads: the outstanding group load has landed
         cp_wait<0>();
         if (gbulk) {
-            if (!mbar_wait(&gbar, gph & 1u)) asm volatile("trap;\n");
+            if (!mbar_wait(&gbar, gph & 1u, kHartWaitNs)) asm volatile("trap;\n");
             ++gph;
         }
         __syncthreads();
@@ -837,7 +838,9 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                 commit_load();
             }
             lap(3);
-            if (!mbar_wait(&xbar[par], xph[par] & 1u)) asm volatile("trap;\n");  // a lost exchange: abort, never hang
+            // a lost exchange aborts the kernel instead of hanging the GPU; the limit is
+            // generous so that a time-sliced or preempted context does not trip it
+            if (!mbar_wait(&xbar[par], xph[par] & 1u, kHartWaitNs)) asm volatile("trap;\n");
             ++xph[par];
             lap(6);
             // ---- (5) every warp: the window's first candidate = the lowest column

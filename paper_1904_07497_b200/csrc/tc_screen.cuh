@@ -49,8 +49,8 @@ RESPCA_DEV void mbar_init(uint64_t* bar, uint32_t count) {
 RESPCA_DEV void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
-// bounded wait: returns false after ~2 s (a hang guard, never expected)
-RESPCA_DEV bool mbar_wait(uint64_t* bar, uint32_t parity) {
+// bounded wait: returns false after ~2 s by default (a hang guard, never expected)
+RESPCA_DEV bool mbar_wait(uint64_t* bar, uint32_t parity, unsigned long long limit_ns = 2000000000ULL) {
     const uint32_t a = smem_u32(bar);
     uint32_t done = 0;
     unsigned long long t0 = 0;
@@ -66,7 +66,7 @@ RESPCA_DEV bool mbar_wait(uint64_t* bar, uint32_t parity) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
             if (!t0) t0 = t;
-            else if (t - t0 > 2000000000ULL) return false;
+            else if (t - t0 > limit_ns) return false;
         }
     }
 }
