@@ -517,8 +517,10 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
     GramScal* sc = reinterpret_cast<GramScal*>(cf + c);
     double* dist = reinterpret_cast<double*>(sc + c);  // [c] exact chains (fallback)
     int* cnt = reinterpret_cast<int*>(dist + c);
-    double* scache = reinterpret_cast<double*>(
-        (reinterpret_cast<uintptr_t>(cnt + ((c + 1) & ~1)) + 15) & ~(uintptr_t)15);  // [NSL][GW][CS]
+    // 16-byte aligned behind cnt (offset arithmetic, so the pointer stays a shared-memory one)
+    const size_t sc_off = ((size_t)c * (sizeof(GramCoef) + sizeof(GramScal) + sizeof(double)) +
+                           sizeof(int) * (size_t)((c + 1) & ~1) + 15) & ~(size_t)15;
+    double* scache = reinterpret_cast<double*>(sm + sc_off);  // [NSL][GW][CS]
     double* gseg = scache + (size_t)NSL * GW * CS;                                   // [NSL][GW][GL]
     __shared__ int clab[NSL][GW];
     __shared__ double cxx[NSL][GW], cxn[NSL][GW], cxl[NSL][GW];
