@@ -4,7 +4,8 @@ iterations bit-identical, on data built to stress it —
 
 * integer-valued columns (exact distance ties),
 * duplicate columns, tiny and large magnitudes,
-* clusters of 1, 2, 4 and 8 CTAs (RESPCA_GRAM_CL), the per-pass path
+* clusters of 1, 2, 4, 8 and 16 CTAs (RESPCA_GRAM_CL; 16 is the default at every n,
+  also where most CTAs of the cluster own no column), the per-pass path
   (RESPCA_HART_GRAM=0) on the same inputs, and every move forced through the
   exact fallback (RESPCA_GRAM_FORCE_EXACT=1: the logged moves are replayed
   onto the reference's centroids and the reference's own chain decides).
@@ -81,7 +82,7 @@ def fallbacks(stderr):
                if "hartigan(gram, CL=" in ln)
 
 
-@pytest.mark.parametrize("cl", ["1", "4"])
+@pytest.mark.parametrize("cl", ["1", "4", "16"])
 def test_gram_exact_fallback_bitwise(cl):
     """Every provable move routed through the exact fallback (log replay onto
     the reference's centroids + the reference's chain): same results."""
@@ -151,7 +152,7 @@ sys.exit(1 if bad else 0)
 """
 
 
-@pytest.mark.parametrize("cl", ["1", "8"])
+@pytest.mark.parametrize("cl", ["1", "8", "16"])
 def test_gram_shapes_bitwise(cl):
     """Odd row/column counts, partial Gram tiles and every lanes-per-centroid
     width of the refinement kernel (c up to its 256 limit)."""
