@@ -337,33 +337,45 @@ RESPCA_DEV int gram_decide(int from, int c, const GramCoef* cf, const int* cnt, 
     const int lane = threadIdx.x & 31;
     if (cnt[from] <= 1) return 0;  // kmeans.cpp:105
     const int fq = from >> 5, fl_ = from & 31;
-    double flo = 0, fhi = 0, fmid = 0;
+    // the common verdict first, on a branch-free path: "provably no move" needs only
+    // the own centroid's upper end and the others' lower ends
+    double fhi = 0;
 #pragma unroll
     for (int q = 0; q < KPL; ++q)
-        if (q == fq) {
-            flo = __shfl_sync(0xffffffffu, lo[q], fl_);
-            fhi = __shfl_sync(0xffffffffu, hi[q], fl_);
-            fmid = __shfl_sync(0xffffffffu, mid[q], fl_);
-        }
+        if (q == fq) fhi = __shfl_sync(0xffffffffu, hi[q], fl_);
     const double w_a = cf[from].wa;
-    const double g_lo = w_a * flo, g_hi = w_a * fhi, g_mid = w_a * fmid;
-    double bd = INFINITY;
-    int bk = 0x7fffffff;
+    const double g_hi = w_a * fhi;
+    double wbq[KPL];
     bool none = true;
 #pragma unroll
     for (int q = 0; q < KPL; ++q) {
         const int k = lane + 32 * q;
+        const bool valid = k < c && k != from;
+        wbq[q] = cf[valid ? k : from].wb;
+        none &= !valid || !(wbq[q] * lo[q] - g_hi < -1e-12);  // kmeans.cpp:116, best_delta = −1e-12
+    }
+    none = __all_sync(0xffffffffu, none);
+    if (none) return 0;
+    double flo = 0, fmid = 0;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q)
+        if (q == fq) {
+            flo = __shfl_sync(0xffffffffu, lo[q], fl_);
+            fmid = __shfl_sync(0xffffffffu, mid[q], fl_);
+        }
+    const double g_lo = w_a * flo, g_mid = w_a * fmid;
+    double bd = INFINITY;
+    int bk = 0x7fffffff;
+#pragma unroll
+    for (int q = 0; q < KPL; ++q) {
+        const int k = lane + 32 * q;
         if (k >= c || k == from) continue;
-        const double w_b = cf[k].wb;
-        none &= !(w_b * lo[q] - g_hi < -1e-12);  // kmeans.cpp:116, best_delta = −1e-12
-        const double dmid = w_b * mid[q] - g_mid;
+        const double dmid = wbq[q] * mid[q] - g_mid;
         if (dmid < bd) {
             bd = dmid;
             bk = k;
         }
     }
-    none = __all_sync(0xffffffffu, none);
-    if (none) return 0;
     warp_argmin(bd, bk);
     if (bk >= c) return 2;
     const int bq_ = bk >> 5, bl = bk & 31;
@@ -757,10 +769,10 @@ __global__ void __launch_bounds__(GRAM_THREADS, 1) k_hart_gram(GramArgs a) {
                     colv.gq = gamG * xnj * xnj * (1.0 + 4.0 * kU) + 7.1 * kU * gjj;
                     double lo[KPL], hi[KPL], mid[KPL];
 #pragma unroll
-                    for (int q = 0; q < KPL; ++q) {
+                    for (int q = 0; q < KPL; ++q) {  // branch-free: lanes past c compute on centroid 0 and discard
                         const int k = lane + 32 * q;
-                        if (k < c) gram_iv(colv, cf[k], sv[q], gamc, lo[q], hi[q], mid[q]);
-                        else lo[q] = hi[q] = mid[q] = INFINITY;
+                        gram_iv(colv, cf[k < c ? k : 0], sv[q], gamc, lo[q], hi[q], mid[q]);
+                        if (k >= c) lo[q] = hi[q] = mid[q] = INFINITY;
                     }
                     st = gram_decide<KPL>(from, c, cf, cnt, lo, hi, mid, to);
                     if (a.force_exact && st == 1) st = 2;
