@@ -412,7 +412,7 @@ def run_ours(args, w, world, rank, local, pg) -> None:
             "config": {**workload_config(w), "parallelism": f"replicas x{world}"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"],
                          "unit": "GB/s", "frac": achieved / pk["hbm_gbs"], "traffic": ncu_traffic(args.workload),
-                         "kernel": ("k_pass_f_stream" if (w.c == 1 and w.d <= 20000 and w.d % (2 if w.dtype == "f64" else 4) == 0)
+                         "kernel": ("k_pass_f_stream" if (w.c == 1 and w.d <= 75776 and w.d % (2 if w.dtype == "f64" else 4) == 0)
                                     else "k_pass_f_ring") + " (Pass F: fused L/S/Θ update + group sums + residuals)",
                          "alg_bytes_per_launch": alg_bytes,
                          "alg_bytes_note": "7·N·s (X,S,Θ,L in; L,S,Θ out), SURVEY.md §8(d)",

@@ -528,7 +528,13 @@ __global__ void __launch_bounds__(PFS_THREADS, NS <= 3 ? 3 : 2) k_pass_f_stream(
             double* sm_ = summ + (size_t)(s & 1) * 2 * CPS * VEC;
 #pragma unroll
             for (int j = 0; j < K; ++j) {
-                if (cmem[j] >= mps) continue;  // a chunk past the stage's members (mps·lpc < CPS)
+                // a chunk past the stage's members (mps·lpc < CPS), or of rows past d in the
+                // last, partial row block: nothing to compute.  (Computing on their
+                // zero-filled tiles sent both divisions down the IEEE slow path — 0/ρ — so
+                // that one stream ran ≈1.5× longer than the others and, every stream
+                // lasting the whole kernel, so did the launch: C3-c1 rb = 32 0.48 of HBM,
+                // against 0.75 at rb = 40 with d % rb = 0.)
+                if (!crow[j]) continue;
                 const int k = tid + 256 * j;
                 const unsigned char* base = stg + (size_t)(s % NS) * 4 * CPS * 16 + (size_t)k * 16;
                 const T* xs = reinterpret_cast<const T*>(base);

@@ -347,40 +347,47 @@ struct Alm : AlmBase {
         // (C3 1.026 -> 0.974 ms, C5 24.8 -> 18.4, C4 0.74 -> 0.45)
         pf_ring = !(cfg.sparse_norm == RESPCA_L21);
         nbP = pf_ring ? ceil_div(d, ring_nt()) * c : nbF;
-        // c = 1 with d up to 2·10⁴ rows: one-thread-per-row walks cannot fill the GPU
-        // (measured Pass F fraction of HBM, ring → stream: C2-c1 0.06 → 0.40,
-        // C3-c1 0.31 → 0.65; C5 (d = 4·10⁴) stays on the ring, 0.74 vs 0.73)
-        pf_stream = !(cfg.sparse_norm == RESPCA_L21) && d % (16 / (int64_t)sizeof(T)) == 0 &&
-                    (passf_stream_env > 0 || (passf_stream_env < 0 && c == 1 && d <= 20000));
-        if (pf_stream) {
-            // rows per stream (a multiple of VEC, 16..RBMAX): the c·⌈d/rb⌉ streams
-            // should fill whole waves of the 2·148 resident CTAs — the fill
-            // (streams / (waves·slots)) decides, ties to the wider segment
-            const int vec = 16 / (int)sizeof(T), rbmax = sizeof(T) == 8 ? 128 : 256;
+        // c = 1 ("rank unknown"): one-thread-per-row walks cannot fill the GPU; Pass F
+        // runs as row-block streams (measured fraction of HBM, ring → stream: C2-c1
+        // 0.06 → 0.57, C3-c1 0.31 → 0.77, C5 0.73 → 0.85).  Every stream lasts the whole
+        // kernel, so the rows per stream decide (sweeps in profiles/round2_ncu.md):
+        //  * one wave only — the c·⌈d/rb⌉ streams fit the 2·148 resident CTAs, and
+        //    at least ≈200 of them so that most SMs hold two;
+        //  * segments on 64-byte boundaries (DRAM moves 64 bytes at a time: rb = 34
+        //    at C3-c1 reads 12 % more than algorithmic), better on 128-byte ones;
+        //  * a stage's 256 chunks well used: ⌊256/(rb/VEC)⌋·(rb/VEC) close to 256.
+        pf_stream = false;
+        if (!(cfg.sparse_norm == RESPCA_L21) && d % (16 / (int64_t)sizeof(T)) == 0 &&
+            (passf_stream_env > 0 || (passf_stream_env < 0 && c == 1))) {
+            const int vec = 16 / (int)sizeof(T), al = 64 / (int)sizeof(T), rbmax = 256;
             const int64_t slots = (stream_ns3 ? 3 : 2) * 148;
             double best = -1.0;
-            for (int r = 16; r <= rbmax; r += vec) {
-                if (r / vec > 256) break;
+            for (int r = al; r <= rbmax; r += al) {
+                const int lpc = r / vec;
+                if (lpc > 256) break;
                 const int64_t ns = (int64_t)c * ceil_div(d, (int64_t)r);
-                const int64_t waves = ceil_div(ns, slots);
-                const double fill = (double)ns / (double)(waves * slots);
-                // a stream needs enough rows for whole 128-byte lines (r·s ≥ 128), and
-                // segments that start on 64-byte boundaries: DRAM moves 64 bytes at a
-                // time (C3-c1: rb = 34 → 0.66 of HBM with 12 % more DRAM reads than
-                // algorithmic, rb = 40 → 0.74; rb = 36 0.64, 42 0.54 — measured)
-                const double score = fill - (r * (int)sizeof(T) < 256 ? 0.05 : 0.0) -
-                                     ((r * (int)sizeof(T)) % 64 != 0 ? 0.25 : 0.0);
-                if (score >= best) {
+                if (ns > slots) continue;
+                const double util = (double)((256 / lpc) * lpc) / 256.0;
+                const double score = util + (r % (2 * al) == 0 ? 0.08 : 0.0) -
+                                     (ns < 200 ? (double)(200 - ns) / 200.0 : 0.0);
+                if (score > best) {
                     best = score;
                     stream_rb = r;
                 }
             }
+            pf_stream = best >= 0.0;  // d beyond 296·256 rows: the ring walks
+            const int rbmax_env = rbmax;
             if (const char* e = std::getenv("RESPCA_STREAM_RB")) {
                 const int r = std::atoi(e);
-                if (r >= vec && r <= rbmax && r % vec == 0) stream_rb = r;
+                if (r >= vec && r <= rbmax_env && r % vec == 0) {
+                    stream_rb = r;
+                    pf_stream = true;
+                }
             }
-            stream_nrb = (int)ceil_div(d, (int64_t)stream_rb);
-            nbP = c * stream_nrb;
+            if (pf_stream) {
+                stream_nrb = (int)ceil_div(d, (int64_t)stream_rb);
+                nbP = c * stream_nrb;
+            }
         }
         partials.ensure((size_t)std::max(nbF, nbP) * PF_STRIDE);
         Ctl h{};
@@ -554,6 +561,7 @@ struct Alm : AlmBase {
         if (pf_stream) {
             if constexpr (sizeof(T) == 8) {
                 if (stream_ns3) launch_stream<1, 3, 128>();
+                else if (stream_rb > 128) launch_stream<1, 5, 256>();
                 else launch_stream<1, 5, 128>();
             } else {
                 launch_stream<1, 4, 256>();

@@ -167,3 +167,24 @@ def test_c1_bitwise_launch_modes(ctx, monkeypatch, pdl):
         case = load(f"solve_{name}.json")
         res = _solve(ctx, make_x(case), cfg_from(case["config"]))
         assert_matches_golden(res, case)
+
+
+@pytest.mark.parametrize("d,n,c,rb", [(200, 150, 1, "48"), (200, 150, 1, "16"), (96, 120, 4, "16"),
+                                      (250, 90, 1, "8"), (64, 300, 3, "32")])
+def test_stream_pass_f_bitwise(ctx, orc, monkeypatch, d, n, c, rb):
+    """Pass F as row-block streams (k_pass_f_stream) forced with an explicit rows-
+    per-stream: a partial last row block (d % rb != 0 — its chunks past d are
+    skipped, not computed), several groups (member lists instead of consecutive
+    columns) and the smallest block — L, S, labels and iterations as the oracle's."""
+    from paper_1904_07497_b200 import synth
+    from paper_1904_07497_b200.respca import SolverConfig
+
+    monkeypatch.setenv("RESPCA_PASSF_STREAM", "1")
+    monkeypatch.setenv("RESPCA_STREAM_RB", rb)
+    X = synth.rpca(d, n, 3, 1.0, 0.08, seed=31 + d + c)
+    cfg = SolverConfig(c=c, tol=1e-6)
+    a = _solve(ctx, X, cfg)
+    b = orc.solve(X, cfg)
+    assert a.report.iters == b.iters
+    assert (a.assignment == b.labels).all()
+    assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
