@@ -52,19 +52,34 @@ RESPCA_DEV void cp_wait() {
 // ---------------------------------------------------------------------------
 // ‖c_k‖² for the screen (FMA chain; only ever used inside the bound)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_col_sq_fma(const double* __restrict__ C, int64_t d,
+__global__ void __launch_bounds__(1024) k_col_sq_fma(const double* __restrict__ C, int64_t d,
                                                     double* __restrict__ out,
                                                     const int* __restrict__ ver = nullptr,
                                                     int c = 0) {
     __shared__ double red[32];
     const int k = blockIdx.x;
     const double* ck = C + ((int64_t)(ver ? ver[k] : 0) * c + k) * d;
-    double s = 0.0;
-    for (int64_t i = threadIdx.x; i < d; i += blockDim.x) {
-        const double v = ck[i];
-        s = __fma_rn(v, v, s);
+    // eight loads in flight per thread (one L2 round trip per eight rows instead of one
+    // per row: C4, d = 76,800, c = 3: 47 µs → a few µs), four chains; any order is
+    // inside the bound that uses the value
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    for (int64_t i0 = threadIdx.x; i0 < d; i0 += 8 * (int64_t)blockDim.x) {
+        double v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int64_t i = i0 + u * (int64_t)blockDim.x;
+            v[u] = i < d ? __ldg(ck + i) : 0.0;
+        }
+        s0 = __fma_rn(v[0], v[0], s0);
+        s1 = __fma_rn(v[1], v[1], s1);
+        s2 = __fma_rn(v[2], v[2], s2);
+        s3 = __fma_rn(v[3], v[3], s3);
+        s0 = __fma_rn(v[4], v[4], s0);
+        s1 = __fma_rn(v[5], v[5], s1);
+        s2 = __fma_rn(v[6], v[6], s2);
+        s3 = __fma_rn(v[7], v[7], s3);
     }
-    double v[1] = {s};
+    double v[1] = {(s0 + s1) + (s2 + s3)};
     block_sum<1>(v, red);
     if (threadIdx.x == 0) out[k] = v[0];
 }

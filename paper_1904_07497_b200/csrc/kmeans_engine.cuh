@@ -172,7 +172,7 @@ struct KMeansEngine {
         const int cs = (int)sub.size();
         kmap.ensure(c);
         CK(cudaMemcpyAsync(kmap.p, sub.data(), sizeof(int) * cs, cudaMemcpyHostToDevice, st));
-        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p, nullptr, c);
+        k_col_sq_fma<<<c, 1024, 0, st>>>(C, d, cc.p, nullptr, c);
         // the split count of the full screen (the partial layout must not change)
         const int tiles = ceil_div(n, tile_j()) * ceil_div(c, tile_k());
         const int chunks = ceil_div(d, 32);
@@ -199,7 +199,7 @@ struct KMeansEngine {
     int scr_n = 0, scr_split = 1;
     // ver != nullptr: centroid k lives in slot ver[k] of a [2][c][d] store
     void screen_cols(const T* Mp, int nn, const double* C, const int* ver = nullptr) {
-        k_col_sq_fma<<<c, 256, 0, st>>>(C, d, cc.p, ver, c);
+        k_col_sq_fma<<<c, 1024, 0, st>>>(C, d, cc.p, ver, c);
         const int tiles = ceil_div(nn, tile_j()) * ceil_div(c, tile_k());
         const int chunks = ceil_div(d, 32);
         int ns = std::max(1, std::min(chunks / 4, ceil_div(2 * 148, tiles)));
