@@ -65,11 +65,12 @@ def test_solve_against_oracle_random(ctx, orc):
         assert bitwise(a.L, b.L) and bitwise(a.S, b.S)
 
 
-@pytest.mark.parametrize("d,n,c", [(200, 300, 10), (201, 300, 10), (151, 120, 1)])
+@pytest.mark.parametrize("d,n,c", [(200, 300, 10), (201, 300, 10), (202, 300, 10), (151, 120, 1), (152, 120, 1)])
 def test_fp32_mode_tolerance(ctx, orc, d, n, c):
     """fp32 storage: ≤1e-4 relative Frobenius error of L and S against the
-    fp64 reference on the same (f32-rounded) input (even d: Pass F with two rows
-    per thread; odd d and c = 1: one row per thread)."""
+    fp64 reference on the same (f32-rounded) input (d % 4 = 0: the four-row FP32
+    walk; d even: two rows per thread; odd d: one; c = 1 with d % 4 = 0: the
+    stream kernel on fp32 storage, with odd d the one-row ring)."""
     from paper_1904_07497_b200 import synth
     from paper_1904_07497_b200.respca import SolverConfig
 
